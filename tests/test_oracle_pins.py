@@ -1,0 +1,327 @@
+"""Pins for the CPU oracle (oracle/), each against something other than itself:
+brute force written independently here, closed forms, library routines,
+paper-printed values (tests/golden/), and invariants.  CPU only."""
+import json
+import math
+import os
+from fractions import Fraction
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from gen import Inputs, f32_to_bf16_bits
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _f(bits):
+    """bf16 bit patterns -> nested python floats (independent of oracle helpers)."""
+    a = np.asarray(bits).astype(np.uint32) << np.uint32(16)
+    return a.view(np.float32).astype(np.float64).tolist()
+
+
+# --------------------------------------------------------------------------
+# 1. Brute force per-token evaluation (plain Python, fp64) vs oracle exact mode
+# --------------------------------------------------------------------------
+
+def _brute_layer(x, wr, wg, wu, wd, k, norm, sg=None, su=None, sd=None):
+    T, H = len(x), len(x[0])
+    E, F = len(wg), len(wg[0])
+    ys = []
+    for t in range(T):
+        logit = [sum(x[t][h] * wr[e][h] for h in range(H)) for e in range(E)]
+        order = sorted(range(E), key=lambda e: (-logit[e], e))[:k]
+        mx = max(logit)
+        den = sum(math.exp(l - mx) for l in logit)
+        p = [math.exp(logit[e] - mx) / den for e in order]
+        if norm:
+            ssum = sum(p)
+            p = [v / ssum for v in p]
+        y = [0.0] * H
+        if sg is not None:
+            Fs = len(sg)
+            hs = []
+            for f in range(Fs):
+                g = sum(x[t][h] * sg[f][h] for h in range(H))
+                u = sum(x[t][h] * su[f][h] for h in range(H))
+                hs.append(g / (1 + math.exp(-g)) * u)
+            for h in range(H):
+                y[h] += sum(hs[f] * sd[h][f] for f in range(Fs))
+        for wj, e in zip(p, order):
+            hh = []
+            for f in range(F):
+                g = sum(x[t][h] * wg[e][f][h] for h in range(H))
+                u = sum(x[t][h] * wu[e][f][h] for h in range(H))
+                hh.append(g / (1 + math.exp(-g)) * u)
+            for h in range(H):
+                y[h] += wj * sum(hh[f] * wd[e][h][f] for f in range(F))
+        ys.append(y)
+    return np.array(ys)
+
+
+@pytest.mark.parametrize("norm,S", [(0, 1), (1, 0)])
+def test_oracle_exact_vs_brute_force(norm, S):
+    inp = Inputs(E=4, k=2, H=16, F=8, S=S, Fs=8, T=12, seed=7)
+    res = oracle.moe_layer(inp.x, inp.w_router, inp.w_gate, inp.w_up, inp.w_down, k=2,
+                           norm_topk=norm, ws_gate_bits=inp.ws_gate, ws_up_bits=inp.ws_up,
+                           ws_down_bits=inp.ws_down, mode="exact")
+    sh = (_f(inp.ws_gate), _f(inp.ws_up), _f(inp.ws_down)) if S else (None, None, None)
+    ref = _brute_layer(_f(inp.x), _f(inp.w_router), _f(inp.w_gate), _f(inp.w_up), _f(inp.w_down),
+                       2, norm, *sh)
+    assert np.max(np.abs(res["y"] - ref)) <= 1e-12 * max(1.0, np.max(np.abs(ref)))
+
+
+# --------------------------------------------------------------------------
+# 2. Special case E=1,k=1,S=0,D=1,norm=1: the layer IS a dense SwiGLU MLP
+# --------------------------------------------------------------------------
+
+def test_dense_mlp_special_case_vs_torch():
+    inp = Inputs(E=1, k=1, H=64, F=96, T=40, seed=11)
+    ex = oracle.moe_layer(inp.x, inp.w_router, inp.w_gate, inp.w_up, inp.w_down, k=1,
+                          norm_topk=1, mode="exact")
+    ct = oracle.moe_layer(inp.x, inp.w_router, inp.w_gate, inp.w_up, inp.w_down, k=1,
+                          norm_topk=1, mode="contract")
+    t = lambda b: torch.from_numpy(np.asarray(b).astype(np.int16)).view(torch.bfloat16).double()
+    x, wg, wu, wd = t(inp.x), t(inp.w_gate[0]), t(inp.w_up[0]), t(inp.w_down[0])
+    ref = (torch.nn.functional.silu(x @ wg.T) * (x @ wu.T)) @ wd.T
+    ref = ref.numpy()
+    assert np.allclose(ex["y"], ref, rtol=0, atol=1e-12 * np.abs(ref).max())
+    # contract mode: bf16 roundings at h, o, y only -> within the bf16 band
+    err = np.abs(ct["y"].astype(np.float64) - ref)
+    assert err.max() <= 1e-2 * np.abs(ref).max()
+    assert err.sum() / np.abs(ref).sum() <= 6e-3
+    # and torch's own bf16 pipeline (RNE casts at h, o) agrees with contract o
+    h = (torch.nn.functional.silu((x @ wg.T).float()) * (x @ wu.T).float()).bfloat16()
+    o = (h.double() @ wd.T).float().bfloat16().float().numpy()
+    assert np.array_equal(o, ct["y"])  # w == 1 and s == 0: y == bf16(fmaf(1, o, 0)) == o
+
+
+# --------------------------------------------------------------------------
+# 3. rounding helpers vs library routines / exact rationals
+# --------------------------------------------------------------------------
+
+def test_round_bf16_matches_torch():
+    rng = np.random.default_rng(0)
+    v = np.concatenate([rng.standard_normal(100000).astype(np.float32) * 10,
+                        np.array([1.00390625, 1.01171875, -1.00390625, 3.0e-30, 65504.0], np.float32)])
+    ref = torch.from_numpy(v).bfloat16().float().numpy()
+    assert np.array_equal(oracle.round_bf16(v), ref)
+
+
+def test_fmaf_correctly_rounded():
+    rng = np.random.default_rng(1)
+    n = 4000
+    a = rng.standard_normal(n).astype(np.float32)
+    b = oracle.round_bf16(rng.standard_normal(n).astype(np.float32))
+    c = (rng.standard_normal(n) * np.exp2(rng.integers(-30, 30, n))).astype(np.float32)
+    # crafted double-rounding cases: a*b + c lands a hair off an fp32 midpoint
+    a[:4] = np.float32(1.0)
+    b[:4] = np.float32(2.0 ** -24)       # half an fp32 ulp of 1.0 ...
+    c[:4] = np.float32(1.0)
+    a[4:8] = np.float32(1.0 + 2.0 ** -23)
+    b[4:8] = np.float32(2.0 ** -24)      # ... plus a tail below fp64 precision
+    c[4:8] = np.float32(1.0)
+    got = oracle.fmaf(a, b, c)
+    for i in range(n):
+        ex = Fraction(float(a[i])) * Fraction(float(b[i])) + Fraction(float(c[i]))
+        lo = np.float32(float(ex))
+        # correctly rounded fp32: nearest, ties to even -- check via exact rationals
+        cands = [lo, np.nextafter(lo, np.float32(np.inf)), np.nextafter(lo, np.float32(-np.inf))]
+        best = min(cands, key=lambda q: (abs(Fraction(float(q)) - ex),
+                                         int(np.array([q], np.float32).view(np.uint32)[0]) & 1))
+        assert got[i] == best, (i, a[i], b[i], c[i], got[i], best)
+
+
+# --------------------------------------------------------------------------
+# 4. Routing: exact-logit grid, ties, k = E, activated-experts formula
+# --------------------------------------------------------------------------
+
+@pytest.mark.parametrize("E,H", [(160, 512), (64, 2048), (8, 4096), (8, 64)])
+def test_grid_logits_exact(E, H):
+    inp = Inputs(E=E, k=2, H=H, F=64, T=32, seed=3, grid=True)
+    l32 = oracle.router_logits(inp.x, inp.w_router)
+    l64 = oracle.router_logits(inp.x, inp.w_router, mode="exact")
+    # every fp64 sum is representable in fp32 (multiples of 2^-9, |sum| < 2^13)
+    assert np.array_equal(l32.astype(np.float64), l64)
+    # and independent of summation order (reverse order, python floats)
+    xf, wf = _f(inp.x), _f(inp.w_router)
+    for t in range(0, 32, 7):
+        for e in range(0, E, max(1, E // 5)):
+            s = 0.0
+            for h in reversed(range(H)):
+                s += xf[t][h] * wf[e][h]
+            assert s == l64[t, e]
+
+
+def test_routing_vs_stable_argsort_and_ties():
+    inp = Inputs(E=16, k=4, H=128, F=64, T=300, seed=5, grid=True)
+    inp.duplicate_router_rows(3, 9)           # tie fixture: e3 and e9 always tie
+    logits = oracle.router_logits(inp.x, inp.w_router)
+    idx, w = oracle.topk_gating(logits, 4, norm_topk=0)
+    for t in range(300):
+        order = sorted(range(16), key=lambda e: (-float(logits[t, e]), e))
+        assert list(idx[t]) == order[:4]
+        if 9 in idx[t]:
+            assert 3 in idx[t] and list(idx[t]).index(3) < list(idx[t]).index(9)
+    # grid inputs produce real k-th/(k+1)-th ties beyond the fixture
+    srt = -np.sort(-logits, axis=1)
+    assert np.any(srt[:, 3] == srt[:, 4])
+
+
+def test_softmax_weights_brute_force():
+    inp = Inputs(E=8, k=2, H=64, F=64, T=50, seed=9)
+    logits = oracle.router_logits(inp.x, inp.w_router)
+    for norm in (0, 1):
+        idx, w = oracle.topk_gating(logits, 2, norm_topk=norm, routed_scale=1.0)
+        for t in range(50):
+            l = [float(v) for v in logits[t]]
+            z = sum(math.exp(v) for v in l)
+            p = [math.exp(l[e]) / z for e in idx[t]]
+            if norm:
+                p = [v / sum(p) for v in p]
+            assert np.allclose(w[t], p, rtol=1e-6, atol=0)
+
+
+def test_k_equals_E_routes_every_token_everywhere():
+    inp = Inputs(E=4, k=4, H=32, F=32, T=20, seed=2)
+    res = oracle.moe_layer(inp.x, inp.w_router, inp.w_gate, inp.w_up, inp.w_down, k=4,
+                           norm_topk=1, D=2, N=2)
+    assert np.array_equal(res["layout"]["hist"], np.full((2, 4), 10))
+    assert np.allclose(res["w"].sum(axis=1), 1.0, atol=1e-6)
+
+
+def test_activated_experts_formula():
+    # P:133 (A2): E(1-(1-k/E)^m) experts touched by m tokens; closed-form example
+    assert abs(oracle.activated_experts(16, 2, 8) - 10.502) < 1e-3
+    assert abs(oracle.activated_experts(160, 6, 10 ** 6) - 160) < 1e-9
+    # statistical pin of the routing on the performance distribution
+    E, k, m = 64, 6, 8
+    inp = Inputs(E=E, k=k, H=256, F=64, T=4000, seed=13)
+    idx, _ = oracle.topk_gating(oracle.router_logits(inp.x, inp.w_router), k, 0)
+    distinct = [len(np.unique(idx[i:i + m])) for i in range(0, 4000, m)]
+    assert abs(np.mean(distinct) - oracle.activated_experts(E, k, m)) < 0.06 * oracle.activated_experts(E, k, m)
+
+
+# --------------------------------------------------------------------------
+# 5. The paper's worked example, fig:eps_overview
+# --------------------------------------------------------------------------
+
+def test_fig_eps_overview_fixture():
+    fx = json.load(open(os.path.join(GOLDEN, "fig_eps_overview.json")))
+    E, k, D, N = fx["E"], fx["k"], fx["D"], fx["N"]
+    idx = np.array(fx["routing"], np.int32)
+    w = np.array(fx["weights"], np.float32)
+    # printed: Expert0 takes [0,1,5,9], Expert1 takes [0,2,5,6]
+    for e, toks in fx["paper_printed"]["expert_tokens"].items():
+        assert sorted(np.nonzero((idx == int(e)).any(axis=1))[0].tolist()) == toks
+    inp = Inputs(E=E, k=k, H=16, F=16, T=10, seed=1)
+    res = oracle.moe_layer(inp.x, inp.w_router, inp.w_gate, inp.w_up, inp.w_down, k=k,
+                           norm_topk=0, D=D, N=N, topk_override=(idx, w))
+    lay = res["layout"]
+    send = res["send_counts"]
+    for tr in fx["paper_printed"]["chunk0_transfers"]:
+        assert send[0, tr["src"], tr["dst"]] == len(tr["tokens"])
+        # the rows src sends dst in chunk 0 are exactly those tokens, in order
+        src, e = tr["src"], tr["expert"]
+        p = lay["pos"][src]
+        start = lay["token_start"][src]
+        loc = idx[start:start + p.shape[0]]
+        tok, slot = np.nonzero(loc == e)
+        order = np.argsort(p[tok, slot])
+        assert (tok[order] + start).tolist() == tr["tokens"]
+    # chunk 0 on rank 0 computes expert 0 over tokens [0,1,5,9] (recv order src, t)
+    assert lay["recv_start"][0, 0].tolist() == [0, 2]
+    assert lay["hist"].tolist() == [[2, 2, 2, 2, 1, 1], [2, 2, 1, 1, 2, 2]]
+    assert res["group_begin"].tolist() == [0, 1, 2, 3]
+    # pos is the (e, t) stable order on rank 0 (R6)
+    assert lay["pos"][0].tolist() == [[0, 2], [1, 6], [3, 4], [7, 8], [5, 9]]
+
+
+# --------------------------------------------------------------------------
+# 6. Conservation, chunked == unchunked, EP=D == EP=1 (bit-exact, contract)
+# --------------------------------------------------------------------------
+
+def _tiny(seed=21, T=60):
+    return Inputs(E=8, k=2, H=32, F=64, S=1, Fs=32, T=T, seed=seed)
+
+
+def test_conservation_and_counts():
+    inp = _tiny()
+    for D in (1, 2, 4):
+        for N in range(1, 8 // D + 1):
+            res = oracle.moe_layer(inp.x, inp.w_router, inp.w_gate, inp.w_up, inp.w_down, k=2,
+                                   norm_topk=1, ws_gate_bits=inp.ws_gate, ws_up_bits=inp.ws_up,
+                                   ws_down_bits=inp.ws_down, D=D, N=N)
+            lay, send = res["layout"], res["send_counts"]
+            T_loc = np.diff(lay["token_start"])
+            assert np.array_equal(lay["hist"].sum(axis=1), T_loc * 2)
+            for r in range(D):            # every (t, j) goes out and returns exactly once
+                assert sorted(lay["pos"][r].ravel().tolist()) == list(range(T_loc[r] * 2))
+            assert send.sum() == 60 * 2
+            for d in range(D):
+                assert send[:, :, d].sum() == lay["recv_total"][d]
+                E_loc = 8 // D
+                assert lay["recv_total"][d] == lay["hist"][:, d * E_loc:(d + 1) * E_loc].sum()
+
+
+def test_chunked_equals_unchunked_and_ep_invariance():
+    inp = _tiny(T=64)
+    args = (inp.x, inp.w_router, inp.w_gate, inp.w_up, inp.w_down)
+    kw = dict(k=2, norm_topk=0, ws_gate_bits=inp.ws_gate, ws_up_bits=inp.ws_up, ws_down_bits=inp.ws_down)
+    base = oracle.moe_layer(*args, D=1, N=1, **kw)["y"]
+    for D, N, S in [(1, 3, 1), (1, 8, 1), (2, 2, 1), (2, 1, 3), (4, 2, 2), (8, 1, 2)]:
+        y = oracle.moe_layer(*args, D=D, N=N, token_slices=S, **kw)["y"]
+        assert np.array_equal(y, base), (D, N, S)
+
+
+def test_contract_vs_exact_band():
+    inp = Inputs(E=8, k=2, H=256, F=192, S=1, Fs=128, T=64, seed=4)
+    args = (inp.x, inp.w_router, inp.w_gate, inp.w_up, inp.w_down)
+    kw = dict(k=2, norm_topk=1, ws_gate_bits=inp.ws_gate, ws_up_bits=inp.ws_up, ws_down_bits=inp.ws_down)
+    ex = oracle.moe_layer(*args, mode="exact", **kw)
+    ct = oracle.moe_layer(*args, mode="contract", **kw)
+    assert np.array_equal(ex["idx"], ct["idx"])
+    rel = np.abs(ct["y"] - ex["y"]).sum() / np.abs(ex["y"]).sum()
+    assert 3e-4 < rel < 6e-3          # three bf16 rounding points (R4)
+    # y values are bf16-representable
+    assert np.array_equal(oracle.round_bf16(ct["y"]), ct["y"])
+
+
+def test_moe_tokens_matches_moe_layer_subset():
+    inp = _tiny(T=40)
+    full = oracle.moe_layer(inp.x, inp.w_router, inp.w_gate, inp.w_up, inp.w_down, k=2, norm_topk=1,
+                            ws_gate_bits=inp.ws_gate, ws_up_bits=inp.ws_up, ws_down_bits=inp.ws_down)
+    sub = [3, 17, 39]
+    r = oracle.moe_tokens(inp.x[sub], inp.w_router,
+                          lambda e: (inp.w_gate[e], inp.w_up[e], inp.w_down[e]), 2, 1,
+                          shared=(inp.ws_gate, inp.ws_up, inp.ws_down))
+    assert np.array_equal(r["y"], full["y"][sub])
+
+
+# --------------------------------------------------------------------------
+# 7. Pipeline-number rule: closed form vs grid argmax
+# --------------------------------------------------------------------------
+
+def test_pn_closed_form_example():
+    n, v = oracle.pn_optimum_grid(t_comm=10.0, t_comp=12.0, k=0.1, b=0.5, e_loc=20)
+    assert n == 10
+    assert abs(oracle.pn_gain(10, 10.0, 12.0, 0.1, 0.5) - 7.5) < 1e-12
+    assert abs(oracle.pn_gain(10, 10.0, 12.0, 0.1, 0.5) - (10 - 0.5 - 2 * math.sqrt(0.1 * 10))) < 1e-12
+    assert oracle.pn_optimum_closed_form(10.0, 12.0, 0.1) == pytest.approx(10.0)
+
+
+def test_pn_grid_within_one_of_closed_form():
+    rng = np.random.default_rng(3)
+    for _ in range(200):
+        tc, tp = rng.uniform(0.1, 10, 2)
+        k, b = rng.uniform(0.001, 0.5), rng.uniform(0, 1)
+        e_loc = int(rng.integers(1, 64))
+        n, _ = oracle.pn_optimum_grid(tc, tp, k, b, e_loc)
+        nstar = min(max(oracle.pn_optimum_closed_form(tc, tp, k), 1), e_loc)
+        assert abs(n - nstar) <= 1.0 + 1e-9
+    # k = 0: more pipelines always better -> N = E
+    assert oracle.pn_optimum_grid(3.0, 5.0, 0.0, 0.2, 20)[0] == 20
+    # small C (few tokens) -> no gain from pipelining -> N = 1
+    assert oracle.pn_optimum_grid(0.01, 0.01, 0.05, 0.0, 20)[0] == 1
