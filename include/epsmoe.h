@@ -1,0 +1,236 @@
+/*
+ * epsmoe.h — C ABI of the B200 (sm_100a) EPS-MoE layer: the expert-parallel
+ * MoE FFN layer in prefill with the paper's expert pipeline scheduler.
+ *
+ * Paper: "EPS-MoE: Expert Pipeline Scheduler for Cost-Efficient MoE
+ * Inference", arXiv 2410.12247.  P:n = line n of its LaTeX.
+ *
+ * The arguments follow Algorithm 1's problem statement:
+ *   m (tokens), k / n (MoE input / output dim = hidden / ffn), ep, topk,
+ *   e (experts), PN (pipeline number); plus shared experts.
+ * What one call computes (the plain MoE layer):
+ *   y_t = FFN_shared(x_t) + sum_{j<topk} w_{t,j} FFN_{e_{t,j}}(x_t),
+ *   FFN_e(x) = (silu(x W_gate,e^T) * (x W_up,e^T)) W_down,e^T,
+ * with (e_{t,.}, w_{t,.}) = topKGating(Router(x_t)), executed as
+ * Algorithm 1: split -> per chunk {All2All dispatch, ComputeMoE,
+ * All2All combine} -> weighted LocalReduce on the token's home rank.
+ *
+ * Conventions
+ *  - Every call returns moe_status_t (0 = MOE_OK).  No C++ exception crosses
+ *    the ABI.  On error, moe_last_error() returns a thread-local message.
+ *  - Device pointers are CUDA device addresses; "host" pointers are plain CPU
+ *    memory (pinned for the *_host entry points' best throughput).
+ *  - Matrices are row-major bf16 unless stated otherwise, with the reduction
+ *    (K) dimension contiguous ("K-major").
+ *  - cudaStream_t / ncclUniqueId are passed as void* / 128-byte buffers so the
+ *    header needs neither cuda_runtime.h nor nccl.h.
+ */
+#ifndef EPSMOE_H_
+#define EPSMOE_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  MOE_OK = 0,
+  MOE_ERR_INVALID = 1,     /* bad argument / unsupported shape                 */
+  MOE_ERR_UNSUPPORTED = 2, /* valid but not implemented on this build          */
+  MOE_ERR_CAPACITY = 3,    /* T_loc > max_tokens, or workspace too small       */
+  MOE_ERR_CUDA = 4,        /* a CUDA runtime / driver call failed              */
+  MOE_ERR_NCCL = 5,        /* an NCCL call failed; the handle must be destroyed */
+  MOE_ERR_MISMATCH = 6     /* ranks disagree on the configuration              */
+} moe_status_t;
+
+#define MOE_MAX_EXPERTS 256     /* e  <= 256 (router tile width)                 */
+#define MOE_MAX_TOPK 8          /* topk <= 8                                     */
+#define MOE_MAX_CHUNKS 64       /* PN <= 64                                      */
+#define MOE_MAX_HIDDEN 8192     /* k (hidden) <= 8192                            */
+
+typedef struct moe_layer moe_layer_t; /* opaque, library-owned */
+
+/* Layer shape (Algorithm 1 "Data").  Identical on every rank
+ * except `rank`.  Constraints: num_experts % ep == 0 (R12), hidden and ffn
+ * multiples of 64 (hidden a multiple of 32 bf16 per output chunk), ffn and
+ * num_shared*shared_ffn multiples of 128, 1 <= top_k <= min(8, num_experts). */
+typedef struct {
+  int32_t num_experts;  /* e: routed experts (global) */
+  int32_t top_k;        /* topk */
+  int32_t hidden;       /* k: MoE input dim = output dim of DownGemm */
+  int32_t ffn;          /* n: output dim of Gate/Up GEMMs per expert */
+  int32_t num_shared;   /* shared experts, fused into one MLP (R10) */
+  int32_t shared_ffn;   /* width of each shared expert                        */
+  int32_t ep;           /* ep: expert-parallel degree = ranks */
+  int32_t rank;         /* this rank, 0 <= rank < ep                          */
+  int64_t max_tokens;   /* capacity: largest T_loc per forward (sizes workspace) */
+  int32_t norm_topk;    /* 1: renormalise the top-k weights (Mixtral); 0: raw
+                           softmax probabilities (DeepSeek)             (R1)  */
+  float routed_scale;   /* multiplies routed weights (1.0)                    */
+} moe_config_t;
+
+/* Caller-owned device weights (bf16, K-major), valid for the layer's life.
+ * Routed experts: only this rank's E_loc = e/ep experts, global ids
+ * [rank*E_loc, (rank+1)*E_loc) (EP).  Router + shared experts are
+ * replicated on every rank (DP). */
+typedef struct {
+  const void* w_router;     /* [e, k]                                       */
+  const void* w_gate;       /* [E_loc, n, k]                                */
+  const void* w_up;         /* [E_loc, n, k]                                */
+  const void* w_down;       /* [E_loc, k, n]                                */
+  const void* ws_gate;      /* [S*F_s, k] or NULL if num_shared == 0        */
+  const void* ws_up;        /* [S*F_s, k]                                   */
+  const void* ws_down;      /* [k, S*F_s]                                   */
+  const float* router_bias; /* [e] fp32 device or NULL: added to the fp32
+                               logits (synthetic skew hook)  */
+} moe_weights_t;
+
+/* GEMM kind per expert: GroupGemm vs DenseGemm. */
+typedef enum {
+  MOE_GEMM_AUTO = 0,    /* per-expert choice from the measured cost model (A8) */
+  MOE_GEMM_GROUPED = 1, /* one persistent launch over every tile of a chunk    */
+  MOE_GEMM_DENSE = 2    /* one persistent launch per expert, experts in turn   */
+} moe_gemm_kind_t;
+
+/* Output of the expert pipeline scheduler (Algorithm 1's PN). */
+typedef struct {
+  int32_t num_chunks;   /* PN, 1 <= PN <= E_loc * token_slices */
+  int32_t token_slices; /* 1 = paper (chunks are expert groups, R8)               */
+  int32_t gemm_kind;    /* moe_gemm_kind_t applied to all experts (AUTO: see below) */
+  int32_t sm_gemm;      /* persistent GEMM grid (0 = all SMs)           P:492, A15 */
+  int32_t comm_ctas;    /* NCCL maxCTAs per communicator (0 = default) */
+  int32_t group_begin[MOE_MAX_CHUNKS + 1]; /* local-expert group bounds (R8)     */
+  uint8_t expert_kind[MOE_MAX_EXPERTS];    /* resolved kind per local expert      */
+  float pred_comm_ms;   /* T_comm before splitting    */
+  float pred_comp_ms;   /* T_comp before splitting    */
+  float pred_k_ms;      /* R(N) = kN + b: slope    */
+  float pred_b_ms;      /*                 intercept                              */
+  float pred_gain_ms;   /* G = C - b - (C/N + kN)    */
+} moe_plan_t;
+
+/* Measured cost model behind moe_plan_pipeline (calibrated on B200 by
+ * moe_layer_calibrate, or supplied by the caller).  GEMM time of one expert
+ * with m rows is linear-interpolated in m from `m_points`; all2all time is
+ * a2a_fixed_ms + bytes / a2a_gbps; per-chunk overhead R(N) = k*N + b. */
+#define MOE_COST_POINTS 12
+typedef struct {
+  int32_t n_points;
+  float m_points[MOE_COST_POINTS];          /* rows per expert, ascending       */
+  float gemm_ms[2][MOE_COST_POINTS];        /* [0] GROUPED, [1] DENSE: ms per
+                                               expert (GateUp+Down) at m       */
+  float a2a_fixed_ms;                       /* latency term of one all2all     */
+  float a2a_gbps;                           /* effective per-rank GB/s         */
+  float k_ms;                               /* R(N) slope         */
+  float b_ms;                               /* R(N) intercept         */
+} moe_cost_model_t;
+
+/* Debug / test hooks (NULL in benchmarks).  All array pointers are DEVICE
+ * pointers sized for T_loc; any may be NULL. */
+typedef struct {
+  int32_t override_routing; /* 1: topk_idx / topk_w below are INPUTS (explicit
+                               routing, e.g. the fig:eps_overview fixture)   */
+  float* logits;            /* out [T_loc, e] fp32                            */
+  int32_t* topk_idx;        /* out/in [T_loc, topk]                           */
+  float* topk_w;            /* out/in [T_loc, topk]                           */
+  int32_t* pos;             /* out [T_loc, topk]: send row of pair (t, j)     */
+  int32_t* hist;            /* out [e]: this rank's pairs per expert          */
+  int32_t* seg_start;       /* out [e+1]: send-layout expert offsets (R6)     */
+  void* shared_out;         /* out [T_loc, k] bf16: shared-expert output s    */
+  int32_t* global_hist_host;/* out HOST [ep, e]                               */
+  moe_plan_t* plan_used;    /* out HOST: the plan the forward executed        */
+} moe_debug_t;
+
+/* ---------------------------------------------------------------- lifecycle */
+
+/* Bytes of device workspace moe_layer_create needs for `cfg` (worst case:
+ * every routed row of every rank lands on this rank, so no reallocation is
+ * ever needed). */
+size_t moe_layer_workspace_bytes(const moe_config_t* cfg);
+
+/* Write a fresh ncclUniqueId (128 bytes) to `out` (host).  Rank 0 calls it
+ * twice (dispatch and combine communicators) and broadcasts the bytes. */
+moe_status_t moe_get_unique_id(void* out128);
+
+/* Create the layer.  Collective over the `ep` ranks when ep > 1 (builds two
+ * NCCL communicators from the two 128-byte ids; NULL allowed when ep == 1).
+ * `workspace` (device, >= moe_layer_workspace_bytes) is caller-owned and
+ * must outlive the layer.  The layer keeps the weight pointers, not copies
+ * (except a zero-padded copy of the router).  Must be called with the target
+ * device current.  On success *out is the new handle. */
+moe_status_t moe_layer_create(const moe_config_t* cfg, const moe_weights_t* w,
+                              const void* nccl_uid_dispatch, const void* nccl_uid_combine,
+                              void* workspace, size_t workspace_bytes, moe_layer_t** out);
+
+moe_status_t moe_layer_destroy(moe_layer_t* layer);
+
+/* ------------------------------------------------------------------ planner */
+
+/* Pure, host-only, deterministic: the expert pipeline scheduler.
+ *   N = argmax_{1<=N<=E_loc} min(T_comm, T_comp)(N-1)/N - (kN + b)  (P:408-415,
+ *       ties -> smaller N), T_comm / T_comp from the cost model for the
+ *       max-loaded rank;
+ *   kind_e = argmin over {GROUPED, DENSE} of the modelled expert time (A8);
+ *   group_begin = balanced contiguous expert groups (R8).
+ * `global_hist` is HOST [ep, e] (pairs per rank and expert) or NULL for
+ * uniform routing (mm = m*topk/e, CalcPN P:540-552).  `global_tokens` = m.
+ * No GPU needed: usable from CPU-only tests. */
+moe_status_t moe_plan_compute(const moe_config_t* cfg, const moe_cost_model_t* cost,
+                              int64_t global_tokens, const int32_t* global_hist, moe_plan_t* out);
+
+/* moe_plan_compute with the layer's calibrated cost model. */
+moe_status_t moe_plan_pipeline(const moe_layer_t* layer, int64_t global_tokens,
+                               const int32_t* global_hist, moe_plan_t* out);
+
+/* Measure the B200 cost model (GEMM time vs rows per expert for both kinds;
+ * all2all time vs bytes and chunk count when ep > 1) and install it in the
+ * layer.  Collective when ep > 1.  Optional; without it a built-in model
+ * is used.  `out` (host, may be NULL) receives the model. */
+moe_status_t moe_layer_calibrate(moe_layer_t* layer, void* stream, moe_cost_model_t* out);
+moe_status_t moe_layer_set_cost_model(moe_layer_t* layer, const moe_cost_model_t* cost);
+
+/* ------------------------------------------------------------------ forward */
+
+/* One MoE layer forward (Algorithm 1).  Collective when ep > 1
+ * (same call order on every rank; T_loc may differ per rank).
+ *   x: DEVICE [T_loc, k] bf16, must stay valid until `stream` reaches the
+ *      end of this call; y: DEVICE [T_loc, k] bf16, written stream-ordered.
+ *   plan: NULL = moe_plan_pipeline on the realised global histogram.
+ *   stream: cudaStream_t (NULL = legacy default stream).
+ * ep == 1: no host synchronisation (CUDA-graph capturable when plan != NULL
+ * and dbg == NULL).  ep > 1: one device->host wait for the histogram
+ * allgather per call (hidden behind the shared-expert GEMMs). */
+moe_status_t moe_layer_forward(moe_layer_t* layer, const void* x, int64_t T_loc, void* y,
+                               const moe_plan_t* plan, void* stream, moe_debug_t* dbg);
+
+/* moe_layer_forward on HOST buffers: copies x host->device, runs the layer,
+ * copies y device->host, all on `stream`, and returns when y_host is ready.
+ * x_host / y_host: [T_loc, k] bf16 (pinned memory recommended). */
+moe_status_t moe_layer_forward_host(moe_layer_t* layer, const void* x_host, int64_t T_loc, void* y_host,
+                                    const moe_plan_t* plan, void* stream);
+
+/* Number of kernels the last forward launched (for the bench's gpu_launches). */
+int32_t moe_layer_last_launches(const moe_layer_t* layer);
+
+/* Thread-local message of the last error ("" if none). */
+const char* moe_last_error(void);
+
+/* --------------------------------------------------------- test / calibration */
+
+/* One grouped GEMM of the layer's kernel family on caller buffers (device):
+ *   epi 0 (GateUp+Silu): out[r, 0:n] = bf16(silu(A_r B0_g^T) * (A_r B1_g^T))
+ *   epi 1 (Down):        out[r, 0:n] = bf16(A_r B0_g^T)
+ *   epi 2 (fp32):        out[r, 0:n] = fp32(A_r B0_g^T) (+ bias)
+ * for rows r of group g in [row_start[g], row_start[g] + row_count[g]),
+ * B*_g = rows [g*b_group_rows, g*b_group_rows + n) (epi 0/1) of B0/B1 [.., kdim].
+ * row_start/row_count: DEVICE int32 [groups].  num_ctas: persistent grid. */
+moe_status_t moe_gemm_grouped(int32_t epi, const void* A, int64_t a_rows, const void* B0, const void* B1,
+                              int64_t b_rows, int32_t b_group_rows, int32_t kdim, int32_t n, void* out,
+                              int64_t ldo, const float* bias, int32_t groups, const int32_t* row_start,
+                              const int32_t* row_count, int32_t num_ctas, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* EPSMOE_H_ */

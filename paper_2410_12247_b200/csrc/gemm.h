@@ -1,0 +1,42 @@
+// Internal interface of the tcgen05 grouped / dense GEMM (gemm_sm100.cu).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace epsmoe {
+
+enum EpiKind : int {
+  EPI_SWIGLU = 0,  // acc = [gate(128) | up(128)] -> h = bf16(silu(g) * u)   (GateUpGemm+SiluAct)
+  EPI_BF16 = 1,    // acc -> bf16                                             (DownGemm)
+  EPI_F32 = 2,     // acc (+ bias[col]) -> fp32                               (Router)
+};
+
+// One grouped GEMM launch: for each group g (an expert), rows
+// [row_start[g], row_start[g] + row_count[g]) of A (K-major, [rows, K] bf16)
+// times B_g^T where B_g = rows [(b_base + g) * b_group_rows, ...) of B
+// ([*, K] bf16, K-major).  Output rows are the same rows of `out`.
+struct GemmArgs {
+  int epi;                 // EpiKind
+  const void* A;           // [a_rows, K] bf16
+  int64_t a_rows;          // allocated rows of A (TMA bound)
+  const void* B0;          // [b_rows, K] bf16 (gate for SWIGLU)
+  const void* B1;          // [b_rows, K] bf16 (up for SWIGLU) or nullptr
+  int64_t b_rows;          // allocated rows of B0/B1
+  int b_group_rows;        // rows of B per group (F for gate/up, H for down, 0 = shared)
+  int b_base;              // first group's index into B
+  int K;                   // reduction length (multiple of 64)
+  int N;                   // logical output columns (F for SWIGLU)
+  void* out;               // bf16 or fp32
+  int64_t ldo;             // output row pitch in elements
+  const float* bias;       // EPI_F32 only, [N] or nullptr
+  int G;                   // groups (<= 256)
+  const int32_t* row_start;  // device [G] (nullptr -> single group at row 0)
+  const int32_t* row_count;  // device [G] (nullptr -> single group of m_single rows)
+  int m_single;
+  int num_ctas;            // persistent grid size (SM budget)
+};
+
+// Launch on `stream`.  Returns a cudaError_t-compatible code (0 = success).
+int gemm_launch(const GemmArgs& a, cudaStream_t stream);
+
+}  // namespace epsmoe

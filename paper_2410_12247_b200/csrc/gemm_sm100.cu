@@ -1,0 +1,365 @@
+// Expert FFN GEMMs on 5th-gen tensor cores (sm_100a): persistent, warp-
+// specialised, TMA -> 4-stage smem ring -> tcgen05.mma (M=128, N=256, K=16,
+// bf16 in / fp32 accumulate in TMEM) -> double-buffered TMEM accumulators ->
+// fused epilogue.  One kernel family serves every GEMM of the layer:
+//
+//   GateUpGemm + SiluAct  EPI_SWIGLU: B tile = 128 rows of W_gate
+//        and 128 rows of W_up of the same expert (two TMA loads, no weight
+//        repacking); epilogue h = bf16(silu(g) * u).
+//   DownGemm                  EPI_BF16:  o = bf16(acc).
+//   Router                    EPI_F32:   logits = fp32(acc) + beta.
+//
+// "GroupGemm" vs "DenseGemm" is a scheduling choice on B200:
+// one launch over all tiles of a chunk's experts vs one launch per expert; the
+// kernel is the same (see layer.cu).  Group row counts are read from device
+// memory, so no host round trip is needed to size the launch (persistent grid).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <mutex>
+
+#include "gemm.h"
+#include "ptx.cuh"
+
+namespace epsmoe {
+namespace {
+
+constexpr int BM = 128, BN = 256, BK = 64, STAGES = 4;
+constexpr int A_BYTES = BM * BK * 2;  // 16 KB
+constexpr int B_BYTES = BN * BK * 2;  // 32 KB
+constexpr int MAX_G = 256;
+constexpr int NUM_THREADS = 192;      // w0 TMA, w1 MMA + TMEM owner, w2..5 epilogue
+constexpr int TMEM_COLS = 512;        // 2 x 256-column fp32 accumulators
+
+struct KParams {
+  int epi, K, N, G, m_single, b_group_rows, b_base;
+  int64_t ldo;
+  void* out;
+  const float* bias;
+  const int32_t* row_start;
+  const int32_t* row_count;
+};
+
+struct __align__(8) SmemTail {
+  uint64_t full[STAGES];
+  uint64_t empty[STAGES];
+  uint64_t tfull[2];
+  uint64_t tempty[2];
+  uint32_t tmem_holder;
+  int32_t tile_prefix[MAX_G + 1];
+  int32_t gstart[MAX_G];
+  int32_t gcount[MAX_G];
+};
+
+constexpr size_t SMEM_BYTES = 1024 /*align slack*/ + STAGES * (A_BYTES + B_BYTES) + sizeof(SmemTail);
+
+__device__ __forceinline__ float silu_f32(float g) { return g / (1.0f + expf(-g)); }
+
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+
+__device__ __forceinline__ void decode_tile(const SmemTail& s, int G, int n_tiles, int t, int& g,
+                                            int& mt, int& nt) {
+  int lo = 0, hi = G - 1;  // largest g with tile_prefix[g] <= t
+  while (lo < hi) {
+    int mid = (lo + hi + 1) >> 1;
+    if (s.tile_prefix[mid] <= t) lo = mid; else hi = mid - 1;
+  }
+  g = lo;
+  int local = t - s.tile_prefix[g];
+  mt = local / n_tiles;
+  nt = local - mt * n_tiles;
+}
+
+template <int EPI>
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB0,
+            const __grid_constant__ CUtensorMap tmB1, const KParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * A_BYTES;
+  SmemTail& st = *reinterpret_cast<SmemTail*>(smem + STAGES * (A_BYTES + B_BYTES));
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int G = p.row_count ? p.G : 1;
+  const int n_out_tile = (EPI == EPI_SWIGLU) ? 128 : BN;     // output columns per tile
+  const int n_tiles = (p.N + n_out_tile - 1) / n_out_tile;
+  const int num_kb = p.K / BK;
+
+  // ---- group table: start rows, counts, tile prefix (warp-parallel scan)
+  for (int g = threadIdx.x; g < G; g += NUM_THREADS) {
+    st.gcount[g] = p.row_count ? p.row_count[g] : p.m_single;
+    st.gstart[g] = p.row_start ? p.row_start[g] : 0;
+  }
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < STAGES; ++i) {
+      ptx::mbar_init(ptx::smem_u32(&st.full[i]), 1);
+      ptx::mbar_init(ptx::smem_u32(&st.empty[i]), 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      ptx::mbar_init(ptx::smem_u32(&st.tfull[i]), 1);
+      ptx::mbar_init(ptx::smem_u32(&st.tempty[i]), 128);
+    }
+    ptx::fence_barrier_init();
+  }
+  if (warp == 1) ptx::tmem_alloc<TMEM_COLS>(ptx::smem_u32(&st.tmem_holder));
+  if (warp == 0 && lane == 0) {
+    ptx::tma_prefetch_desc(&tmA);
+    ptx::tma_prefetch_desc(&tmB0);
+    if (EPI == EPI_SWIGLU) ptx::tma_prefetch_desc(&tmB1);
+  }
+  __syncthreads();
+  if (warp == 0) {
+    constexpr int PER = (MAX_G + 31) / 32;
+    int local[PER];
+    int sum = 0;
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+      int g = lane * PER + i;
+      int tiles = (g < G) ? ((st.gcount[g] + BM - 1) / BM) * n_tiles : 0;
+      local[i] = sum;
+      sum += tiles;
+    }
+    int incl = sum;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      int v = __shfl_up_sync(0xffffffffu, incl, off);
+      if (lane >= off) incl += v;
+    }
+    int excl = incl - sum;
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+      int g = lane * PER + i;
+      if (g < G) st.tile_prefix[g] = excl + local[i];
+    }
+    if (lane == 31) st.tile_prefix[G] = incl;
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = st.tmem_holder;
+  const int total = st.tile_prefix[G];
+
+  if (warp == 0) {
+    // ===================== TMA producer =====================
+    if (lane == 0) {
+      uint32_t stage = 0, phase = 0;
+      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+        int g, mt, nt;
+        decode_tile(st, G, n_tiles, t, g, mt, nt);
+        const int a_row = st.gstart[g] + mt * BM;
+        const int b_row = (p.b_base + g) * p.b_group_rows + nt * n_out_tile;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          ptx::mbar_wait(ptx::smem_u32(&st.empty[stage]), phase ^ 1);
+          const uint32_t fb = ptx::smem_u32(&st.full[stage]);
+          ptx::mbar_arrive_expect_tx(fb, A_BYTES + B_BYTES);
+          const uint32_t a_dst = ptx::smem_u32(sA + stage * A_BYTES);
+          const uint32_t b_dst = ptx::smem_u32(sB + stage * B_BYTES);
+          ptx::tma_load_2d(a_dst, &tmA, fb, kb * BK, a_row);
+          if (EPI == EPI_SWIGLU) {
+            ptx::tma_load_2d(b_dst, &tmB0, fb, kb * BK, b_row);
+            ptx::tma_load_2d(b_dst + B_BYTES / 2, &tmB1, fb, kb * BK, b_row);
+          } else {
+            ptx::tma_load_2d(b_dst, &tmB0, fb, kb * BK, b_row);
+          }
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ===================== MMA issuer (one thread) =====================
+    if (lane == 0) {
+      constexpr uint32_t idesc = ptx::idesc_bf16_f32(BM, BN);
+      uint32_t stage = 0, phase = 0, iter = 0;
+      for (int t = blockIdx.x; t < total; t += gridDim.x, ++iter) {
+        const uint32_t acc = iter & 1, accph = (iter >> 1) & 1;
+        ptx::mbar_wait(ptx::smem_u32(&st.tempty[acc]), accph ^ 1);
+        ptx::tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          ptx::mbar_wait(ptx::smem_u32(&st.full[stage]), phase);
+          ptx::tc_fence_after();
+          const uint64_t adesc = ptx::sdesc_k_sw128(ptx::smem_u32(sA + stage * A_BYTES));
+          const uint64_t bdesc = ptx::sdesc_k_sw128(ptx::smem_u32(sB + stage * B_BYTES));
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            // advance 16 bf16 = 32 B along K inside the 128 B swizzle atom
+            ptx::mma_bf16_ss(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (kb | k) != 0);
+          }
+          ptx::mma_commit(ptx::smem_u32(&st.empty[stage]));
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+        ptx::mma_commit(ptx::smem_u32(&st.tfull[acc]));
+      }
+    }
+  } else {
+    // ===================== epilogue (4 warps, TMEM lane quadrant = warp % 4) =====
+    const int q = warp & 3;
+    uint32_t iter = 0;
+    for (int t = blockIdx.x; t < total; t += gridDim.x, ++iter) {
+      int g, mt, nt;
+      decode_tile(st, G, n_tiles, t, g, mt, nt);
+      const uint32_t acc = iter & 1, accph = (iter >> 1) & 1;
+      ptx::mbar_wait(ptx::smem_u32(&st.tfull[acc]), accph);
+      ptx::tc_fence_after();
+      const int local_row = mt * BM + q * 32 + lane;
+      const bool valid = local_row < st.gcount[g];
+      const int64_t grow = (int64_t)st.gstart[g] + local_row;
+      const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
+      if (EPI == EPI_SWIGLU) {
+        __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(p.out) + grow * p.ldo + nt * 128;
+#pragma unroll 1
+        for (int c = 0; c < 4; ++c) {
+          uint32_t gr[32], ur[32];
+          ptx::tmem_ld32(taddr + c * 32, gr);
+          ptx::tmem_ld32(taddr + 128 + c * 32, ur);
+          ptx::tmem_wait_ld();
+          uint32_t pk[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            float g0 = __uint_as_float(gr[2 * i]), g1 = __uint_as_float(gr[2 * i + 1]);
+            float u0 = __uint_as_float(ur[2 * i]), u1 = __uint_as_float(ur[2 * i + 1]);
+            pk[i] = pack_bf16(silu_f32(g0) * u0, silu_f32(g1) * u1);
+          }
+          if (valid) {
+            uint4* dst = reinterpret_cast<uint4*>(out + c * 32);
+#pragma unroll
+            for (int v = 0; v < 4; ++v)
+              dst[v] = make_uint4(pk[4 * v], pk[4 * v + 1], pk[4 * v + 2], pk[4 * v + 3]);
+          }
+        }
+      } else if (EPI == EPI_BF16) {
+        __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(p.out) + grow * p.ldo;
+#pragma unroll 1
+        for (int c = 0; c < BN / 32; ++c) {
+          uint32_t r[32];
+          ptx::tmem_ld32(taddr + c * 32, r);
+          ptx::tmem_wait_ld();
+          const int col = nt * BN + c * 32;
+          if (valid && col < p.N) {
+            uint4* dst = reinterpret_cast<uint4*>(out + col);
+#pragma unroll
+            for (int v = 0; v < 4; ++v)
+              dst[v] = make_uint4(pack_bf16(__uint_as_float(r[8 * v + 0]), __uint_as_float(r[8 * v + 1])),
+                                  pack_bf16(__uint_as_float(r[8 * v + 2]), __uint_as_float(r[8 * v + 3])),
+                                  pack_bf16(__uint_as_float(r[8 * v + 4]), __uint_as_float(r[8 * v + 5])),
+                                  pack_bf16(__uint_as_float(r[8 * v + 6]), __uint_as_float(r[8 * v + 7])));
+          }
+        }
+      } else {
+        float* out = reinterpret_cast<float*>(p.out) + grow * p.ldo;
+#pragma unroll 1
+        for (int c = 0; c < BN / 32; ++c) {
+          uint32_t r[32];
+          ptx::tmem_ld32(taddr + c * 32, r);
+          ptx::tmem_wait_ld();
+          const int col0 = nt * BN + c * 32;
+          if (valid) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+              const int col = col0 + i;
+              if (col < p.N) {
+                float v = __uint_as_float(r[i]);
+                if (p.bias) v = __fadd_rn(v, p.bias[col]);
+                out[col] = v;
+              }
+            }
+          }
+        }
+      }
+      ptx::tc_fence_before();
+      ptx::mbar_arrive(ptx::smem_u32(&st.tempty[acc]));
+    }
+  }
+
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  if (warp == 1) ptx::tmem_dealloc<TMEM_COLS>(tmem_base);
+}
+
+// ------------------------------------------------------------------ host side
+
+PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* f = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  });
+  return fn;
+}
+
+// 2D bf16 K-major tensor [rows, K] with a {64, box_rows} box and 128 B swizzle.
+bool make_tmap(CUtensorMap* m, const void* base, int64_t rows, int K, int box_rows) {
+  auto enc = get_encode_fn();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)K * 2};
+  cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box,
+                   estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+template <int EPI>
+int launch_epi(const GemmArgs& a, cudaStream_t stream) {
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(gemm_kernel<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)SMEM_BYTES);
+    if (e != cudaSuccess) return (int)e;
+    attr_set = true;
+  }
+  CUtensorMap tA, tB0, tB1;
+  const int b_box = (EPI == EPI_SWIGLU) ? 128 : 256;
+  if (!make_tmap(&tA, a.A, a.a_rows, a.K, BM)) return (int)cudaErrorInvalidValue;
+  if (!make_tmap(&tB0, a.B0, a.b_rows, a.K, b_box)) return (int)cudaErrorInvalidValue;
+  if (EPI == EPI_SWIGLU) {
+    if (!make_tmap(&tB1, a.B1, a.b_rows, a.K, b_box)) return (int)cudaErrorInvalidValue;
+  } else {
+    tB1 = tB0;
+  }
+  KParams p;
+  p.epi = EPI;
+  p.K = a.K;
+  p.N = a.N;
+  p.G = a.G;
+  p.m_single = a.m_single;
+  p.b_group_rows = a.b_group_rows;
+  p.b_base = a.b_base;
+  p.ldo = a.ldo;
+  p.out = a.out;
+  p.bias = a.bias;
+  p.row_start = a.row_start;
+  p.row_count = a.row_count;
+  gemm_kernel<EPI><<<a.num_ctas, NUM_THREADS, SMEM_BYTES, stream>>>(tA, tB0, tB1, p);
+  return (int)cudaGetLastError();
+}
+
+}  // namespace
+
+int gemm_launch(const GemmArgs& a, cudaStream_t stream) {
+  if (a.K % BK != 0 || a.K <= 0 || a.G < 1 || a.G > MAX_G || a.num_ctas < 1) return (int)cudaErrorInvalidValue;
+  if (a.row_count == nullptr && a.m_single <= 0) return 0;
+  switch (a.epi) {
+    case EPI_SWIGLU: return launch_epi<EPI_SWIGLU>(a, stream);
+    case EPI_BF16: return launch_epi<EPI_BF16>(a, stream);
+    case EPI_F32: return launch_epi<EPI_F32>(a, stream);
+  }
+  return (int)cudaErrorInvalidValue;
+}
+
+}  // namespace epsmoe

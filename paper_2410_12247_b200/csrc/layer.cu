@@ -1,0 +1,676 @@
+// The MoE layer: create / forward / destroy, workspace carve-up, the stream &
+// event DAG of Algorithm 1 and the NCCL all2all over NVLink.
+//
+// Streams (ep > 1): the caller's stream carries routing, permute, shared
+// experts and the expert GEMMs (ComputeMoE); s_disp carries the dispatch
+// All2All of every chunk on communicator A; s_comb the combine All2All on
+// communicator B.  Per chunk c:  D_c (dispatch done) -> GEMMs -> G_c -> combine.
+// Issue order = Algorithm 1: dispatch(0); for p: dispatch(p), compute(p-1),
+// combine(p-2); combine(PN-1).
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/epsmoe.h"
+#include "gemm.h"
+#include "internal.h"
+#include "route.h"
+
+struct moe_layer {
+  moe_config_t cfg;
+  moe_weights_t w;
+  int E_loc = 0, SF = 0, num_sms = 148, device = 0;
+  int64_t send_cap = 0, recv_cap = 0, gemm_rows_cap = 0;
+  // workspace carve-up (device)
+  void* wr_pad = nullptr;
+  float* logits = nullptr;
+  int32_t *topk_idx = nullptr, *pos = nullptr, *range_hist = nullptr, *range_off = nullptr;
+  float* topk_w = nullptr;
+  int32_t *hist = nullptr, *seg_start = nullptr, *ghist = nullptr;
+  int32_t *recv_start_d = nullptr, *recv_count_d = nullptr;
+  void *send = nullptr, *recv = nullptr, *h = nullptr, *o = nullptr, *comb = nullptr;
+  void *hs = nullptr, *s = nullptr;
+  void *x_dev = nullptr, *y_dev = nullptr;  // staging for forward_host
+  // host
+  int32_t* ghist_host = nullptr;    // pinned [ep*E]
+  int32_t* tables_host = nullptr;   // pinned [2*E_loc]
+  cudaStream_t s_disp = nullptr, s_comb = nullptr;
+  cudaEvent_t ev_hist = nullptr, ev_ready = nullptr, ev_comb_done = nullptr;
+  std::vector<cudaEvent_t> ev_disp, ev_gemm;
+  ncclComm_t comm_d = nullptr, comm_c = nullptr;
+  moe_cost_model_t cost;
+  int last_launches = 0;
+};
+
+namespace epsmoe {
+
+static thread_local std::string g_err;
+void set_error(const std::string& msg) { g_err = msg; }
+
+}  // namespace epsmoe
+
+using namespace epsmoe;
+
+#define CUDA_TRY(expr)                                                                    \
+  do {                                                                                    \
+    cudaError_t _e = (expr);                                                              \
+    if (_e != cudaSuccess) {                                                              \
+      set_error(std::string(#expr) + ": " + cudaGetErrorString(_e));                      \
+      return MOE_ERR_CUDA;                                                                \
+    }                                                                                     \
+  } while (0)
+#define KERNEL_TRY(expr)                                                                  \
+  do {                                                                                    \
+    int _e = (expr);                                                                      \
+    if (_e != 0) {                                                                        \
+      set_error(std::string(#expr) + ": " + cudaGetErrorString((cudaError_t)_e));         \
+      return MOE_ERR_CUDA;                                                                \
+    }                                                                                     \
+    ++L->last_launches;                                                                   \
+  } while (0)
+#define NCCL_TRY(expr)                                                                    \
+  do {                                                                                    \
+    ncclResult_t _r = (expr);                                                             \
+    if (_r != ncclSuccess) {                                                              \
+      set_error(std::string(#expr) + ": " + ncclGetErrorString(_r));                      \
+      return MOE_ERR_NCCL;                                                                \
+    }                                                                                     \
+  } while (0)
+
+namespace {
+
+constexpr size_t ALIGN = 256;
+inline size_t align_up(size_t v) { return (v + ALIGN - 1) & ~(ALIGN - 1); }
+
+struct Carve {
+  size_t off = 0;
+  char* base = nullptr;
+  template <typename T>
+  T* take(size_t count) {
+    size_t o = off;
+    off = align_up(off + count * sizeof(T));
+    return base ? reinterpret_cast<T*>(base + o) : nullptr;
+  }
+};
+
+int validate(const moe_config_t* c) {
+  if (!c) return MOE_ERR_INVALID;
+  std::string why;
+  if (c->num_experts < 1 || c->num_experts > MOE_MAX_EXPERTS) why = "num_experts out of [1, 256]";
+  else if (c->ep < 1 || c->num_experts % c->ep) why = "num_experts % ep != 0 (R12)";
+  else if (c->rank < 0 || c->rank >= c->ep) why = "rank out of range";
+  else if (c->top_k < 1 || c->top_k > MOE_MAX_TOPK || c->top_k > c->num_experts) why = "top_k out of range";
+  else if (c->hidden < 64 || c->hidden % 64 || c->hidden > MOE_MAX_HIDDEN) why = "hidden must be a multiple of 64 in [64, 8192]";
+  else if (c->ffn < 128 || c->ffn % 128) why = "ffn must be a positive multiple of 128";
+  else if (c->num_shared < 0 || (c->num_shared > 0 && ((int64_t)c->num_shared * c->shared_ffn) % 128))
+    why = "num_shared * shared_ffn must be a multiple of 128";
+  else if (c->max_tokens < 1) why = "max_tokens must be >= 1";
+  if (!why.empty()) { set_error("invalid config: " + why); return MOE_ERR_INVALID; }
+  return MOE_OK;
+}
+
+// Carve the workspace (base == nullptr: only measure).
+size_t carve(moe_layer* L, char* base) {
+  const moe_config_t& c = L->cfg;
+  const int64_t T = c.max_tokens, E = c.num_experts, k = c.top_k, H = c.hidden, F = c.ffn;
+  const int64_t D = c.ep, E_loc = E / D, SF = (int64_t)c.num_shared * c.shared_ffn;
+  const int64_t R = num_ranges(T);
+  L->send_cap = T * k;
+  L->recv_cap = (D == 1) ? 0 : D * T * std::min<int64_t>(k, E_loc);
+  L->gemm_rows_cap = (D == 1) ? L->send_cap : L->recv_cap;
+  Carve cv;
+  cv.base = base;
+  L->wr_pad = cv.take<uint16_t>(256 * H);
+  L->logits = cv.take<float>(T * E);
+  L->topk_idx = cv.take<int32_t>(T * k);
+  L->topk_w = cv.take<float>(T * k);
+  L->pos = cv.take<int32_t>(T * k);
+  L->range_hist = cv.take<int32_t>(E * R);
+  L->range_off = cv.take<int32_t>(E * R);
+  L->hist = cv.take<int32_t>(MOE_MAX_EXPERTS + 1);
+  L->seg_start = cv.take<int32_t>(MOE_MAX_EXPERTS + 1);
+  L->ghist = cv.take<int32_t>(D * E);
+  L->recv_start_d = cv.take<int32_t>(MOE_MAX_EXPERTS);
+  L->recv_count_d = cv.take<int32_t>(MOE_MAX_EXPERTS);
+  L->send = cv.take<uint16_t>(L->send_cap * H);
+  L->recv = (D == 1) ? nullptr : cv.take<uint16_t>(L->recv_cap * H);
+  L->h = cv.take<uint16_t>(L->gemm_rows_cap * F);
+  L->o = cv.take<uint16_t>(L->gemm_rows_cap * H);
+  L->comb = (D == 1) ? nullptr : cv.take<uint16_t>(L->send_cap * H);
+  L->hs = SF ? cv.take<uint16_t>(T * SF) : nullptr;
+  L->s = SF ? cv.take<uint16_t>(T * H) : nullptr;
+  L->x_dev = cv.take<uint16_t>(T * H);
+  L->y_dev = cv.take<uint16_t>(T * H);
+  return cv.off + ALIGN;
+}
+
+GemmArgs base_args(int epi, int num_ctas) {
+  GemmArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.epi = epi;
+  a.G = 1;
+  a.num_ctas = num_ctas;
+  return a;
+}
+
+// ComputeMoE for local experts [g0, g1): GateUpGemm+SiluAct fused,
+// then DownGemm.  Rows of expert g are [row_start[g], +row_count[g]) of A.
+int compute_moe(moe_layer* L, const void* A, int64_t a_rows, const int32_t* row_start, const int32_t* row_count,
+                int g0, int g1, int kind, int num_ctas, cudaStream_t st) {
+  const moe_config_t& c = L->cfg;
+  GemmArgs g1a = base_args(EPI_SWIGLU, num_ctas);
+  g1a.A = A;
+  g1a.a_rows = a_rows;
+  g1a.B0 = L->w.w_gate;
+  g1a.B1 = L->w.w_up;
+  g1a.b_rows = (int64_t)L->E_loc * c.ffn;
+  g1a.b_group_rows = c.ffn;
+  g1a.K = c.hidden;
+  g1a.N = c.ffn;
+  g1a.out = L->h;
+  g1a.ldo = c.ffn;
+  GemmArgs g2a = base_args(EPI_BF16, num_ctas);
+  g2a.A = L->h;
+  g2a.a_rows = L->gemm_rows_cap;
+  g2a.B0 = L->w.w_down;
+  g2a.b_rows = (int64_t)L->E_loc * c.hidden;
+  g2a.b_group_rows = c.hidden;
+  g2a.K = c.ffn;
+  g2a.N = c.hidden;
+  g2a.out = L->o;
+  g2a.ldo = c.hidden;
+  auto run = [&](int a, int b) -> int {
+    for (GemmArgs* ga : {&g1a, &g2a}) {
+      ga->G = b - a;
+      ga->b_base = a;
+      ga->row_start = row_start + a;
+      ga->row_count = row_count + a;
+      int e = gemm_launch(*ga, st);
+      if (e) return e;
+      ++L->last_launches;
+    }
+    return 0;
+  };
+  if (kind == MOE_GEMM_GROUPED) return run(g0, g1);
+  for (int e = g0; e < g1; ++e) {
+    int e2 = run(e, e + 1);
+    if (e2) return e2;
+  }
+  return 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* moe_last_error(void) { return g_err.c_str(); }
+
+size_t moe_layer_workspace_bytes(const moe_config_t* cfg) {
+  if (validate(cfg) != MOE_OK) return 0;
+  moe_layer tmp;
+  tmp.cfg = *cfg;
+  return carve(&tmp, nullptr);
+}
+
+moe_status_t moe_get_unique_id(void* out128) {
+  if (!out128) return MOE_ERR_INVALID;
+  ncclUniqueId id;
+  NCCL_TRY(ncclGetUniqueId(&id));
+  std::memcpy(out128, &id, sizeof(id));
+  return MOE_OK;
+}
+
+moe_status_t moe_plan_compute(const moe_config_t* cfg, const moe_cost_model_t* cost, int64_t global_tokens,
+                              const int32_t* global_hist, moe_plan_t* out) {
+  if (!out) return MOE_ERR_INVALID;
+  int v = validate(cfg);
+  if (v) return (moe_status_t)v;
+  moe_cost_model_t def;
+  if (!cost) {
+    default_cost_model(*cfg, &def);
+    cost = &def;
+  }
+  return (moe_status_t)plan_compute(*cfg, *cost, global_tokens, global_hist, out);
+}
+
+moe_status_t moe_layer_create(const moe_config_t* cfg, const moe_weights_t* w, const void* uid_d,
+                              const void* uid_c, void* workspace, size_t workspace_bytes, moe_layer_t** out) {
+  if (!out || !w) { set_error("null argument"); return MOE_ERR_INVALID; }
+  *out = nullptr;
+  int v = validate(cfg);
+  if (v) return (moe_status_t)v;
+  if (!w->w_router || !w->w_gate || !w->w_up || !w->w_down) { set_error("missing weights"); return MOE_ERR_INVALID; }
+  if (cfg->num_shared > 0 && (!w->ws_gate || !w->ws_up || !w->ws_down)) {
+    set_error("missing shared-expert weights");
+    return MOE_ERR_INVALID;
+  }
+  if (cfg->ep > 1 && (!uid_d || !uid_c)) { set_error("ep > 1 needs two NCCL unique ids"); return MOE_ERR_INVALID; }
+  moe_layer* L = new moe_layer();
+  L->cfg = *cfg;
+  L->w = *w;
+  L->E_loc = cfg->num_experts / cfg->ep;
+  L->SF = cfg->num_shared * cfg->shared_ffn;
+  size_t need = carve(L, nullptr);
+  if (!workspace || workspace_bytes < need) {
+    set_error("workspace too small: need " + std::to_string(need) + " bytes");
+    delete L;
+    return MOE_ERR_CAPACITY;
+  }
+  char* base = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(workspace) + ALIGN - 1) & ~(uintptr_t)(ALIGN - 1));
+  carve(L, base);
+  auto fail = [&](moe_status_t st) { moe_layer_destroy(L); return st; };
+  if (cudaGetDevice(&L->device) != cudaSuccess) return fail(MOE_ERR_CUDA);
+  cudaDeviceGetAttribute(&L->num_sms, cudaDevAttrMultiProcessorCount, L->device);
+  int cc_major = 0, cc_minor = 0;
+  cudaDeviceGetAttribute(&cc_major, cudaDevAttrComputeCapabilityMajor, L->device);
+  cudaDeviceGetAttribute(&cc_minor, cudaDevAttrComputeCapabilityMinor, L->device);
+  if (cc_major != 10 || cc_minor != 0) {
+    set_error("this build targets sm_100a (B200); device is sm_" + std::to_string(cc_major * 10 + cc_minor));
+    return fail(MOE_ERR_UNSUPPORTED);
+  }
+  if (launch_pad_rows(w->w_router, cfg->num_experts, cfg->hidden, L->wr_pad, 256, 0)) {
+    set_error("router pad failed");
+    return fail(MOE_ERR_CUDA);
+  }
+  if (cudaHostAlloc(&L->ghist_host, sizeof(int32_t) * cfg->ep * cfg->num_experts, cudaHostAllocDefault) != cudaSuccess ||
+      cudaHostAlloc(&L->tables_host, sizeof(int32_t) * 2 * MOE_MAX_EXPERTS, cudaHostAllocDefault) != cudaSuccess) {
+    set_error("cudaHostAlloc failed");
+    return fail(MOE_ERR_CUDA);
+  }
+  default_cost_model(L->cfg, &L->cost);
+  if (cfg->ep > 1) {
+    if (cudaStreamCreateWithFlags(&L->s_disp, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&L->s_comb, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&L->ev_hist, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&L->ev_ready, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&L->ev_comb_done, cudaEventDisableTiming) != cudaSuccess) {
+      set_error("stream/event creation failed");
+      return fail(MOE_ERR_CUDA);
+    }
+    L->ev_disp.resize(MOE_MAX_CHUNKS);
+    L->ev_gemm.resize(MOE_MAX_CHUNKS);
+    for (int i = 0; i < MOE_MAX_CHUNKS; ++i) {
+      cudaEventCreateWithFlags(&L->ev_disp[i], cudaEventDisableTiming);
+      cudaEventCreateWithFlags(&L->ev_gemm[i], cudaEventDisableTiming);
+    }
+    ncclUniqueId id_d, id_c;
+    std::memcpy(&id_d, uid_d, sizeof(id_d));
+    std::memcpy(&id_c, uid_c, sizeof(id_c));
+    ncclConfig_t ncfg = NCCL_CONFIG_INITIALIZER;
+    ncfg.blocking = 1;
+    ncclResult_t r1 = ncclCommInitRankConfig(&L->comm_d, cfg->ep, id_d, cfg->rank, &ncfg);
+    ncclResult_t r2 = r1 == ncclSuccess ? ncclCommInitRankConfig(&L->comm_c, cfg->ep, id_c, cfg->rank, &ncfg) : r1;
+    if (r1 != ncclSuccess || r2 != ncclSuccess) {
+      set_error(std::string("ncclCommInitRankConfig: ") + ncclGetErrorString(r1 != ncclSuccess ? r1 : r2));
+      return fail(MOE_ERR_NCCL);
+    }
+    // every rank must agree on the shape (MOE_ERR_MISMATCH)
+    int64_t sig[8] = {cfg->num_experts, cfg->top_k, cfg->hidden, cfg->ffn, cfg->num_shared, cfg->shared_ffn,
+                      cfg->norm_topk, (int64_t)(cfg->routed_scale * 1e6)};
+    int64_t* d_sig = nullptr;
+    if (cudaMalloc(&d_sig, sizeof(sig) * (cfg->ep + 1)) != cudaSuccess) return fail(MOE_ERR_CUDA);
+    cudaMemcpy(d_sig, sig, sizeof(sig), cudaMemcpyHostToDevice);
+    ncclResult_t r3 = ncclAllGather(d_sig, d_sig + 8, 8, ncclInt64, L->comm_d, 0);
+    std::vector<int64_t> all(8 * cfg->ep);
+    cudaMemcpy(all.data(), d_sig + 8, sizeof(int64_t) * 8 * cfg->ep, cudaMemcpyDeviceToHost);
+    cudaFree(d_sig);
+    if (r3 != ncclSuccess) return fail(MOE_ERR_NCCL);
+    for (int r = 0; r < cfg->ep; ++r)
+      if (std::memcmp(all.data() + 8 * r, sig, sizeof(sig)) != 0) {
+        set_error("config mismatch across ranks");
+        return fail(MOE_ERR_MISMATCH);
+      }
+  }
+  if (cudaDeviceSynchronize() != cudaSuccess) {
+    set_error(std::string("create: ") + cudaGetErrorString(cudaGetLastError()));
+    return fail(MOE_ERR_CUDA);
+  }
+  *out = L;
+  return MOE_OK;
+}
+
+moe_status_t moe_layer_destroy(moe_layer_t* L) {
+  if (!L) return MOE_OK;
+  if (L->comm_d) ncclCommDestroy(L->comm_d);
+  if (L->comm_c) ncclCommDestroy(L->comm_c);
+  if (L->s_disp) cudaStreamDestroy(L->s_disp);
+  if (L->s_comb) cudaStreamDestroy(L->s_comb);
+  for (cudaEvent_t e : {L->ev_hist, L->ev_ready, L->ev_comb_done})
+    if (e) cudaEventDestroy(e);
+  for (auto e : L->ev_disp) if (e) cudaEventDestroy(e);
+  for (auto e : L->ev_gemm) if (e) cudaEventDestroy(e);
+  if (L->ghist_host) cudaFreeHost(L->ghist_host);
+  if (L->tables_host) cudaFreeHost(L->tables_host);
+  delete L;
+  return MOE_OK;
+}
+
+moe_status_t moe_plan_pipeline(const moe_layer_t* L, int64_t global_tokens, const int32_t* global_hist,
+                               moe_plan_t* out) {
+  if (!L || !out) return MOE_ERR_INVALID;
+  return (moe_status_t)plan_compute(L->cfg, L->cost, global_tokens, global_hist, out);
+}
+
+moe_status_t moe_layer_set_cost_model(moe_layer_t* L, const moe_cost_model_t* cost) {
+  if (!L || !cost || cost->n_points < 1 || cost->n_points > MOE_COST_POINTS) return MOE_ERR_INVALID;
+  L->cost = *cost;
+  return MOE_OK;
+}
+
+int32_t moe_layer_last_launches(const moe_layer_t* L) { return L ? L->last_launches : 0; }
+
+moe_status_t moe_layer_forward(moe_layer_t* L, const void* x, int64_t T, void* y, const moe_plan_t* plan_in,
+                               void* stream_v, moe_debug_t* dbg) {
+  if (!L || (!x && T > 0) || (!y && T > 0) || T < 0) { set_error("null argument"); return MOE_ERR_INVALID; }
+  const moe_config_t& c = L->cfg;
+  if (T > c.max_tokens) { set_error("T_loc > max_tokens"); return MOE_ERR_CAPACITY; }
+  cudaStream_t st = (cudaStream_t)stream_v;
+  const int E = c.num_experts, k = c.top_k, H = c.hidden, D = c.ep, E_loc = L->E_loc;
+  L->last_launches = 0;
+  const bool override_routing = dbg && dbg->override_routing;
+  if (override_routing && (!dbg->topk_idx || !dbg->topk_w)) { set_error("override needs topk_idx/topk_w"); return MOE_ERR_INVALID; }
+  int32_t* topk_idx = override_routing ? dbg->topk_idx : L->topk_idx;
+  float* topk_w = override_routing ? dbg->topk_w : L->topk_w;
+
+  moe_plan_t plan;
+  if (plan_in) {
+    plan = *plan_in;
+    int pv = plan_normalise(c, &plan);
+    if (pv) { set_error("invalid plan"); return (moe_status_t)pv; }
+  }
+  int num_ctas = (plan_in && plan.sm_gemm > 0) ? std::min(plan.sm_gemm, L->num_sms) : L->num_sms;
+
+  // ---- Router (K1) + topKGating (K2) + histogram
+  if (T > 0 && !override_routing) {
+    GemmArgs ra = base_args(EPI_F32, num_ctas);
+    ra.A = x;
+    ra.a_rows = T;
+    ra.B0 = L->wr_pad;
+    ra.b_rows = 256;
+    ra.K = H;
+    ra.N = E;
+    ra.out = L->logits;
+    ra.ldo = E;
+    ra.bias = L->w.router_bias;
+    ra.m_single = (int)T;
+    KERNEL_TRY(gemm_launch(ra, st));
+  }
+  KERNEL_TRY(launch_gate_topk(L->logits, (int)T, E, k, c.norm_topk, c.routed_scale, override_routing ? 1 : 0,
+                              topk_idx, topk_w, L->range_hist, st));
+  KERNEL_TRY(launch_range_scan(L->range_hist, (int)T, E, L->range_off, L->hist, st));
+  // ---- split (K3): x -> send rows, expert-major (R6)
+  KERNEL_TRY(launch_permute(x, (int)T, H, E, k, topk_idx, L->range_off, L->hist, L->send, L->pos,
+                            L->seg_start, st));
+
+  auto shared_experts = [&]() -> int {
+    if (!L->SF || T == 0) return 0;
+    GemmArgs a = base_args(EPI_SWIGLU, num_ctas);
+    a.A = x;
+    a.a_rows = T;
+    a.B0 = L->w.ws_gate;
+    a.B1 = L->w.ws_up;
+    a.b_rows = L->SF;
+    a.K = H;
+    a.N = L->SF;
+    a.out = L->hs;
+    a.ldo = L->SF;
+    a.m_single = (int)T;
+    int e = gemm_launch(a, st);
+    if (e) return e;
+    ++L->last_launches;
+    GemmArgs b = base_args(EPI_BF16, num_ctas);
+    b.A = L->hs;
+    b.a_rows = T;
+    b.B0 = L->w.ws_down;
+    b.b_rows = H;
+    b.K = L->SF;
+    b.N = H;
+    b.out = L->s;
+    b.ldo = H;
+    b.m_single = (int)T;
+    e = gemm_launch(b, st);
+    if (!e) ++L->last_launches;
+    return e;
+  };
+
+  if (D == 1) {
+    // ---- EP = 1: no all2all; every chunk is local (C = 0 => PN = 1 is optimal)
+    if (!plan_in) plan_compute(c, L->cost, T, nullptr, &plan);
+    int e = shared_experts();
+    if (e) { set_error(std::string("shared experts: ") + cudaGetErrorString((cudaError_t)e)); return MOE_ERR_CUDA; }
+    for (int ch = 0; ch < plan.num_chunks; ++ch) {
+      int g0 = plan.group_begin[ch], g1 = plan.group_begin[ch + 1];
+      // maximal runs of equal kind inside the chunk
+      int a = g0;
+      while (a < g1) {
+        int b = a + 1;
+        while (b < g1 && plan.expert_kind[b] == plan.expert_kind[a]) ++b;
+        int err = compute_moe(L, L->send, L->send_cap, L->seg_start, L->hist, a, b, plan.expert_kind[a], num_ctas, st);
+        if (err) { set_error(std::string("ComputeMoE: ") + cudaGetErrorString((cudaError_t)err)); return MOE_ERR_CUDA; }
+        a = b;
+      }
+    }
+    KERNEL_TRY(launch_combine(L->o, L->SF ? L->s : nullptr, (int)T, H, k, L->pos, topk_w, y, st));
+  } else {
+    // ---- EP > 1: count exchange (C3), plan, chunked dispatch / compute / combine
+    NCCL_TRY(ncclAllGather(L->hist, L->ghist, E, ncclInt32, L->comm_d, st));
+    CUDA_TRY(cudaMemcpyAsync(L->ghist_host, L->ghist, sizeof(int32_t) * D * E, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaEventRecord(L->ev_hist, st));
+    int e = shared_experts();  // overlaps the host wait and dispatch(0)
+    if (e) { set_error(std::string("shared experts: ") + cudaGetErrorString((cudaError_t)e)); return MOE_ERR_CUDA; }
+    CUDA_TRY(cudaEventSynchronize(L->ev_hist));
+    const int32_t* gh = L->ghist_host;
+    if (!plan_in) {
+      int64_t m = 0;
+      for (int i = 0; i < D * E; ++i) m += gh[i];
+      plan_compute(c, L->cost, m / k, gh, &plan);
+    }
+    const int me = c.rank;
+    // send offsets (local, expert-major) and recv layout [e_l][src] (R6)
+    std::vector<int64_t> send_off(E + 1, 0);
+    for (int ex = 0; ex < E; ++ex) send_off[ex + 1] = send_off[ex] + gh[(int64_t)me * E + ex];
+    std::vector<int64_t> recv_off((size_t)E_loc * D + 1, 0);
+    for (int el = 0; el < E_loc; ++el)
+      for (int src = 0; src < D; ++src) {
+        size_t i = (size_t)el * D + src;
+        recv_off[i + 1] = recv_off[i] + gh[(int64_t)src * E + me * E_loc + el];
+      }
+    if (recv_off.back() > L->recv_cap) { set_error("recv rows exceed capacity"); return MOE_ERR_CAPACITY; }
+    for (int el = 0; el < E_loc; ++el) {
+      L->tables_host[el] = (int32_t)recv_off[(size_t)el * D];
+      L->tables_host[MOE_MAX_EXPERTS + el] = (int32_t)(recv_off[(size_t)(el + 1) * D] - recv_off[(size_t)el * D]);
+    }
+    CUDA_TRY(cudaMemcpyAsync(L->recv_start_d, L->tables_host, sizeof(int32_t) * E_loc, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemcpyAsync(L->recv_count_d, L->tables_host + MOE_MAX_EXPERTS, sizeof(int32_t) * E_loc,
+                             cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaEventRecord(L->ev_ready, st));
+    CUDA_TRY(cudaStreamWaitEvent(L->s_disp, L->ev_ready, 0));
+    CUDA_TRY(cudaStreamWaitEvent(L->s_comb, L->ev_ready, 0));
+    const size_t row_bytes = (size_t)H * 2;
+    auto dispatch = [&](int ch) -> moe_status_t {
+      int g0 = plan.group_begin[ch], g1 = plan.group_begin[ch + 1];
+      NCCL_TRY(ncclGroupStart());
+      for (int peer = 0; peer < D; ++peer)
+        for (int el = g0; el < g1; ++el) {
+          int ex = peer * E_loc + el;
+          int64_t n_send = gh[(int64_t)me * E + ex];
+          if (n_send)
+            NCCL_TRY(ncclSend((char*)L->send + send_off[ex] * row_bytes, n_send * H, ncclBfloat16, peer, L->comm_d, L->s_disp));
+          int64_t n_recv = gh[(int64_t)peer * E + me * E_loc + el];
+          if (n_recv)
+            NCCL_TRY(ncclRecv((char*)L->recv + recv_off[(size_t)el * D + peer] * row_bytes, n_recv * H, ncclBfloat16,
+                              peer, L->comm_d, L->s_disp));
+        }
+      NCCL_TRY(ncclGroupEnd());
+      CUDA_TRY(cudaEventRecord(L->ev_disp[ch], L->s_disp));
+      return MOE_OK;
+    };
+    auto combine_send = [&](int ch) -> moe_status_t {
+      int g0 = plan.group_begin[ch], g1 = plan.group_begin[ch + 1];
+      CUDA_TRY(cudaStreamWaitEvent(L->s_comb, L->ev_gemm[ch], 0));
+      NCCL_TRY(ncclGroupStart());
+      for (int peer = 0; peer < D; ++peer)
+        for (int el = g0; el < g1; ++el) {
+          int64_t n_back = gh[(int64_t)peer * E + me * E_loc + el];
+          if (n_back)
+            NCCL_TRY(ncclSend((char*)L->o + recv_off[(size_t)el * D + peer] * row_bytes, n_back * H, ncclBfloat16, peer,
+                              L->comm_c, L->s_comb));
+          int ex = peer * E_loc + el;
+          int64_t n_home = gh[(int64_t)me * E + ex];
+          if (n_home)
+            NCCL_TRY(ncclRecv((char*)L->comb + send_off[ex] * row_bytes, n_home * H, ncclBfloat16, peer, L->comm_c,
+                              L->s_comb));
+        }
+      NCCL_TRY(ncclGroupEnd());
+      return MOE_OK;
+    };
+    auto compute = [&](int ch) -> moe_status_t {
+      int g0 = plan.group_begin[ch], g1 = plan.group_begin[ch + 1];
+      CUDA_TRY(cudaStreamWaitEvent(st, L->ev_disp[ch], 0));
+      int a = g0;
+      while (a < g1) {
+        int b = a + 1;
+        while (b < g1 && plan.expert_kind[b] == plan.expert_kind[a]) ++b;
+        int err = compute_moe(L, L->recv, L->recv_cap, L->recv_start_d, L->recv_count_d, a, b, plan.expert_kind[a],
+                              num_ctas, st);
+        if (err) { set_error(std::string("ComputeMoE: ") + cudaGetErrorString((cudaError_t)err)); return MOE_ERR_CUDA; }
+        a = b;
+      }
+      CUDA_TRY(cudaEventRecord(L->ev_gemm[ch], st));
+      return MOE_OK;
+    };
+    // Algorithm 1 issue order
+    const int PN = plan.num_chunks;
+    moe_status_t s_ = dispatch(0);
+    if (s_) return s_;
+    for (int p = 1; p <= PN; ++p) {
+      if (p <= PN - 1 && (s_ = dispatch(p))) return s_;
+      if ((s_ = compute(p - 1))) return s_;
+      if (p - 2 >= 0 && (s_ = combine_send(p - 2))) return s_;
+    }
+    if ((s_ = combine_send(PN - 1))) return s_;
+    CUDA_TRY(cudaEventRecord(L->ev_comb_done, L->s_comb));
+    CUDA_TRY(cudaStreamWaitEvent(st, L->ev_comb_done, 0));
+    KERNEL_TRY(launch_combine(L->comb, L->SF ? L->s : nullptr, (int)T, H, k, L->pos, topk_w, y, st));
+  }
+
+  if (dbg) {
+    if (dbg->logits && !override_routing)
+      CUDA_TRY(cudaMemcpyAsync(dbg->logits, L->logits, sizeof(float) * T * E, cudaMemcpyDeviceToDevice, st));
+    if (dbg->topk_idx && !override_routing)
+      CUDA_TRY(cudaMemcpyAsync(dbg->topk_idx, L->topk_idx, sizeof(int32_t) * T * k, cudaMemcpyDeviceToDevice, st));
+    if (dbg->topk_w && !override_routing)
+      CUDA_TRY(cudaMemcpyAsync(dbg->topk_w, L->topk_w, sizeof(float) * T * k, cudaMemcpyDeviceToDevice, st));
+    if (dbg->pos) CUDA_TRY(cudaMemcpyAsync(dbg->pos, L->pos, sizeof(int32_t) * T * k, cudaMemcpyDeviceToDevice, st));
+    if (dbg->hist) CUDA_TRY(cudaMemcpyAsync(dbg->hist, L->hist, sizeof(int32_t) * E, cudaMemcpyDeviceToDevice, st));
+    if (dbg->seg_start)
+      CUDA_TRY(cudaMemcpyAsync(dbg->seg_start, L->seg_start, sizeof(int32_t) * (E + 1), cudaMemcpyDeviceToDevice, st));
+    if (dbg->shared_out && L->SF)
+      CUDA_TRY(cudaMemcpyAsync(dbg->shared_out, L->s, (size_t)T * H * 2, cudaMemcpyDeviceToDevice, st));
+    if (dbg->global_hist_host) {
+      if (D == 1) {
+        CUDA_TRY(cudaMemcpyAsync(dbg->global_hist_host, L->hist, sizeof(int32_t) * E, cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(cudaStreamSynchronize(st));
+      } else {
+        std::memcpy(dbg->global_hist_host, L->ghist_host, sizeof(int32_t) * D * E);
+      }
+    }
+    if (dbg->plan_used) *dbg->plan_used = plan;
+  }
+  return MOE_OK;
+}
+
+moe_status_t moe_layer_forward_host(moe_layer_t* L, const void* x_host, int64_t T, void* y_host,
+                                    const moe_plan_t* plan, void* stream_v) {
+  if (!L || T < 0 || T > L->cfg.max_tokens) { set_error("bad argument"); return MOE_ERR_INVALID; }
+  cudaStream_t st = (cudaStream_t)stream_v;
+  size_t bytes = (size_t)T * L->cfg.hidden * 2;
+  CUDA_TRY(cudaMemcpyAsync(L->x_dev, x_host, bytes, cudaMemcpyHostToDevice, st));
+  moe_status_t s = moe_layer_forward(L, L->x_dev, T, L->y_dev, plan, stream_v, nullptr);
+  if (s) return s;
+  CUDA_TRY(cudaMemcpyAsync(y_host, L->y_dev, bytes, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  return MOE_OK;
+}
+
+moe_status_t moe_gemm_grouped(int32_t epi, const void* A, int64_t a_rows, const void* B0, const void* B1,
+                              int64_t b_rows, int32_t b_group_rows, int32_t kdim, int32_t n, void* out, int64_t ldo,
+                              const float* bias, int32_t groups, const int32_t* row_start, const int32_t* row_count,
+                              int32_t num_ctas, void* stream) {
+  if (epi < 0 || epi > 2 || !A || !B0 || (epi == 0 && !B1) || !out || groups < 1 || !row_start || !row_count) {
+    set_error("moe_gemm_grouped: bad argument");
+    return MOE_ERR_INVALID;
+  }
+  GemmArgs a = base_args(epi, num_ctas > 0 ? num_ctas : 148);
+  a.A = A;
+  a.a_rows = a_rows;
+  a.B0 = B0;
+  a.B1 = B1;
+  a.b_rows = b_rows;
+  a.b_group_rows = b_group_rows;
+  a.K = kdim;
+  a.N = n;
+  a.out = out;
+  a.ldo = ldo;
+  a.bias = bias;
+  a.G = groups;
+  a.row_start = row_start;
+  a.row_count = row_count;
+  int e = gemm_launch(a, (cudaStream_t)stream);
+  if (e) { set_error(std::string("gemm: ") + cudaGetErrorString((cudaError_t)e)); return MOE_ERR_CUDA; }
+  return MOE_OK;
+}
+
+moe_status_t moe_layer_calibrate(moe_layer_t* L, void* stream, moe_cost_model_t* out) {
+  if (!L) return MOE_ERR_INVALID;
+  // Measured GEMM time per expert vs rows, both kinds (X2/X3 analog on B200).
+  const moe_config_t& c = L->cfg;
+  cudaStream_t st = (cudaStream_t)stream;
+  moe_cost_model_t m = L->cost;
+  const int G = std::min(L->E_loc, 8);
+  const float pts[MOE_COST_POINTS] = {16, 64, 128, 256, 512, 1024, 2048, 3072, 4096, 6144, 8192, 16384};
+  cudaEvent_t e0, e1;
+  CUDA_TRY(cudaEventCreate(&e0));
+  CUDA_TRY(cudaEventCreate(&e1));
+  std::vector<int32_t> hs(2 * MOE_MAX_EXPERTS);
+  int np = 0;
+  for (int i = 0; i < MOE_COST_POINTS; ++i) {
+    int64_t rows = (int64_t)pts[i];
+    if (rows * G > L->gemm_rows_cap) break;
+    for (int g = 0; g < G; ++g) { hs[g] = (int32_t)(g * rows); hs[MOE_MAX_EXPERTS + g] = (int32_t)rows; }
+    CUDA_TRY(cudaMemcpy(L->recv_start_d, hs.data(), sizeof(int32_t) * G, cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(L->recv_count_d, hs.data() + MOE_MAX_EXPERTS, sizeof(int32_t) * G, cudaMemcpyHostToDevice));
+    const void* A = L->recv ? L->recv : L->send;
+    int64_t arows = L->recv ? L->recv_cap : L->send_cap;
+    for (int kind = 1; kind <= 2; ++kind) {
+      float best = 1e30f;
+      for (int rep = 0; rep < 3; ++rep) {
+        CUDA_TRY(cudaEventRecord(e0, st));
+        int err = compute_moe(L, A, arows, L->recv_start_d, L->recv_count_d, 0, G, kind, L->num_sms, st);
+        if (err) { set_error("calibrate gemm failed"); return MOE_ERR_CUDA; }
+        CUDA_TRY(cudaEventRecord(e1, st));
+        CUDA_TRY(cudaEventSynchronize(e1));
+        float ms = 0;
+        cudaEventElapsedTime(&ms, e0, e1);
+        best = std::min(best, ms);
+      }
+      m.gemm_ms[kind - 1][i] = best / G;
+    }
+    m.m_points[i] = pts[i];
+    np = i + 1;
+  }
+  m.n_points = np;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  (void)c;
+  L->cost = m;
+  if (out) *out = m;
+  return MOE_OK;
+}
+
+}  // extern "C"

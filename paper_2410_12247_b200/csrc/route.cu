@@ -1,0 +1,328 @@
+// HBM-bound kernels of the layer: topKGating (K2), histogram/scan/permute
+// (`split`, K3) and the gate-weighted unpermute fused into combine (K7).
+//
+// Layout readings: send buffer rows are ordered by (expert asc,
+// token asc) (R6); tokens are processed in ranges of RANGE_T consecutive
+// tokens, one warp per range, so every per-expert offset is a deterministic
+// prefix sum: no atomics decide any row index.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "route.h"
+
+namespace epsmoe {
+namespace {
+
+constexpr int WARPS = 8;
+constexpr int MAX_EPL = 8;  // E <= 256: logits per lane
+
+struct Cand {
+  float v;
+  int e;
+};
+__device__ __forceinline__ bool better(float av, int ae, float bv, int be) {
+  return av > bv || (av == bv && ae < be);
+}
+
+// K2 topKGating.  One warp per range of RANGE_T tokens, tokens
+// in order.  idx = k largest logits (ties -> lower expert id, R2); p = softmax
+// over all E in fp32; w_j = p_{idx_j} (/ sum_j p_{idx_j} if norm_topk) * scale.
+// Also writes the range's expert histogram range_hist[e * R + r].
+__global__ void __launch_bounds__(WARPS * 32)
+gate_topk_kernel(const float* __restrict__ logits, int T, int E, int k, int norm_topk, float scale,
+                 int override_routing, int32_t* __restrict__ topk_idx, float* __restrict__ topk_w,
+                 int32_t* __restrict__ range_hist, int R) {
+  __shared__ int32_t hist_s[WARPS][256];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int r = blockIdx.x * WARPS + warp;
+  for (int e = lane; e < E; e += 32) hist_s[warp][e] = 0;
+  __syncwarp();
+  if (r < R) {
+    const int t_end = min(T, (r + 1) * RANGE_T);
+    for (int t = r * RANGE_T; t < t_end; ++t) {
+      if (override_routing) {
+        if (lane < k) {
+          int e = topk_idx[(int64_t)t * k + lane];
+          atomicAdd(&hist_s[warp][e], 1);  // order-free count
+        }
+        continue;
+      }
+      float v[MAX_EPL];
+      const float* row = logits + (int64_t)t * E;
+#pragma unroll
+      for (int i = 0; i < MAX_EPL; ++i) {
+        int e = lane + 32 * i;
+        v[i] = (e < E) ? row[e] : -INFINITY;
+      }
+      uint32_t taken = 0;
+      float top_v[8];
+      int top_e[8];
+      for (int j = 0; j < k; ++j) {
+        float bv = -INFINITY;
+        int be = 0x7fffffff;
+#pragma unroll
+        for (int i = 0; i < MAX_EPL; ++i) {
+          int e = lane + 32 * i;
+          if (e < E && !((taken >> i) & 1u) && better(v[i], e, bv, be)) { bv = v[i]; be = e; }
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+          float ov = __shfl_xor_sync(0xffffffffu, bv, off);
+          int oe = __shfl_xor_sync(0xffffffffu, be, off);
+          if (better(ov, oe, bv, be)) { bv = ov; be = oe; }
+        }
+        top_v[j] = bv;
+        top_e[j] = be;
+        if ((be & 31) == lane) taken |= 1u << (be >> 5);
+      }
+      // softmax denominator over all E (max = top-1 logit)
+      const float m = top_v[0];
+      float s = 0.f;
+#pragma unroll
+      for (int i = 0; i < MAX_EPL; ++i) s += expf(v[i] - m);   // -inf lanes add 0
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+      float psel = 0.f;
+      float pj = 0.f;
+      for (int j = 0; j < k; ++j) {
+        float pv = expf(top_v[j] - m) / s;
+        psel += pv;
+        if (j == lane) pj = pv;
+      }
+      if (lane < k) {
+        float w = norm_topk ? pj / psel : pj;
+        topk_idx[(int64_t)t * k + lane] = top_e[lane];
+        topk_w[(int64_t)t * k + lane] = w * scale;
+      }
+      if (lane == 0)
+        for (int j = 0; j < k; ++j) hist_s[warp][top_e[j]] += 1;
+      __syncwarp();
+    }
+  }
+  __syncwarp();
+  if (r < R)
+    for (int e = lane; e < E; e += 32) range_hist[(int64_t)e * R + r] = hist_s[warp][e];
+}
+
+// Exclusive scan of range_hist[e][0..R) per expert (one block per expert);
+// range_off[e][r] = sum_{r' < r}, hist[e] = total.
+__global__ void __launch_bounds__(1024)
+range_scan_kernel(const int32_t* __restrict__ range_hist, int R, int32_t* __restrict__ range_off,
+                  int32_t* __restrict__ hist) {
+  __shared__ int32_t warp_sum[32];
+  const int e = blockIdx.x;
+  const int per = (R + blockDim.x - 1) / blockDim.x;
+  const int r0 = threadIdx.x * per;
+  const int32_t* src = range_hist + (int64_t)e * R;
+  int local = 0;
+  for (int i = 0; i < per; ++i)
+    if (r0 + i < R) local += src[r0 + i];
+  // block exclusive scan of `local`
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int incl = local;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    int v = __shfl_up_sync(0xffffffffu, incl, off);
+    if (lane >= off) incl += v;
+  }
+  if (lane == 31) warp_sum[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    int ws = (lane < (int)(blockDim.x >> 5)) ? warp_sum[lane] : 0;
+    int wi = ws;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      int v = __shfl_up_sync(0xffffffffu, wi, off);
+      if (lane >= off) wi += v;
+    }
+    warp_sum[lane] = wi - ws;  // exclusive per-warp base
+    if (lane == 31) hist[e] = wi;
+  }
+  __syncthreads();
+  int run = warp_sum[warp] + incl - local;
+  int32_t* dst = range_off + (int64_t)e * R;
+  for (int i = 0; i < per; ++i)
+    if (r0 + i < R) {
+      dst[r0 + i] = run;
+      run += src[r0 + i];
+    }
+}
+
+__device__ __forceinline__ int block_exclusive_scan_256(int v, int* sh) {
+  // blockDim.x == 256
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int incl = v;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    int o = __shfl_up_sync(0xffffffffu, incl, off);
+    if (lane >= off) incl += o;
+  }
+  if (lane == 31) sh[warp] = incl;
+  __syncthreads();
+  int base = 0;
+  for (int w = 0; w < warp; ++w) base += sh[w];
+  __syncthreads();
+  return base + incl - v;
+}
+
+// K3 permute (`split`).  seg_start[e] = sum_{e' < e} hist[e'] (send
+// layout expert-major, R6).  One warp per token range; each token's row is
+// read once and written to its k destination rows with 16-byte stores.
+__global__ void __launch_bounds__(WARPS * 32)
+permute_kernel(const __nv_bfloat16* __restrict__ x, int T, int H, int E, int k,
+               const int32_t* __restrict__ topk_idx, const int32_t* __restrict__ range_off,
+               const int32_t* __restrict__ hist, int R, __nv_bfloat16* __restrict__ send,
+               int32_t* __restrict__ pos, int32_t* __restrict__ seg_start_out) {
+  __shared__ int32_t seg_s[256];
+  __shared__ int32_t scan_tmp[8];
+  __shared__ int32_t off_s[WARPS][256];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  {
+    int hv = (threadIdx.x < E) ? hist[threadIdx.x] : 0;
+    int ex = block_exclusive_scan_256(hv, scan_tmp);
+    if (threadIdx.x < E) seg_s[threadIdx.x] = ex;
+    if (blockIdx.x == 0 && threadIdx.x < E) seg_start_out[threadIdx.x] = ex;
+    if (blockIdx.x == 0 && threadIdx.x == WARPS * 32 - 1) seg_start_out[E] = ex + hv;  // total
+  }
+  __syncthreads();
+  const int r = blockIdx.x * WARPS + warp;
+  if (r >= R) return;
+  for (int e = lane; e < E; e += 32) off_s[warp][e] = seg_s[e] + range_off[(int64_t)e * R + r];
+  __syncwarp();
+  const int nvec = H >> 3;  // uint4 = 8 bf16
+  const int t_end = min(T, (r + 1) * RANGE_T);
+  for (int t = r * RANGE_T; t < t_end; ++t) {
+    int dest = 0;
+    if (lane < k) {
+      int e = topk_idx[(int64_t)t * k + lane];
+      dest = off_s[warp][e];
+      pos[(int64_t)t * k + lane] = dest;
+    }
+    __syncwarp();
+    if (lane < k) {
+      int e = topk_idx[(int64_t)t * k + lane];
+      off_s[warp][e] = dest + 1;  // experts of one token are distinct
+    }
+    __syncwarp();
+    const uint4* src = reinterpret_cast<const uint4*>(x + (int64_t)t * H);
+    constexpr int MAXV = 32;  // H <= 8192
+    uint4 buf[MAXV];
+#pragma unroll
+    for (int i = 0; i < MAXV; ++i) {
+      int c = lane + 32 * i;
+      if (c < nvec) buf[i] = __ldg(src + c);
+    }
+    for (int j = 0; j < k; ++j) {
+      int d = __shfl_sync(0xffffffffu, dest, j);
+      uint4* dst = reinterpret_cast<uint4*>(send + (int64_t)d * H);
+#pragma unroll
+      for (int i = 0; i < MAXV; ++i) {
+        int c = lane + 32 * i;
+        if (c < nvec) dst[c] = buf[i];
+      }
+    }
+  }
+}
+
+// K7 LocalReduce fused into combine (R7): one warp per token,
+// acc = fp32(s) (0 without shared experts); acc = fmaf(w_j, o[pos[t][j]], acc)
+// in slot order; y = bf16(acc).
+__global__ void __launch_bounds__(WARPS * 32)
+combine_kernel(const __nv_bfloat16* __restrict__ o, const __nv_bfloat16* __restrict__ s, int T, int H,
+               int k, const int32_t* __restrict__ pos, const float* __restrict__ topk_w,
+               __nv_bfloat16* __restrict__ y) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int t = blockIdx.x * WARPS + warp;
+  if (t >= T) return;
+  int prow = 0;
+  float pw = 0.f;
+  if (lane < k) {
+    prow = pos[(int64_t)t * k + lane];
+    pw = topk_w[(int64_t)t * k + lane];
+  }
+  const int nvec = H >> 3;
+  for (int c = lane; c < nvec; c += 32) {
+    float acc[8];
+    if (s) {
+      uint4 sv = __ldg(reinterpret_cast<const uint4*>(s + (int64_t)t * H) + c);
+      const __nv_bfloat16* sb = reinterpret_cast<const __nv_bfloat16*>(&sv);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) acc[i] = __bfloat162float(sb[i]);
+    } else {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) acc[i] = 0.f;
+    }
+    uint4 ov[8];
+    for (int j = 0; j < k; ++j) {
+      int row = __shfl_sync(0xffffffffu, prow, j);
+      ov[j & 7] = __ldg(reinterpret_cast<const uint4*>(o + (int64_t)row * H) + c);
+      float w = __shfl_sync(0xffffffffu, pw, j);
+      const __nv_bfloat16* ob = reinterpret_cast<const __nv_bfloat16*>(&ov[j & 7]);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) acc[i] = __fmaf_rn(w, __bfloat162float(ob[i]), acc[i]);
+    }
+    uint4 outv;
+    __nv_bfloat162* ob2 = reinterpret_cast<__nv_bfloat162*>(&outv);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) ob2[i] = __floats2bfloat162_rn(acc[2 * i], acc[2 * i + 1]);
+    reinterpret_cast<uint4*>(y + (int64_t)t * H)[c] = outv;
+  }
+}
+
+// Zero-pad copy of the router weight into a [256, H] buffer (create time).
+__global__ void pad_rows_kernel(const __nv_bfloat16* __restrict__ src, int rows, int H,
+                                __nv_bfloat16* __restrict__ dst, int rows_pad) {
+  int64_t n = (int64_t)rows_pad * H;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t rr = i / H;
+    dst[i] = rr < rows ? src[i] : __float2bfloat16(0.f);
+  }
+}
+
+}  // namespace
+
+int num_ranges(int64_t T) { return (int)((T + RANGE_T - 1) / RANGE_T); }
+
+int launch_gate_topk(const float* logits, int T, int E, int k, int norm_topk, float scale, int override_routing,
+                     int32_t* topk_idx, float* topk_w, int32_t* range_hist, cudaStream_t st) {
+  int R = num_ranges(T);
+  if (R == 0) return 0;
+  gate_topk_kernel<<<(R + WARPS - 1) / WARPS, WARPS * 32, 0, st>>>(logits, T, E, k, norm_topk, scale,
+                                                                   override_routing, topk_idx, topk_w,
+                                                                   range_hist, R);
+  return (int)cudaGetLastError();
+}
+
+int launch_range_scan(const int32_t* range_hist, int T, int E, int32_t* range_off, int32_t* hist, cudaStream_t st) {
+  int R = num_ranges(T);
+  if (R == 0) return (int)cudaMemsetAsync(hist, 0, sizeof(int32_t) * E, st);
+  range_scan_kernel<<<E, 1024, 0, st>>>(range_hist, R, range_off, hist);
+  return (int)cudaGetLastError();
+}
+
+int launch_permute(const void* x, int T, int H, int E, int k, const int32_t* topk_idx, const int32_t* range_off,
+                   const int32_t* hist, void* send, int32_t* pos, int32_t* seg_start, cudaStream_t st) {
+  int R = num_ranges(T);
+  int blocks = R == 0 ? 1 : (R + WARPS - 1) / WARPS;
+  permute_kernel<<<blocks, WARPS * 32, 0, st>>>((const __nv_bfloat16*)x, T, H, E, k, topk_idx, range_off, hist,
+                                                R, (__nv_bfloat16*)send, pos, seg_start);
+  return (int)cudaGetLastError();
+}
+
+int launch_combine(const void* o, const void* s, int T, int H, int k, const int32_t* pos, const float* topk_w,
+                   void* y, cudaStream_t st) {
+  if (T == 0) return 0;
+  combine_kernel<<<(T + WARPS - 1) / WARPS, WARPS * 32, 0, st>>>((const __nv_bfloat16*)o,
+                                                                 (const __nv_bfloat16*)s, T, H, k, pos, topk_w,
+                                                                 (__nv_bfloat16*)y);
+  return (int)cudaGetLastError();
+}
+
+int launch_pad_rows(const void* src, int rows, int H, void* dst, int rows_pad, cudaStream_t st) {
+  pad_rows_kernel<<<296, 256, 0, st>>>((const __nv_bfloat16*)src, rows, H, (__nv_bfloat16*)dst, rows_pad);
+  return (int)cudaGetLastError();
+}
+
+}  // namespace epsmoe
