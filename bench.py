@@ -1,0 +1,425 @@
+#!/usr/bin/env python
+"""bench.py — MoE-layer prefill tokens/s of the B200 EPS-MoE layer.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config dsv2|mixtral|dsv2_lite|tiny]
+                  [--skew S] [--chunks N] [--kind auto|grouped|dense] [--sm-gemm C]
+                  [--impl ours|reference]
+
+A step = one forward of the whole MoE layer (router, topKGating, split,
+[all2all dispatch], expert SwiGLU GEMMs, [all2all combine], weighted
+LocalReduce) over the config's global token batch, split evenly over the N
+ranks (strong scaling, EP = N).  Inputs are resident in HBM before the timed
+region; x alone (671 MB for DeepSeek-V2) exceeds the 126 MB L2, so no flush
+is needed between steps.  Prints ONE JSON line on rank 0.
+
+--impl reference times the CPU oracle (oracle/, the reference arm for this
+paper-only tier) on a bounded token sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "MoE-layer prefill tokens/s"
+UNIT = "tokens/s"
+FALLBACK_PEAKS = dict(hbm_gbs=6650.0, bf16_tflops=1590.0, bf16_tflops_sustained=1400.0, nvlink_gbs=770.0)
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--config", default="dsv2")
+    p.add_argument("--skew", type=float, default=0.0)
+    p.add_argument("--chunks", type=int, default=0, help="0 = planner")
+    p.add_argument("--kind", default="auto", choices=["auto", "grouped", "dense"])
+    p.add_argument("--sm-gemm", type=int, default=0)
+    p.add_argument("--tile-m", type=int, default=0, choices=[0, 128, 256])
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--cpu-sample", type=int, default=0, help="oracle sample tokens (0 = auto)")
+    p.add_argument("--e2e-steps", type=int, default=5)
+    p.add_argument("--seed", type=int, default=20241016)
+    return p.parse_args()
+
+
+def load_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        try:
+            d = json.load(open(path))
+            return d, "measured"
+        except Exception:
+            pass
+    return dict(FALLBACK_PEAKS), "fallback"
+
+
+def peak_tflops(peaks):
+    for key in ("bf16_tflops_sustained", "bf16_tflops"):
+        if key in peaks:
+            return float(peaks[key]), key
+    return FALLBACK_PEAKS["bf16_tflops_sustained"], "bf16_tflops_sustained"
+
+
+# ---------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = "index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active," \
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown," \
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap"
+
+    def __init__(self, gpu_index):
+        self.gpu_index = gpu_index
+        self.proc = None
+        self.path = f"/tmp/epsmoe_clocks_{os.getpid()}.csv"
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu_index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        rows = []
+        for line in open(self.path):
+            parts = [s.strip() for s in line.split(",")]
+            if len(parts) >= 9:
+                rows.append(parts)
+        os.unlink(self.path)
+        if not rows:
+            return None
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in rows for n, v in zip(names, r[5:9]) if v.lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows),
+                "power_w_median": statistics.median([float(r[3]) for r in rows if _isnum(r[3])]) if rows else None}
+
+
+def _isnum(s):
+    try:
+        float(s)
+        return True
+    except ValueError:
+        return False
+
+
+# ---------------------------------------------------------------- oracle (cpu_baseline / reference arm)
+def oracle_sample(cfg, seed, n_tokens, token0=0, skew=0.0, device_gen=False):
+    """Inputs for an oracle run on tokens [token0, token0+n).  Expert weights
+    come from gen/ (numpy, or its bit-identical device twin when device_gen,
+    which only speeds up input generation; tests/test_gpu_parity.py checks the
+    twin).  The oracle itself never touches the GPU."""
+    from gen import Inputs, TID_WDOWN, TID_WGATE, TID_WUP, MODE_UNIF, fill_bf16, unif_scale
+    E, k, H, F = cfg["E"], cfg["k"], cfg["H"], cfg["F"]
+    tok = np.arange(token0, token0 + n_tokens)
+    inp = Inputs(E=E, k=k, H=H, F=F, S=cfg["S"], Fs=cfg["Fs"], T=cfg["T"], seed=seed, experts=[], tokens=tok,
+                 skew=skew)
+    cache = {}
+    sH, sF = unif_scale(H), unif_scale(F)
+
+    def dev_fill(n, tid, base, scale):
+        import torch
+        from gen import device_fill_bf16
+        t = torch.empty(n, dtype=torch.int16, device="cuda")
+        device_fill_bf16(t.data_ptr(), n, seed, tid, base, MODE_UNIF, float(scale))
+        return t.cpu().numpy().view(np.uint16)
+
+    def expert_weights(e):
+        if e not in cache and device_gen:
+            cache[e] = (dev_fill(F * H, TID_WGATE, e * F * H, sH).reshape(F, H),
+                        dev_fill(F * H, TID_WUP, e * F * H, sH).reshape(F, H),
+                        dev_fill(H * F, TID_WDOWN, e * H * F, sF).reshape(H, F))
+        if e not in cache:
+            cache[e] = (fill_bf16(F * H, seed, TID_WGATE, e * F * H, MODE_UNIF, sH).reshape(F, H),
+                        fill_bf16(F * H, seed, TID_WUP, e * F * H, MODE_UNIF, sH).reshape(F, H),
+                        fill_bf16(H * F, seed, TID_WDOWN, e * H * F, MODE_UNIF, sF).reshape(H, F))
+        return cache[e]
+    return inp, expert_weights, cache
+
+
+def run_oracle_timed(cfg, inp, expert_weights, cache):
+    import oracle
+    # pre-generate the experts these tokens route to (generation is not timed)
+    idx, _ = oracle.topk_gating(oracle.router_logits(inp.x, inp.w_router, inp.router_bias), cfg["k"],
+                                cfg["norm_topk"])
+    for e in np.unique(idx):
+        expert_weights(int(e))
+    shared = (inp.ws_gate, inp.ws_up, inp.ws_down) if cfg["S"] else None
+    t0 = time.perf_counter()
+    oracle.moe_tokens(inp.x, inp.w_router, expert_weights, cfg["k"], cfg["norm_topk"], shared=shared,
+                      router_bias=inp.router_bias)
+    return time.perf_counter() - t0
+
+
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count()
+
+
+def cpu_baseline(cfg, seed, skew, sample=0):
+    n = sample or {"tiny": 256, "dsv2_lite": 16, "mixtral": 4, "dsv2": 8}.get(cfg["name"], 8)
+    inp, ew, cache = oracle_sample(cfg, seed, n, 0, skew, device_gen=True)
+    dt = run_oracle_timed(cfg, inp, ew, cache)
+    return {"value": n / dt, "unit": UNIT, "cores": host_cores(), "kind": "oracle",
+            "sample": f"first {n} tokens of the {cfg['name']} workload (all their experts + shared), "
+                      f"contract mode fp64 numpy, {dt:.1f} s"}
+
+
+def reference_arm(args, cfg):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    n = args.cpu_sample or {"tiny": 64, "dsv2_lite": 4, "mixtral": 1, "dsv2": 2}.get(cfg["name"], 2)
+    inp, ew, cache = oracle_sample(cfg, args.seed, n, 0, args.skew)
+    times = []
+    for i in range(args.warmup + args.steps):
+        dt = run_oracle_timed(cfg, inp, ew, cache)
+        if i >= args.warmup:
+            times.append(dt)
+    ms = 1e3 * sum(times) / len(times)
+    value = n / (ms / 1e3)
+    cores = host_cores()
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": cfg["name"], "tokens_per_step": n, "E": cfg["E"], "k": cfg["k"], "H": cfg["H"],
+                       "F": cfg["F"], "shared": cfg["S"], "skew": args.skew},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+                             "sample": f"{n} tokens per step of the {cfg['name']} workload"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- our arm
+def token_shards(T, D):
+    """DP token shards: rank r owns [start[r], start[r+1]); first T mod D ranks get one extra (R12)."""
+    base, rem = divmod(T, D)
+    return np.concatenate([[0], np.cumsum([base + (1 if r < rem else 0) for r in range(D)])]).astype(np.int64)
+
+
+def ours(args, cfg):
+    import torch
+    import torch.distributed as dist
+
+    from gen import (MODE_UNIF, TID_WDOWN, TID_WGATE, TID_WR, TID_WS_DOWN, TID_WS_GATE, TID_WS_UP, TID_WUP, TID_X,
+                     device_fill_bf16, router_skew_bias, unif_scale)
+    from paper_2410_12247_b200 import MOE_GEMM_AUTO, MOE_GEMM_DENSE, MOE_GEMM_GROUPED, MoELayer, make_plan
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    E, k, H, F, S, Fs, T = cfg["E"], cfg["k"], cfg["H"], cfg["F"], cfg["S"], cfg["Fs"], cfg["T"]
+    D = world
+    if E % D:
+        raise SystemExit(f"E={E} not divisible by {D}")
+    E_loc = E // D
+    starts = token_shards(T, D)
+    t0, T_loc = int(starts[rank]), int(starts[rank + 1] - starts[rank])
+    seed = args.seed
+
+    def gen(shape, tid, base, scale):
+        t = torch.empty(shape, dtype=torch.bfloat16, device=dev)
+        device_fill_bf16(t.data_ptr(), t.numel(), seed, tid, base, MODE_UNIF, float(scale))
+        return t
+
+    sH, sF = unif_scale(H), unif_scale(F)
+    e0 = rank * E_loc
+    w = dict(w_router=gen((E, H), TID_WR, 0, sH),
+             w_gate=gen((E_loc, F, H), TID_WGATE, e0 * F * H, sH),
+             w_up=gen((E_loc, F, H), TID_WUP, e0 * F * H, sH),
+             w_down=gen((E_loc, H, F), TID_WDOWN, e0 * H * F, sF))
+    SF = S * Fs
+    if SF:
+        w.update(ws_gate=gen((SF, H), TID_WS_GATE, 0, sH), ws_up=gen((SF, H), TID_WS_UP, 0, sH),
+                 ws_down=gen((H, SF), TID_WS_DOWN, 0, unif_scale(SF)))
+    if args.skew:
+        w["router_bias"] = torch.from_numpy(router_skew_bias(E, args.skew, seed)).to(dev)
+    x = gen((T_loc, H), TID_X, t0 * H, unif_scale(1))
+    y = torch.empty_like(x)
+
+    uid_d = uid_c = None
+    if D > 1:
+        ids = [MoELayer.unique_id(), MoELayer.unique_id()] if rank == 0 else [None, None]
+        dist.broadcast_object_list(ids, src=0)
+        uid_d, uid_c = ids
+    layer = MoELayer(E, k, H, F, w, S=S, Fs=Fs, ep=D, rank=rank, max_tokens=T_loc, norm_topk=cfg["norm_topk"],
+                     uid_dispatch=uid_d, uid_combine=uid_c, device=dev)
+    plan = None
+    if args.chunks or args.kind != "auto" or args.sm_gemm or args.tile_m:
+        kind = {"auto": MOE_GEMM_AUTO, "grouped": MOE_GEMM_GROUPED, "dense": MOE_GEMM_DENSE}[args.kind]
+        plan = make_plan(max(1, args.chunks), kind, args.sm_gemm, tile_m=args.tile_m)
+        if not args.chunks:
+            plan.num_chunks = layer.plan(T).num_chunks
+    stream = torch.cuda.current_stream(dev)
+
+    for _ in range(args.warmup):
+        layer.forward(x, y, plan=plan)
+    torch.cuda.synchronize()
+
+    layer.set_profiling(True)
+    gpu_idx = local
+    vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+    if vis:
+        try:
+            gpu_idx = int(vis.split(",")[local])
+        except ValueError:
+            pass
+    clocks = ClockSampler(gpu_idx)
+    clocks.start()
+    time.sleep(0.3)
+    if D > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    stage_sum, stage_cnt = {}, {}
+    launches = 0
+    ev0.record(stream)
+    for _ in range(args.steps):
+        layer.forward(x, y, plan=plan)
+        launches += layer.last_launches()
+        for name, (ms, cnt) in layer.stage_ms().items():
+            stage_sum[name] = stage_sum.get(name, 0.0) + ms
+            stage_cnt[name] = stage_cnt.get(name, 0) + cnt
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    if D > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    layer.set_profiling(False)
+    ms_total = ev0.elapsed_time(ev1)
+    t = torch.tensor([ms_total], dtype=torch.float64, device=dev)
+    if D > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_step = float(t.item()) / args.steps
+    value = T / (ms_step / 1e3)
+
+    # ---- realised routing of one step (for the algorithmic FLOPs / bytes)
+    d, bufs = layer.debug_buffers(T_loc)
+    layer.forward(x, y, plan=plan, debug=d)
+    torch.cuda.synchronize()
+    ghist = bufs["global_hist"].astype(np.int64)            # [D, E]
+    plan_used = bufs["plan_used"].as_dict()
+    rows_local = [int(ghist[:, r * E_loc:(r + 1) * E_loc].sum()) for r in range(D)]
+    rows_me = rows_local[rank]
+
+    # ---- roofline of the dominant kernel: GateUpGemm + SiluAct (tcgen05)
+    peaks, peak_src = load_peaks()
+    ptf, pkey = peak_tflops(peaks)
+    gu_ms = stage_sum.get("gateup", 0.0) / args.steps
+    gu_flop = 4.0 * H * F * rows_me
+    achieved = gu_flop / (gu_ms / 1e3) / 1e12 if gu_ms > 0 else None
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get(cfg["name"], {}).get("gateup_dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    roofline = {"bound": "tensor", "kernel": "gemm_kernel<EPI_SWIGLU> (GateUpGemm+SiluAct)",
+                "achieved": achieved, "peak": ptf, "unit": "TFLOP/s",
+                "frac": (achieved / ptf) if achieved else None, "traffic": traffic,
+                "peak_source": f"{peak_src} {pkey}",
+                "algorithmic": f"4*H*F*rows = {gu_flop:.4g} FLOP per step over {stage_cnt.get('gateup', 0) // args.steps} launch(es)"}
+
+    # ---- layer roofline: max(expert+shared+router FLOPs / peak, all2all bytes / NVLink), max over ranks
+    flops_rank = [6.0 * H * F * rl + 6.0 * H * SF * (starts[r + 1] - starts[r]) + 2.0 * H * E * (starts[r + 1] - starts[r])
+                  for r, rl in enumerate(rows_local)]
+    a2a_bytes = []
+    for r in range(D):
+        sent = int(ghist[r].sum() - ghist[r, r * E_loc:(r + 1) * E_loc].sum())
+        recv = int(ghist[:, r * E_loc:(r + 1) * E_loc].sum() - ghist[r, r * E_loc:(r + 1) * E_loc].sum())
+        a2a_bytes.append(2.0 * H * 2 * max(sent, recv))
+    nvl = float(peaks.get("nvlink_gbs", FALLBACK_PEAKS["nvlink_gbs"]))
+    t_roof = max(max(flops_rank) / (ptf * 1e12), max(a2a_bytes) / (nvl * 1e9) if D > 1 else 0.0) * 1e3
+    layer_roofline = {"bound": "tensor" if max(flops_rank) / (ptf * 1e12) >= max(a2a_bytes) / (nvl * 1e9) else "nvlink",
+                      "t_roof_ms": t_roof, "t_layer_ms": ms_step, "frac": t_roof / ms_step,
+                      "flops_max_rank": max(flops_rank), "a2a_bytes_max_rank": max(a2a_bytes),
+                      "achieved_tflops": max(flops_rank) / (ms_step / 1e3) / 1e12}
+
+    # ---- e2e through the public host-buffer entry point (H2D + layer + D2H per step)
+    xh = x.cpu().pin_memory()
+    yh = torch.empty_like(xh).pin_memory()
+    layer.forward_host(xh, yh, plan=plan)
+    if D > 1:
+        dist.barrier()
+    e_ev0, e_ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e_ev0.record(stream)
+    for _ in range(args.e2e_steps):
+        layer.forward_host(xh, yh, plan=plan)
+    e_ev1.record(stream)
+    torch.cuda.synchronize()
+    te = torch.tensor([e_ev0.elapsed_time(e_ev1)], dtype=torch.float64, device=dev)
+    if D > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_ms = float(te.item()) / args.e2e_steps
+    e2e = {"value": T / (e2e_ms / 1e3), "unit": UNIT, "ms_per_step": e2e_ms,
+           "h2d_bytes_per_step": int(T_loc * H * 2), "d2h_bytes_per_step": int(T_loc * H * 2),
+           "api": "moe_layer_forward_host (pinned host x/y)"}
+
+    stages = {n: round(v / args.steps, 4) for n, v in stage_sum.items()}
+    cpu = None
+    if rank == 0 and D == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(cfg, seed, args.skew, args.cpu_sample)
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": D, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+                "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded counter-hash; x~U(-sqrt3,sqrt3), "
+                "W~U(-sqrt3,sqrt3)/sqrt(fan_in), bf16; random-init weights of the config's shape)",
+                "config": {"workload": cfg["name"], "E": E, "k": k, "H": H, "F": F, "shared": S, "shared_ffn": Fs,
+                           "global_tokens": T, "ep": D, "parallelism": f"ep{D}" + (f"+dp{D}" if D > 1 else ""),
+                           "skew": args.skew, "l2": "inputs > L2 (x alone %.0f MB), no flush" % (T_loc * H * 2 / 1e6),
+                           "plan": plan_used},
+                "roofline": roofline, "layer_roofline": layer_roofline,
+                "exposed_a2a_ms": stages.get("exposed_a2a", 0.0), "stages_ms": stages,
+                "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk}
+        print(json.dumps(line), flush=True)
+    layer.close()
+    if D > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    from gen import CONFIGS
+    if args.config not in CONFIGS:
+        raise SystemExit(f"unknown config {args.config}; one of {list(CONFIGS)}")
+    cfg = dict(CONFIGS[args.config], name=args.config)
+    if args.impl == "reference":
+        reference_arm(args, cfg)
+    else:
+        ours(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

@@ -153,15 +153,26 @@ class Inputs:
             self.x = np.stack([fill_bf16(H, seed, TID_X, int(t) * H, MODE_UNIF, sx) for t in tok]) \
                 if tokens is not None else fill_bf16(T * H, seed, TID_X, 0, MODE_UNIF, sx).reshape(T, H)
             self.w_router = fill_bf16(E * H, seed, TID_WR, 0, MODE_UNIF, unif_scale(H)).reshape(E, H)
-        self.experts = np.arange(E) if experts is None else np.asarray(experts)
+        self.experts = np.arange(E) if experts is None else np.asarray(experts, dtype=np.int64)
         sH, sF = unif_scale(H), unif_scale(F)
+        if len(self.experts) == 0:
+            self.w_gate = self.w_up = self.w_down = None
+        else:
+            self._gen_experts(seed, sH, sF)
+        self._gen_shared(seed, sH)
+        self.router_bias = router_skew_bias(E, skew, seed, skew_identity) if skew else None
+
+    def _gen_experts(self, seed, sH, sF):
+        E, H, F = self.E, self.H, self.F
         self.w_gate = np.stack([fill_bf16(F * H, seed, TID_WGATE, int(e) * F * H, MODE_UNIF, sH)
                                 for e in self.experts]).reshape(len(self.experts), F, H)
         self.w_up = np.stack([fill_bf16(F * H, seed, TID_WUP, int(e) * F * H, MODE_UNIF, sH)
                               for e in self.experts]).reshape(len(self.experts), F, H)
         self.w_down = np.stack([fill_bf16(H * F, seed, TID_WDOWN, int(e) * H * F, MODE_UNIF, sF)
                                 for e in self.experts]).reshape(len(self.experts), H, F)
-        SF = S * Fs
+
+    def _gen_shared(self, seed, sH):
+        H, SF = self.H, self.S * self.Fs
         if SF:
             sS = unif_scale(SF)
             self.ws_gate = fill_bf16(SF * H, seed, TID_WS_GATE, 0, MODE_UNIF, sH).reshape(SF, H)
@@ -169,7 +180,6 @@ class Inputs:
             self.ws_down = fill_bf16(H * SF, seed, TID_WS_DOWN, 0, MODE_UNIF, sS).reshape(H, SF)
         else:
             self.ws_gate = self.ws_up = self.ws_down = None
-        self.router_bias = router_skew_bias(E, skew, seed, skew_identity) if skew else None
 
     def duplicate_router_rows(self, e_src: int, e_dst: int) -> None:
         """Tie fixture: W_r[e_dst] := W_r[e_src], so the pair always ties."""

@@ -108,6 +108,9 @@ typedef struct {
   float pred_k_ms;      /* R(N) = kN + b: slope    */
   float pred_b_ms;      /*                 intercept                              */
   float pred_gain_ms;   /* G = C - b - (C/N + kN)    */
+  int32_t tile_m;       /* expert-GEMM tile rows: 256 (CTA pair, cta_group::2),
+                           128 (single CTA), 0 = by load (256 if the chunk's mean
+                           rows per expert >= 512)                               */
 } moe_plan_t;
 
 /* Measured cost model behind moe_plan_pipeline (calibrated on B200 by
@@ -210,6 +213,26 @@ moe_status_t moe_layer_forward(moe_layer_t* layer, const void* x, int64_t T_loc,
 moe_status_t moe_layer_forward_host(moe_layer_t* layer, const void* x_host, int64_t T_loc, void* y_host,
                                     const moe_plan_t* plan, void* stream);
 
+/* Per-stage device timing of the last forward (CUDA events recorded on the
+ * stream each stage is launched on).  enable = 1 turns recording on. */
+enum {
+  MOE_STAGE_ROUTER = 0,  /* K1 router GEMM                                  */
+  MOE_STAGE_ROUTE = 1,   /* K2 gating + histogram + scan + K3 permute        */
+  MOE_STAGE_SHARED = 2,  /* shared-expert GEMMs                              */
+  MOE_STAGE_GATEUP = 3,  /* GateUpGemm + SiluAct, summed over launches       */
+  MOE_STAGE_DOWN = 4,    /* DownGemm, summed over launches                   */
+  MOE_STAGE_COMBINE = 5, /* weighted unpermute (LocalReduce)                 */
+  MOE_STAGE_DISPATCH = 6,/* all2all dispatch, summed over chunks (ep > 1)    */
+  MOE_STAGE_COMB_A2A = 7,/* all2all combine, summed over chunks (ep > 1)     */
+  MOE_STAGE_TOTAL = 8,   /* whole forward on the caller's stream             */
+  MOE_STAGE_EXPOSED_A2A = 9, /* all2all time not covered by compute (ep > 1) */
+  MOE_NUM_STAGES = 10
+};
+moe_status_t moe_layer_set_profiling(moe_layer_t* layer, int32_t enable);
+/* Waits for the last forward's events; ms[MOE_NUM_STAGES] (host) in ms;
+ * counts[MOE_NUM_STAGES] (host, may be NULL) = launches timed per stage. */
+moe_status_t moe_layer_stage_ms(const moe_layer_t* layer, float* ms, int32_t* counts);
+
 /* Number of kernels the last forward launched (for the bench's gpu_launches). */
 int32_t moe_layer_last_launches(const moe_layer_t* layer);
 
@@ -224,11 +247,12 @@ const char* moe_last_error(void);
  *   epi 2 (fp32):        out[r, 0:n] = fp32(A_r B0_g^T) (+ bias)
  * for rows r of group g in [row_start[g], row_start[g] + row_count[g]),
  * B*_g = rows [g*b_group_rows, g*b_group_rows + n) (epi 0/1) of B0/B1 [.., kdim].
- * row_start/row_count: DEVICE int32 [groups].  num_ctas: persistent grid. */
+ * row_start/row_count: DEVICE int32 [groups].  num_ctas: persistent grid.
+ * tile_m: 128 (single-CTA tiles) or 256 (CTA-pair tiles, cta_group::2). */
 moe_status_t moe_gemm_grouped(int32_t epi, const void* A, int64_t a_rows, const void* B0, const void* B1,
                               int64_t b_rows, int32_t b_group_rows, int32_t kdim, int32_t n, void* out,
                               int64_t ldo, const float* bias, int32_t groups, const int32_t* row_start,
-                              const int32_t* row_count, int32_t num_ctas, void* stream);
+                              const int32_t* row_count, int32_t num_ctas, int32_t tile_m, void* stream);
 
 #ifdef __cplusplus
 }

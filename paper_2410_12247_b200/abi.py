@@ -18,6 +18,8 @@ MOE_MAX_CHUNKS = 64
 MOE_COST_POINTS = 12
 
 MOE_GEMM_AUTO, MOE_GEMM_GROUPED, MOE_GEMM_DENSE = 0, 1, 2
+STAGES = ["router", "route", "shared", "gateup", "down", "combine", "dispatch_a2a", "combine_a2a", "total",
+          "exposed_a2a"]
 STATUS = {0: "MOE_OK", 1: "MOE_ERR_INVALID", 2: "MOE_ERR_UNSUPPORTED", 3: "MOE_ERR_CAPACITY",
           4: "MOE_ERR_CUDA", 5: "MOE_ERR_NCCL", 6: "MOE_ERR_MISMATCH"}
 
@@ -41,7 +43,7 @@ class moe_plan_t(C.Structure):
                 ("group_begin", C.c_int32 * (MOE_MAX_CHUNKS + 1)),
                 ("expert_kind", C.c_uint8 * MOE_MAX_EXPERTS),
                 ("pred_comm_ms", C.c_float), ("pred_comp_ms", C.c_float), ("pred_k_ms", C.c_float),
-                ("pred_b_ms", C.c_float), ("pred_gain_ms", C.c_float)]
+                ("pred_b_ms", C.c_float), ("pred_gain_ms", C.c_float), ("tile_m", C.c_int32)]
 
     def as_dict(self):
         n = self.num_chunks
@@ -49,7 +51,8 @@ class moe_plan_t(C.Structure):
                     sm_gemm=self.sm_gemm, comm_ctas=self.comm_ctas,
                     group_begin=list(self.group_begin[:n + 1]),
                     pred_comm_ms=self.pred_comm_ms, pred_comp_ms=self.pred_comp_ms,
-                    pred_k_ms=self.pred_k_ms, pred_b_ms=self.pred_b_ms, pred_gain_ms=self.pred_gain_ms)
+                    pred_k_ms=self.pred_k_ms, pred_b_ms=self.pred_b_ms, pred_gain_ms=self.pred_gain_ms,
+                    tile_m=self.tile_m)
 
 
 class moe_cost_model_t(C.Structure):
@@ -81,10 +84,12 @@ _SIGS = {
     "moe_layer_forward_host": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p,
                                          C.POINTER(moe_plan_t), C.c_void_p]),
     "moe_layer_last_launches": (C.c_int32, [C.c_void_p]),
+    "moe_layer_set_profiling": (C.c_int, [C.c_void_p, C.c_int32]),
+    "moe_layer_stage_ms": (C.c_int, [C.c_void_p, C.POINTER(C.c_float), C.POINTER(C.c_int32)]),
     "moe_last_error": (C.c_char_p, []),
     "moe_gemm_grouped": (C.c_int, [C.c_int32, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_int64,
                                    C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_int64, C.c_void_p,
-                                   C.c_int32, C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p]),
+                                   C.c_int32, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p]),
 }
 
 _LIB = None
@@ -133,8 +138,9 @@ def plan_compute(cfg: moe_config_t, global_tokens: int, global_hist=None, cost: 
     return plan
 
 
-def make_plan(num_chunks=1, gemm_kind=MOE_GEMM_GROUPED, sm_gemm=0, comm_ctas=0):
+def make_plan(num_chunks=1, gemm_kind=MOE_GEMM_GROUPED, sm_gemm=0, comm_ctas=0, tile_m=0):
     p = moe_plan_t()
+    p.tile_m = tile_m
     p.num_chunks = num_chunks
     p.token_slices = 1
     p.gemm_kind = gemm_kind

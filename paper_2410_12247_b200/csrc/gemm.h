@@ -34,6 +34,7 @@ struct GemmArgs {
   const int32_t* row_count;  // device [G] (nullptr -> single group of m_single rows)
   int m_single;
   int num_ctas;            // persistent grid size (SM budget)
+  int cta_pair;            // 1: 256-row tiles on CTA pairs (cta_group::2); 0: 128-row tiles
 };
 
 // Launch on `stream`.  Returns a cudaError_t-compatible code (0 = success).

@@ -1,24 +1,28 @@
 // Expert FFN GEMMs on 5th-gen tensor cores (sm_100a): persistent, warp-
-// specialised, TMA -> 4-stage smem ring -> tcgen05.mma (M=128, N=256, K=16,
-// bf16 in / fp32 accumulate in TMEM) -> double-buffered TMEM accumulators ->
-// fused epilogue.  One kernel family serves every GEMM of the layer:
+// specialised, TMA -> smem ring -> tcgen05.mma (bf16 in / fp32 accumulate in
+// TMEM) -> double-buffered TMEM accumulators -> fused epilogue.
 //
-//   GateUpGemm + SiluAct  EPI_SWIGLU: B tile = 128 rows of W_gate
-//        and 128 rows of W_up of the same expert (two TMA loads, no weight
-//        repacking); epilogue h = bf16(silu(g) * u).
+// Two tile shapes (template CG):
+//   CG = 1: one CTA per 128x256 tile, cta_group::1, 4 x 48 KB stages.
+//   CG = 2: a CTA pair (cluster of 2) per 256x256 tile, cta_group::2: each CTA
+//           TMA-loads its 128 rows of A and half (128 rows) of B, the leader
+//           CTA issues M=256 MMAs that read both CTAs' smem and write each
+//           CTA's own TMEM; 6 x 32 KB stages per CTA.  Per MAC this halves B's
+//           smem/L2 traffic (the paper's DenseGemm regime: large per-expert M).
+//
+// One kernel family serves every GEMM of the layer:
+//   GateUpGemm + SiluAct  EPI_SWIGLU: the 256 accumulator columns
+//        are 128 rows of W_gate and 128 rows of W_up of one expert (two TMA
+//        boxes; no weight repacking); epilogue h = bf16(silu(g) * u).
 //   DownGemm                  EPI_BF16:  o = bf16(acc).
 //   Router                    EPI_F32:   logits = fp32(acc) + beta.
-//
-// "GroupGemm" vs "DenseGemm" is a scheduling choice on B200:
-// one launch over all tiles of a chunk's experts vs one launch per expert; the
-// kernel is the same (see layer.cu).  Group row counts are read from device
-// memory, so no host round trip is needed to size the launch (persistent grid).
+// Group row counts are read from device memory, so no host round trip sizes
+// the launch (persistent grid over a device-computed tile prefix).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
-#include <cstdio>
 #include <mutex>
 
 #include "gemm.h"
@@ -27,15 +31,24 @@
 namespace epsmoe {
 namespace {
 
-constexpr int BM = 128, BN = 256, BK = 64, STAGES = 4;
-constexpr int A_BYTES = BM * BK * 2;  // 16 KB
-constexpr int B_BYTES = BN * BK * 2;  // 32 KB
+constexpr int BM = 128;         // rows per CTA
+constexpr int BN = 256;         // accumulator columns per tile
+constexpr int BK = 64;          // K per stage (one 128 B swizzle atom of bf16)
 constexpr int MAX_G = 256;
-constexpr int NUM_THREADS = 192;      // w0 TMA, w1 MMA + TMEM owner, w2..5 epilogue
-constexpr int TMEM_COLS = 512;        // 2 x 256-column fp32 accumulators
+constexpr int NUM_THREADS = 192;  // w0 TMA, w1 MMA + TMEM owner, w2..5 epilogue
+constexpr int TMEM_COLS = 512;    // 2 x 256-column fp32 accumulators
+
+template <int CG>
+struct Cfg {
+  static constexpr int TILE_M = BM * CG;
+  static constexpr int B_ROWS = BN / CG;              // B rows each CTA loads per stage
+  static constexpr int A_BYTES = BM * BK * 2;         // 16 KB
+  static constexpr int B_BYTES = B_ROWS * BK * 2;     // 32 KB (CG=1) / 16 KB (CG=2)
+  static constexpr int STAGES = (CG == 1) ? 4 : 6;
+};
 
 struct KParams {
-  int epi, K, N, G, m_single, b_group_rows, b_base;
+  int K, N, G, m_single, b_group_rows, b_base;
   int64_t ldo;
   void* out;
   const float* bias;
@@ -43,9 +56,10 @@ struct KParams {
   const int32_t* row_count;
 };
 
+template <int CG>
 struct __align__(8) SmemTail {
-  uint64_t full[STAGES];
-  uint64_t empty[STAGES];
+  uint64_t full[Cfg<CG>::STAGES];
+  uint64_t empty[Cfg<CG>::STAGES];
   uint64_t tfull[2];
   uint64_t tempty[2];
   uint32_t tmem_holder;
@@ -54,7 +68,10 @@ struct __align__(8) SmemTail {
   int32_t gcount[MAX_G];
 };
 
-constexpr size_t SMEM_BYTES = 1024 /*align slack*/ + STAGES * (A_BYTES + B_BYTES) + sizeof(SmemTail);
+template <int CG>
+constexpr size_t smem_bytes() {
+  return 1024 + Cfg<CG>::STAGES * (Cfg<CG>::A_BYTES + Cfg<CG>::B_BYTES) + sizeof(SmemTail<CG>);
+}
 
 __device__ __forceinline__ float silu_f32(float g) { return g / (1.0f + expf(-g)); }
 
@@ -63,8 +80,9 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   return *reinterpret_cast<uint32_t*>(&v);
 }
 
-__device__ __forceinline__ void decode_tile(const SmemTail& s, int G, int n_tiles, int t, int& g,
-                                            int& mt, int& nt) {
+template <int CG>
+__device__ __forceinline__ void decode_tile(const SmemTail<CG>& s, int G, int n_tiles, int t, int& g, int& mt,
+                                            int& nt) {
   int lo = 0, hi = G - 1;  // largest g with tile_prefix[g] <= t
   while (lo < hi) {
     int mid = (lo + hi + 1) >> 1;
@@ -76,20 +94,24 @@ __device__ __forceinline__ void decode_tile(const SmemTail& s, int G, int n_tile
   nt = local - mt * n_tiles;
 }
 
-template <int EPI>
+template <int EPI, int CG>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
 gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB0,
             const __grid_constant__ CUtensorMap tmB1, const KParams p) {
+  using C = Cfg<CG>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
-  uint8_t* sB = smem + STAGES * A_BYTES;
-  SmemTail& st = *reinterpret_cast<SmemTail*>(smem + STAGES * (A_BYTES + B_BYTES));
+  uint8_t* sB = smem + C::STAGES * C::A_BYTES;
+  SmemTail<CG>& st = *reinterpret_cast<SmemTail<CG>*>(smem + C::STAGES * (C::A_BYTES + C::B_BYTES));
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  const uint32_t rank = (CG == 2) ? ptx::cluster_ctarank() : 0;  // CTA rank inside the pair
+  const int unit = blockIdx.x / CG;                               // pair (or CTA) id
+  const int num_units = gridDim.x / CG;
   const int G = p.row_count ? p.G : 1;
-  const int n_out_tile = (EPI == EPI_SWIGLU) ? 128 : BN;     // output columns per tile
+  const int n_out_tile = (EPI == EPI_SWIGLU) ? 128 : BN;  // output columns per tile
   const int n_tiles = (p.N + n_out_tile - 1) / n_out_tile;
   const int num_kb = p.K / BK;
 
@@ -99,17 +121,17 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
     st.gstart[g] = p.row_start ? p.row_start[g] : 0;
   }
   if (threadIdx.x == 0) {
-    for (int i = 0; i < STAGES; ++i) {
+    for (int i = 0; i < C::STAGES; ++i) {
       ptx::mbar_init(ptx::smem_u32(&st.full[i]), 1);
       ptx::mbar_init(ptx::smem_u32(&st.empty[i]), 1);
     }
     for (int i = 0; i < 2; ++i) {
       ptx::mbar_init(ptx::smem_u32(&st.tfull[i]), 1);
-      ptx::mbar_init(ptx::smem_u32(&st.tempty[i]), 128);
+      ptx::mbar_init(ptx::smem_u32(&st.tempty[i]), 4 * CG);  // one arrive per epilogue warp (both CTAs)
     }
     ptx::fence_barrier_init();
   }
-  if (warp == 1) ptx::tmem_alloc<TMEM_COLS>(ptx::smem_u32(&st.tmem_holder));
+  if (warp == 1) ptx::tmem_alloc<TMEM_COLS, CG>(ptx::smem_u32(&st.tmem_holder));
   if (warp == 0 && lane == 0) {
     ptx::tma_prefetch_desc(&tmA);
     ptx::tma_prefetch_desc(&tmB0);
@@ -123,7 +145,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
 #pragma unroll
     for (int i = 0; i < PER; ++i) {
       int g = lane * PER + i;
-      int tiles = (g < G) ? ((st.gcount[g] + BM - 1) / BM) * n_tiles : 0;
+      int tiles = (g < G) ? ((st.gcount[g] + C::TILE_M - 1) / C::TILE_M) * n_tiles : 0;
       local[i] = sum;
       sum += tiles;
     }
@@ -143,42 +165,53 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
   }
   ptx::tc_fence_before();
   __syncthreads();
+  if constexpr (CG == 2) ptx::cluster_sync();  // peer barriers initialised before any remote signal
   ptx::tc_fence_after();
   const uint32_t tmem_base = st.tmem_holder;
   const int total = st.tile_prefix[G];
 
   if (warp == 0) {
-    // ===================== TMA producer =====================
+    // ===================== TMA producer (each CTA loads its own halves) =====================
     if (lane == 0) {
       uint32_t stage = 0, phase = 0;
-      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+      for (int t = unit; t < total; t += num_units) {
         int g, mt, nt;
         decode_tile(st, G, n_tiles, t, g, mt, nt);
-        const int a_row = st.gstart[g] + mt * BM;
-        const int b_row = (p.b_base + g) * p.b_group_rows + nt * n_out_tile;
+        const int a_row = st.gstart[g] + mt * C::TILE_M + (int)rank * BM;
+        const int b_row0 = (p.b_base + g) * p.b_group_rows + nt * n_out_tile;
         for (int kb = 0; kb < num_kb; ++kb) {
           ptx::mbar_wait(ptx::smem_u32(&st.empty[stage]), phase ^ 1);
           const uint32_t fb = ptx::smem_u32(&st.full[stage]);
-          ptx::mbar_arrive_expect_tx(fb, A_BYTES + B_BYTES);
-          const uint32_t a_dst = ptx::smem_u32(sA + stage * A_BYTES);
-          const uint32_t b_dst = ptx::smem_u32(sB + stage * B_BYTES);
-          ptx::tma_load_2d(a_dst, &tmA, fb, kb * BK, a_row);
-          if (EPI == EPI_SWIGLU) {
-            ptx::tma_load_2d(b_dst, &tmB0, fb, kb * BK, b_row);
-            ptx::tma_load_2d(b_dst + B_BYTES / 2, &tmB1, fb, kb * BK, b_row);
+          const uint32_t a_dst = ptx::smem_u32(sA + stage * C::A_BYTES);
+          const uint32_t b_dst = ptx::smem_u32(sB + stage * C::B_BYTES);
+          if constexpr (CG == 1) {
+            ptx::mbar_arrive_expect_tx(fb, C::A_BYTES + C::B_BYTES);
+            ptx::tma_load_2d(a_dst, &tmA, fb, kb * BK, a_row);
+            if (EPI == EPI_SWIGLU) {
+              ptx::tma_load_2d(b_dst, &tmB0, fb, kb * BK, b_row0);
+              ptx::tma_load_2d(b_dst + C::B_BYTES / 2, &tmB1, fb, kb * BK, b_row0);
+            } else {
+              ptx::tma_load_2d(b_dst, &tmB0, fb, kb * BK, b_row0);
+            }
           } else {
-            ptx::tma_load_2d(b_dst, &tmB0, fb, kb * BK, b_row);
+            // the leader's full barrier counts both CTAs' bytes
+            if (rank == 0) ptx::mbar_arrive_expect_tx(fb, 2 * (C::A_BYTES + C::B_BYTES));
+            ptx::tma_load_2d_pair(a_dst, &tmA, fb, kb * BK, a_row);
+            if (EPI == EPI_SWIGLU)  // CTA0: gate rows -> acc cols [0,128); CTA1: up rows -> [128,256)
+              ptx::tma_load_2d_pair(b_dst, rank == 0 ? &tmB0 : &tmB1, fb, kb * BK, b_row0);
+            else
+              ptx::tma_load_2d_pair(b_dst, &tmB0, fb, kb * BK, b_row0 + (int)rank * C::B_ROWS);
           }
-          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+          if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
         }
       }
     }
   } else if (warp == 1) {
-    // ===================== MMA issuer (one thread) =====================
-    if (lane == 0) {
-      constexpr uint32_t idesc = ptx::idesc_bf16_f32(BM, BN);
+    // ===================== MMA issuer (one thread of the leader CTA) =====================
+    if (lane == 0 && rank == 0) {
+      constexpr uint32_t idesc = ptx::idesc_bf16_f32(C::TILE_M, BN);
       uint32_t stage = 0, phase = 0, iter = 0;
-      for (int t = blockIdx.x; t < total; t += gridDim.x, ++iter) {
+      for (int t = unit; t < total; t += num_units, ++iter) {
         const uint32_t acc = iter & 1, accph = (iter >> 1) & 1;
         ptx::mbar_wait(ptx::smem_u32(&st.tempty[acc]), accph ^ 1);
         ptx::tc_fence_after();
@@ -186,30 +219,37 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
         for (int kb = 0; kb < num_kb; ++kb) {
           ptx::mbar_wait(ptx::smem_u32(&st.full[stage]), phase);
           ptx::tc_fence_after();
-          const uint64_t adesc = ptx::sdesc_k_sw128(ptx::smem_u32(sA + stage * A_BYTES));
-          const uint64_t bdesc = ptx::sdesc_k_sw128(ptx::smem_u32(sB + stage * B_BYTES));
+          const uint64_t adesc = ptx::sdesc_k_sw128(ptx::smem_u32(sA + stage * C::A_BYTES));
+          const uint64_t bdesc = ptx::sdesc_k_sw128(ptx::smem_u32(sB + stage * C::B_BYTES));
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k) {
             // advance 16 bf16 = 32 B along K inside the 128 B swizzle atom
-            ptx::mma_bf16_ss(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (kb | k) != 0);
+            if constexpr (CG == 1)
+              ptx::mma_bf16_ss(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (kb | k) != 0);
+            else
+              ptx::mma_bf16_ss_pair(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (kb | k) != 0);
           }
-          ptx::mma_commit(ptx::smem_u32(&st.empty[stage]));
-          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+          if constexpr (CG == 1) ptx::mma_commit(ptx::smem_u32(&st.empty[stage]));
+          else ptx::mma_commit_pair(ptx::smem_u32(&st.empty[stage]), 0x3);
+          if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
         }
-        ptx::mma_commit(ptx::smem_u32(&st.tfull[acc]));
+        if constexpr (CG == 1) ptx::mma_commit(ptx::smem_u32(&st.tfull[acc]));
+        else ptx::mma_commit_pair(ptx::smem_u32(&st.tfull[acc]), 0x3);
       }
     }
   } else {
     // ===================== epilogue (4 warps, TMEM lane quadrant = warp % 4) =====
     const int q = warp & 3;
+    const uint32_t tempty_leader0 = (CG == 2) ? ptx::mapa(ptx::smem_u32(&st.tempty[0]), 0) : 0;
+    const uint32_t tempty_leader1 = (CG == 2) ? ptx::mapa(ptx::smem_u32(&st.tempty[1]), 0) : 0;
     uint32_t iter = 0;
-    for (int t = blockIdx.x; t < total; t += gridDim.x, ++iter) {
+    for (int t = unit; t < total; t += num_units, ++iter) {
       int g, mt, nt;
       decode_tile(st, G, n_tiles, t, g, mt, nt);
       const uint32_t acc = iter & 1, accph = (iter >> 1) & 1;
       ptx::mbar_wait(ptx::smem_u32(&st.tfull[acc]), accph);
       ptx::tc_fence_after();
-      const int local_row = mt * BM + q * 32 + lane;
+      const int local_row = mt * C::TILE_M + (int)rank * BM + q * 32 + lane;
       const bool valid = local_row < st.gcount[g];
       const int64_t grow = (int64_t)st.gstart[g] + local_row;
       const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
@@ -275,14 +315,19 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
         }
       }
       ptx::tc_fence_before();
-      ptx::mbar_arrive(ptx::smem_u32(&st.tempty[acc]));
+      __syncwarp();
+      if (lane == 0) {
+        if constexpr (CG == 1) ptx::mbar_arrive(ptx::smem_u32(&st.tempty[acc]));
+        else ptx::mbar_arrive_cluster(acc ? tempty_leader1 : tempty_leader0);
+      }
     }
   }
 
   ptx::tc_fence_before();
   __syncthreads();
+  if constexpr (CG == 2) ptx::cluster_sync();  // no CTA leaves while its peer may still signal it
   ptx::tc_fence_after();
-  if (warp == 1) ptx::tmem_dealloc<TMEM_COLS>(tmem_base);
+  if (warp == 1) ptx::tmem_dealloc<TMEM_COLS, CG>(tmem_base);
 }
 
 // ------------------------------------------------------------------ host side
@@ -308,23 +353,27 @@ bool make_tmap(CUtensorMap* m, const void* base, int64_t rows, int K, int box_ro
   cuuint64_t strides[1] = {(cuuint64_t)K * 2};
   cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)box_rows};
   cuuint32_t estr[2] = {1, 1};
-  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box,
-                   estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
 
-template <int EPI>
+template <int EPI, int CG>
 int launch_epi(const GemmArgs& a, cudaStream_t stream) {
   static bool attr_set = false;
+  auto kern = gemm_kernel<EPI, CG>;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_kernel<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)SMEM_BYTES);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes<CG>());
     if (e != cudaSuccess) return (int)e;
+    if (CG == 2) {
+      e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 0);
+      (void)e;
+    }
     attr_set = true;
   }
   CUtensorMap tA, tB0, tB1;
-  const int b_box = (EPI == EPI_SWIGLU) ? 128 : 256;
+  const int b_box = (EPI == EPI_SWIGLU || CG == 2) ? 128 : 256;
   if (!make_tmap(&tA, a.A, a.a_rows, a.K, BM)) return (int)cudaErrorInvalidValue;
   if (!make_tmap(&tB0, a.B0, a.b_rows, a.K, b_box)) return (int)cudaErrorInvalidValue;
   if (EPI == EPI_SWIGLU) {
@@ -333,7 +382,6 @@ int launch_epi(const GemmArgs& a, cudaStream_t stream) {
     tB1 = tB0;
   }
   KParams p;
-  p.epi = EPI;
   p.K = a.K;
   p.N = a.N;
   p.G = a.G;
@@ -345,8 +393,33 @@ int launch_epi(const GemmArgs& a, cudaStream_t stream) {
   p.bias = a.bias;
   p.row_start = a.row_start;
   p.row_count = a.row_count;
-  gemm_kernel<EPI><<<a.num_ctas, NUM_THREADS, SMEM_BYTES, stream>>>(tA, tB0, tB1, p);
-  return (int)cudaGetLastError();
+  int grid = a.num_ctas;
+  if (CG == 2) grid &= ~1;
+  if (grid < CG) grid = CG;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(NUM_THREADS);
+  cfg.dynamicSmemBytes = smem_bytes<CG>();
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CG;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, tA, tB0, tB1, p);
+  return (int)e;
+}
+
+template <int CG>
+int launch_cg(const GemmArgs& a, cudaStream_t stream) {
+  switch (a.epi) {
+    case EPI_SWIGLU: return launch_epi<EPI_SWIGLU, CG>(a, stream);
+    case EPI_BF16: return launch_epi<EPI_BF16, CG>(a, stream);
+    case EPI_F32: return launch_epi<EPI_F32, CG>(a, stream);
+  }
+  return (int)cudaErrorInvalidValue;
 }
 
 }  // namespace
@@ -354,12 +427,7 @@ int launch_epi(const GemmArgs& a, cudaStream_t stream) {
 int gemm_launch(const GemmArgs& a, cudaStream_t stream) {
   if (a.K % BK != 0 || a.K <= 0 || a.G < 1 || a.G > MAX_G || a.num_ctas < 1) return (int)cudaErrorInvalidValue;
   if (a.row_count == nullptr && a.m_single <= 0) return 0;
-  switch (a.epi) {
-    case EPI_SWIGLU: return launch_epi<EPI_SWIGLU>(a, stream);
-    case EPI_BF16: return launch_epi<EPI_BF16>(a, stream);
-    case EPI_F32: return launch_epi<EPI_F32>(a, stream);
-  }
-  return (int)cudaErrorInvalidValue;
+  return a.cta_pair ? launch_cg<2>(a, stream) : launch_cg<1>(a, stream);
 }
 
 }  // namespace epsmoe

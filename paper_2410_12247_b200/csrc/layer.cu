@@ -45,6 +45,12 @@ struct moe_layer {
   ncclComm_t comm_d = nullptr, comm_c = nullptr;
   moe_cost_model_t cost;
   int last_launches = 0;
+  // per-stage device timing (moe_layer_set_profiling)
+  bool prof = false;
+  std::vector<cudaEvent_t> pev;
+  int pev_used = 0;
+  struct Mark { int stage, e0, e1; };
+  std::vector<Mark> marks;
 };
 
 namespace epsmoe {
@@ -149,21 +155,41 @@ size_t carve(moe_layer* L, char* base) {
   return cv.off + ALIGN;
 }
 
+// Record a profiling event on `st` (no-op unless profiling is on).
+int prof_rec(moe_layer* L, cudaStream_t st) {
+  if (!L->prof || L->pev_used >= (int)L->pev.size()) return -1;
+  cudaEventRecord(L->pev[L->pev_used], st);
+  return L->pev_used++;
+}
+void prof_mark(moe_layer* L, int stage, int e0, int e1) {
+  if (e0 >= 0 && e1 >= 0) L->marks.push_back({stage, e0, e1});
+}
+
 GemmArgs base_args(int epi, int num_ctas) {
   GemmArgs a;
   std::memset(&a, 0, sizeof(a));
   a.epi = epi;
   a.G = 1;
   a.num_ctas = num_ctas;
+  a.cta_pair = 1;  // dense single-group GEMMs (router, shared experts): large M
   return a;
+}
+
+// Tile rows for a chunk's expert GEMMs: 256 (CTA pair) unless the plan says
+// otherwise or the chunk's mean rows per expert is small (decode-like load).
+int pick_cta_pair(const moe_plan_t& plan, double mean_rows) {
+  if (plan.tile_m == 256) return 1;
+  if (plan.tile_m == 128) return 0;
+  return mean_rows >= 512.0 ? 1 : 0;
 }
 
 // ComputeMoE for local experts [g0, g1): GateUpGemm+SiluAct fused,
 // then DownGemm.  Rows of expert g are [row_start[g], +row_count[g]) of A.
 int compute_moe(moe_layer* L, const void* A, int64_t a_rows, const int32_t* row_start, const int32_t* row_count,
-                int g0, int g1, int kind, int num_ctas, cudaStream_t st) {
+                int g0, int g1, int kind, int num_ctas, int cta_pair, cudaStream_t st) {
   const moe_config_t& c = L->cfg;
   GemmArgs g1a = base_args(EPI_SWIGLU, num_ctas);
+  g1a.cta_pair = cta_pair;
   g1a.A = A;
   g1a.a_rows = a_rows;
   g1a.B0 = L->w.w_gate;
@@ -175,6 +201,7 @@ int compute_moe(moe_layer* L, const void* A, int64_t a_rows, const int32_t* row_
   g1a.out = L->h;
   g1a.ldo = c.ffn;
   GemmArgs g2a = base_args(EPI_BF16, num_ctas);
+  g2a.cta_pair = cta_pair;
   g2a.A = L->h;
   g2a.a_rows = L->gemm_rows_cap;
   g2a.B0 = L->w.w_down;
@@ -185,14 +212,18 @@ int compute_moe(moe_layer* L, const void* A, int64_t a_rows, const int32_t* row_
   g2a.out = L->o;
   g2a.ldo = c.hidden;
   auto run = [&](int a, int b) -> int {
+    int stage = MOE_STAGE_GATEUP;
     for (GemmArgs* ga : {&g1a, &g2a}) {
       ga->G = b - a;
       ga->b_base = a;
       ga->row_start = row_start + a;
       ga->row_count = row_count + a;
+      int p0 = prof_rec(L, st);
       int e = gemm_launch(*ga, st);
       if (e) return e;
+      prof_mark(L, stage, p0, prof_rec(L, st));
       ++L->last_launches;
+      stage = MOE_STAGE_DOWN;
     }
     return 0;
   };
@@ -344,6 +375,7 @@ moe_status_t moe_layer_destroy(moe_layer_t* L) {
     if (e) cudaEventDestroy(e);
   for (auto e : L->ev_disp) if (e) cudaEventDestroy(e);
   for (auto e : L->ev_gemm) if (e) cudaEventDestroy(e);
+  for (auto e : L->pev) if (e) cudaEventDestroy(e);
   if (L->ghist_host) cudaFreeHost(L->ghist_host);
   if (L->tables_host) cudaFreeHost(L->tables_host);
   delete L;
@@ -364,6 +396,57 @@ moe_status_t moe_layer_set_cost_model(moe_layer_t* L, const moe_cost_model_t* co
 
 int32_t moe_layer_last_launches(const moe_layer_t* L) { return L ? L->last_launches : 0; }
 
+moe_status_t moe_layer_set_profiling(moe_layer_t* L, int32_t enable) {
+  if (!L) return MOE_ERR_INVALID;
+  if (enable && L->pev.empty()) {
+    L->pev.resize(4096);
+    for (auto& e : L->pev) CUDA_TRY(cudaEventCreate(&e));
+  }
+  L->prof = enable != 0;
+  return MOE_OK;
+}
+
+moe_status_t moe_layer_stage_ms(const moe_layer_t* L, float* ms, int32_t* counts) {
+  if (!L || !ms) return MOE_ERR_INVALID;
+  for (int i = 0; i < MOE_NUM_STAGES; ++i) {
+    ms[i] = 0.f;
+    if (counts) counts[i] = 0;
+  }
+  if (L->pev_used > 0) CUDA_TRY(cudaEventSynchronize(L->pev[L->pev_used - 1]));
+  // exposed all2all: comm intervals not covered by any compute interval
+  std::vector<std::pair<float, float>> comp, comm;
+  int t0 = -1;
+  for (auto& m : L->marks)
+    if (m.stage == MOE_STAGE_TOTAL) t0 = m.e0;
+  for (auto& m : L->marks) {
+    float v = 0.f;
+    CUDA_TRY(cudaEventElapsedTime(&v, L->pev[m.e0], L->pev[m.e1]));
+    ms[m.stage] += v;
+    if (counts) counts[m.stage] += 1;
+    if (t0 >= 0 && m.stage != MOE_STAGE_TOTAL) {
+      float a = 0.f, b = 0.f;
+      cudaEventElapsedTime(&a, L->pev[t0], L->pev[m.e0]);
+      cudaEventElapsedTime(&b, L->pev[t0], L->pev[m.e1]);
+      (m.stage == MOE_STAGE_DISPATCH || m.stage == MOE_STAGE_COMB_A2A ? comm : comp).push_back({a, b});
+    }
+  }
+  std::sort(comp.begin(), comp.end());
+  float exposed = 0.f;
+  for (auto& c : comm) {
+    // subtract the union of compute intervals from [c.first, c.second]
+    float cur = c.first, cov = 0.f;
+    for (auto& k : comp) {
+      if (k.second <= cur) continue;
+      if (k.first >= c.second) break;
+      float lo = std::max(cur, k.first), hi = std::min(c.second, k.second);
+      if (hi > lo) { cov += hi - lo; cur = hi; }
+    }
+    exposed += std::max(0.f, (c.second - c.first) - cov);
+  }
+  ms[MOE_STAGE_EXPOSED_A2A] = exposed;
+  return MOE_OK;
+}
+
 moe_status_t moe_layer_forward(moe_layer_t* L, const void* x, int64_t T, void* y, const moe_plan_t* plan_in,
                                void* stream_v, moe_debug_t* dbg) {
   if (!L || (!x && T > 0) || (!y && T > 0) || T < 0) { set_error("null argument"); return MOE_ERR_INVALID; }
@@ -372,6 +455,9 @@ moe_status_t moe_layer_forward(moe_layer_t* L, const void* x, int64_t T, void* y
   cudaStream_t st = (cudaStream_t)stream_v;
   const int E = c.num_experts, k = c.top_k, H = c.hidden, D = c.ep, E_loc = L->E_loc;
   L->last_launches = 0;
+  L->pev_used = 0;
+  L->marks.clear();
+  const int p_total = prof_rec(L, st);
   const bool override_routing = dbg && dbg->override_routing;
   if (override_routing && (!dbg->topk_idx || !dbg->topk_w)) { set_error("override needs topk_idx/topk_w"); return MOE_ERR_INVALID; }
   int32_t* topk_idx = override_routing ? dbg->topk_idx : L->topk_idx;
@@ -386,6 +472,7 @@ moe_status_t moe_layer_forward(moe_layer_t* L, const void* x, int64_t T, void* y
   int num_ctas = (plan_in && plan.sm_gemm > 0) ? std::min(plan.sm_gemm, L->num_sms) : L->num_sms;
 
   // ---- Router (K1) + topKGating (K2) + histogram
+  int p0 = prof_rec(L, st);
   if (T > 0 && !override_routing) {
     GemmArgs ra = base_args(EPI_F32, num_ctas);
     ra.A = x;
@@ -400,15 +487,19 @@ moe_status_t moe_layer_forward(moe_layer_t* L, const void* x, int64_t T, void* y
     ra.m_single = (int)T;
     KERNEL_TRY(gemm_launch(ra, st));
   }
+  int p1 = prof_rec(L, st);
+  prof_mark(L, MOE_STAGE_ROUTER, p0, p1);
   KERNEL_TRY(launch_gate_topk(L->logits, (int)T, E, k, c.norm_topk, c.routed_scale, override_routing ? 1 : 0,
                               topk_idx, topk_w, L->range_hist, st));
   KERNEL_TRY(launch_range_scan(L->range_hist, (int)T, E, L->range_off, L->hist, st));
   // ---- split (K3): x -> send rows, expert-major (R6)
   KERNEL_TRY(launch_permute(x, (int)T, H, E, k, topk_idx, L->range_off, L->hist, L->send, L->pos,
                             L->seg_start, st));
+  prof_mark(L, MOE_STAGE_ROUTE, p1, prof_rec(L, st));
 
   auto shared_experts = [&]() -> int {
     if (!L->SF || T == 0) return 0;
+    int q0 = prof_rec(L, st);
     GemmArgs a = base_args(EPI_SWIGLU, num_ctas);
     a.A = x;
     a.a_rows = T;
@@ -435,6 +526,7 @@ moe_status_t moe_layer_forward(moe_layer_t* L, const void* x, int64_t T, void* y
     b.m_single = (int)T;
     e = gemm_launch(b, st);
     if (!e) ++L->last_launches;
+    prof_mark(L, MOE_STAGE_SHARED, q0, prof_rec(L, st));
     return e;
   };
 
@@ -450,12 +542,15 @@ moe_status_t moe_layer_forward(moe_layer_t* L, const void* x, int64_t T, void* y
       while (a < g1) {
         int b = a + 1;
         while (b < g1 && plan.expert_kind[b] == plan.expert_kind[a]) ++b;
-        int err = compute_moe(L, L->send, L->send_cap, L->seg_start, L->hist, a, b, plan.expert_kind[a], num_ctas, st);
+        int err = compute_moe(L, L->send, L->send_cap, L->seg_start, L->hist, a, b, plan.expert_kind[a], num_ctas,
+                              pick_cta_pair(plan, (double)T * k / E), st);
         if (err) { set_error(std::string("ComputeMoE: ") + cudaGetErrorString((cudaError_t)err)); return MOE_ERR_CUDA; }
         a = b;
       }
     }
+    int c0 = prof_rec(L, st);
     KERNEL_TRY(launch_combine(L->o, L->SF ? L->s : nullptr, (int)T, H, k, L->pos, topk_w, y, st));
+    prof_mark(L, MOE_STAGE_COMBINE, c0, prof_rec(L, st));
   } else {
     // ---- EP > 1: count exchange (C3), plan, chunked dispatch / compute / combine
     NCCL_TRY(ncclAllGather(L->hist, L->ghist, E, ncclInt32, L->comm_d, st));
@@ -494,6 +589,7 @@ moe_status_t moe_layer_forward(moe_layer_t* L, const void* x, int64_t T, void* y
     const size_t row_bytes = (size_t)H * 2;
     auto dispatch = [&](int ch) -> moe_status_t {
       int g0 = plan.group_begin[ch], g1 = plan.group_begin[ch + 1];
+      int d0 = prof_rec(L, L->s_disp);
       NCCL_TRY(ncclGroupStart());
       for (int peer = 0; peer < D; ++peer)
         for (int el = g0; el < g1; ++el) {
@@ -507,12 +603,14 @@ moe_status_t moe_layer_forward(moe_layer_t* L, const void* x, int64_t T, void* y
                               peer, L->comm_d, L->s_disp));
         }
       NCCL_TRY(ncclGroupEnd());
+      prof_mark(L, MOE_STAGE_DISPATCH, d0, prof_rec(L, L->s_disp));
       CUDA_TRY(cudaEventRecord(L->ev_disp[ch], L->s_disp));
       return MOE_OK;
     };
     auto combine_send = [&](int ch) -> moe_status_t {
       int g0 = plan.group_begin[ch], g1 = plan.group_begin[ch + 1];
       CUDA_TRY(cudaStreamWaitEvent(L->s_comb, L->ev_gemm[ch], 0));
+      int b0 = prof_rec(L, L->s_comb);
       NCCL_TRY(ncclGroupStart());
       for (int peer = 0; peer < D; ++peer)
         for (int el = g0; el < g1; ++el) {
@@ -527,6 +625,7 @@ moe_status_t moe_layer_forward(moe_layer_t* L, const void* x, int64_t T, void* y
                               L->s_comb));
         }
       NCCL_TRY(ncclGroupEnd());
+      prof_mark(L, MOE_STAGE_COMB_A2A, b0, prof_rec(L, L->s_comb));
       return MOE_OK;
     };
     auto compute = [&](int ch) -> moe_status_t {
@@ -536,8 +635,10 @@ moe_status_t moe_layer_forward(moe_layer_t* L, const void* x, int64_t T, void* y
       while (a < g1) {
         int b = a + 1;
         while (b < g1 && plan.expert_kind[b] == plan.expert_kind[a]) ++b;
+        double rows = 0;
+        for (int el = a; el < b; ++el) rows += L->tables_host[MOE_MAX_EXPERTS + el];
         int err = compute_moe(L, L->recv, L->recv_cap, L->recv_start_d, L->recv_count_d, a, b, plan.expert_kind[a],
-                              num_ctas, st);
+                              num_ctas, pick_cta_pair(plan, rows / (b - a)), st);
         if (err) { set_error(std::string("ComputeMoE: ") + cudaGetErrorString((cudaError_t)err)); return MOE_ERR_CUDA; }
         a = b;
       }
@@ -556,8 +657,11 @@ moe_status_t moe_layer_forward(moe_layer_t* L, const void* x, int64_t T, void* y
     if ((s_ = combine_send(PN - 1))) return s_;
     CUDA_TRY(cudaEventRecord(L->ev_comb_done, L->s_comb));
     CUDA_TRY(cudaStreamWaitEvent(st, L->ev_comb_done, 0));
+    int c0 = prof_rec(L, st);
     KERNEL_TRY(launch_combine(L->comb, L->SF ? L->s : nullptr, (int)T, H, k, L->pos, topk_w, y, st));
+    prof_mark(L, MOE_STAGE_COMBINE, c0, prof_rec(L, st));
   }
+  prof_mark(L, MOE_STAGE_TOTAL, p_total, prof_rec(L, st));
 
   if (dbg) {
     if (dbg->logits && !override_routing)
@@ -601,12 +705,14 @@ moe_status_t moe_layer_forward_host(moe_layer_t* L, const void* x_host, int64_t 
 moe_status_t moe_gemm_grouped(int32_t epi, const void* A, int64_t a_rows, const void* B0, const void* B1,
                               int64_t b_rows, int32_t b_group_rows, int32_t kdim, int32_t n, void* out, int64_t ldo,
                               const float* bias, int32_t groups, const int32_t* row_start, const int32_t* row_count,
-                              int32_t num_ctas, void* stream) {
+                              int32_t num_ctas, int32_t tile_m, void* stream) {
   if (epi < 0 || epi > 2 || !A || !B0 || (epi == 0 && !B1) || !out || groups < 1 || !row_start || !row_count) {
     set_error("moe_gemm_grouped: bad argument");
     return MOE_ERR_INVALID;
   }
   GemmArgs a = base_args(epi, num_ctas > 0 ? num_ctas : 148);
+  if (tile_m != 128 && tile_m != 256) { set_error("moe_gemm_grouped: tile_m must be 128 or 256"); return MOE_ERR_INVALID; }
+  a.cta_pair = tile_m == 256;
   a.A = A;
   a.a_rows = a_rows;
   a.B0 = B0;
@@ -651,7 +757,8 @@ moe_status_t moe_layer_calibrate(moe_layer_t* L, void* stream, moe_cost_model_t*
       float best = 1e30f;
       for (int rep = 0; rep < 3; ++rep) {
         CUDA_TRY(cudaEventRecord(e0, st));
-        int err = compute_moe(L, A, arows, L->recv_start_d, L->recv_count_d, 0, G, kind, L->num_sms, st);
+        int err = compute_moe(L, A, arows, L->recv_start_d, L->recv_count_d, 0, G, kind, L->num_sms,
+                              rows >= 512 ? 1 : 0, st);
         if (err) { set_error("calibrate gemm failed"); return MOE_ERR_CUDA; }
         CUDA_TRY(cudaEventRecord(e1, st));
         CUDA_TRY(cudaEventSynchronize(e1));

@@ -98,6 +98,16 @@ class MoELayer:
                   "moe_layer_forward_host")
         return y_host
 
+    def set_profiling(self, on: bool = True) -> None:
+        abi.check(self.lib.moe_layer_set_profiling(self.handle, 1 if on else 0), "moe_layer_set_profiling")
+
+    def stage_ms(self) -> dict:
+        """Per-stage device ms of the last forward (events on the launching streams)."""
+        ms = (C.c_float * len(abi.STAGES))()
+        cnt = (C.c_int32 * len(abi.STAGES))()
+        abi.check(self.lib.moe_layer_stage_ms(self.handle, ms, cnt), "moe_layer_stage_ms")
+        return {n: (float(ms[i]), int(cnt[i])) for i, n in enumerate(abi.STAGES)}
+
     def last_launches(self) -> int:
         return int(self.lib.moe_layer_last_launches(self.handle))
 
@@ -142,12 +152,12 @@ class MoELayer:
 
 
 def gemm_grouped(epi, A, B0, B1, n, out, row_start, row_count, b_group_rows, bias=None, num_ctas=148,
-                 stream=None):
+                 tile_m=128, stream=None):
     """Test / calibration hook: one launch of the layer's tcgen05 GEMM family."""
     st = stream if stream is not None else torch.cuda.current_stream(A.device)
     abi.check(abi.lib().moe_gemm_grouped(int(epi), _ptr(A), A.shape[0], _ptr(B0), _ptr(B1), B0.shape[0],
                                          int(b_group_rows), A.shape[1], int(n), _ptr(out), out.shape[1],
                                          _ptr(bias), row_start.numel(), _ptr(row_start), _ptr(row_count),
-                                         int(num_ctas), C.c_void_p(st.cuda_stream)),
+                                         int(num_ctas), int(tile_m), C.c_void_p(st.cuda_stream)),
               "moe_gemm_grouped")
     return out

@@ -37,8 +37,9 @@ def _rows_ref_swiglu(A, Wg, Wu):
     return oracle.round_bf16(oracle.silu_f32(g) * u)
 
 
-@pytest.mark.parametrize("counts", [[300, 0, 129, 1, 128], [5], [1000, 777]])
-def test_grouped_gemm_swiglu_and_down(counts):
+@pytest.mark.parametrize("tile_m", [128, 256])
+@pytest.mark.parametrize("counts", [[300, 0, 129, 1, 128], [5], [1000, 777], [257, 255, 511, 3]])
+def test_grouped_gemm_swiglu_and_down(counts, tile_m):
     H, F = 256, 384
     G = len(counts)
     rng_rows = sum(counts)
@@ -50,9 +51,9 @@ def test_grouped_gemm_swiglu_and_down(counts):
     rs = torch.from_numpy(starts).cuda()
     rc = torch.from_numpy(np.array(counts, np.int32)).cuda()
     h = torch.zeros(rng_rows, F, dtype=torch.bfloat16, device="cuda")
-    gemm_grouped(0, dev_bf16(A), dev_bf16(Wg), dev_bf16(Wu), F, h, rs, rc, F)
+    gemm_grouped(0, dev_bf16(A), dev_bf16(Wg), dev_bf16(Wu), F, h, rs, rc, F, tile_m=tile_m)
     o = torch.zeros(rng_rows, H, dtype=torch.bfloat16, device="cuda")
-    gemm_grouped(1, h, dev_bf16(Wd), None, H, o, rs, rc, H)
+    gemm_grouped(1, h, dev_bf16(Wd), None, H, o, rs, rc, H, tile_m=tile_m)
     torch.cuda.synchronize()
     h_np, o_np = to_f32(h), to_f32(o)
     for g in range(G):
@@ -67,7 +68,8 @@ def test_grouped_gemm_swiglu_and_down(counts):
         assert_close(o_np[a:b], ref_o, f"o group {g}")
 
 
-def test_router_gemm_exact_on_grid():
+@pytest.mark.parametrize("tile_m", [128, 256])
+def test_router_gemm_exact_on_grid(tile_m):
     T, H, E = 333, 512, 160
     x = fill_bf16(T * H, 2, 1, 0, MODE_GRID, 8.0).reshape(T, H)
     wr = fill_bf16(256 * H, 2, 2, 0, MODE_GRID, 64.0).reshape(256, H)
@@ -75,7 +77,8 @@ def test_router_gemm_exact_on_grid():
     out = torch.zeros(T, E, dtype=torch.float32, device="cuda")
     rs = torch.zeros(1, dtype=torch.int32, device="cuda")
     rc = torch.full((1,), T, dtype=torch.int32, device="cuda")
-    gemm_grouped(2, dev_bf16(x), dev_bf16(wr), None, E, out, rs, rc, 0, bias=torch.from_numpy(bias).cuda())
+    gemm_grouped(2, dev_bf16(x), dev_bf16(wr), None, E, out, rs, rc, 0, bias=torch.from_numpy(bias).cuda(),
+                 tile_m=tile_m)
     torch.cuda.synchronize()
     ref = oracle.router_logits(x, wr[:E], bias)
     assert np.array_equal(out.cpu().numpy(), ref)
@@ -142,9 +145,9 @@ def test_chunked_equals_unchunked_and_kinds():
     L = layer_from_inputs(inp, k, norm)
     x = dev_bf16(inp.x)
     ys = []
-    for n, kind in [(1, MOE_GEMM_GROUPED), (3, MOE_GEMM_GROUPED), (7, MOE_GEMM_GROUPED), (1, MOE_GEMM_DENSE),
-                    (4, MOE_GEMM_DENSE)]:
-        ys.append(L.forward(x, plan=make_plan(n, kind)).clone())
+    for n, kind, tm in [(1, MOE_GEMM_GROUPED, 128), (3, MOE_GEMM_GROUPED, 256), (7, MOE_GEMM_GROUPED, 128),
+                        (1, MOE_GEMM_DENSE, 256), (4, MOE_GEMM_DENSE, 128), (1, MOE_GEMM_GROUPED, 256)]:
+        ys.append(L.forward(x, plan=make_plan(n, kind, tile_m=tm)).clone())
     torch.cuda.synchronize()
     for v in ys[1:]:
         assert torch.equal(v, ys[0])
