@@ -182,6 +182,18 @@ moe_status_t moe_layer_destroy(moe_layer_t* layer);
 moe_status_t moe_plan_compute(const moe_config_t* cfg, const moe_cost_model_t* cost,
                               int64_t global_tokens, const int32_t* global_hist, moe_plan_t* out);
 
+/* Pure, host-only: the all2all layout one forward uses on rank cfg->rank
+ * (R6: send rows expert-major in token order; recv rows ordered by (local
+ * expert, source rank, token)).  ghist: HOST [ep, e] pairs per (rank, expert).
+ * Outputs (HOST, caller-allocated; chunk_* may be NULL):
+ *   send_off  [e + 1]            first send row of expert e on this rank
+ *   recv_off  [E_loc * ep + 1]   first recv row of (local expert, source rank)
+ *   chunk_send[PN * ep]          rows this rank sends peer p in chunk c
+ *   chunk_recv[PN * ep]          rows this rank receives from peer p in chunk c
+ * chunk_send on rank r for peer d equals chunk_recv on rank d for peer r. */
+moe_status_t moe_exchange_layout(const moe_config_t* cfg, const moe_plan_t* plan, const int32_t* ghist,
+                                 int64_t* send_off, int64_t* recv_off, int64_t* chunk_send, int64_t* chunk_recv);
+
 /* moe_plan_compute with the layer's calibrated cost model. */
 moe_status_t moe_plan_pipeline(const moe_layer_t* layer, int64_t global_tokens,
                                const int32_t* global_hist, moe_plan_t* out);

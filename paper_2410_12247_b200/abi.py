@@ -77,6 +77,8 @@ _SIGS = {
     "moe_plan_compute": (C.c_int, [C.POINTER(moe_config_t), C.POINTER(moe_cost_model_t), C.c_int64,
                                    C.c_void_p, C.POINTER(moe_plan_t)]),
     "moe_plan_pipeline": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.POINTER(moe_plan_t)]),
+    "moe_exchange_layout": (C.c_int, [C.POINTER(moe_config_t), C.POINTER(moe_plan_t), C.c_void_p, C.c_void_p,
+                                      C.c_void_p, C.c_void_p, C.c_void_p]),
     "moe_layer_calibrate": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(moe_cost_model_t)]),
     "moe_layer_set_cost_model": (C.c_int, [C.c_void_p, C.POINTER(moe_cost_model_t)]),
     "moe_layer_forward": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.POINTER(moe_plan_t),
@@ -138,7 +140,22 @@ def plan_compute(cfg: moe_config_t, global_tokens: int, global_hist=None, cost: 
     return plan
 
 
-def make_plan(num_chunks=1, gemm_kind=MOE_GEMM_GROUPED, sm_gemm=0, comm_ctas=0, tile_m=0):
+def exchange_layout(cfg: moe_config_t, plan: moe_plan_t, global_hist):
+    """Host-only all2all layout of rank cfg.rank (see moe_exchange_layout)."""
+    import numpy as np
+    E, D = cfg.num_experts, cfg.ep
+    gh = np.ascontiguousarray(global_hist, dtype=np.int32)
+    send_off = np.zeros(E + 1, np.int64)
+    recv_off = np.zeros((E // D) * D + 1, np.int64)
+    cs = np.zeros((plan.num_chunks, D), np.int64)
+    cr = np.zeros((plan.num_chunks, D), np.int64)
+    p = lambda a: a.ctypes.data_as(C.c_void_p)  # noqa: E731
+    check(lib().moe_exchange_layout(C.byref(cfg), C.byref(plan), p(gh), p(send_off), p(recv_off), p(cs), p(cr)),
+          "moe_exchange_layout")
+    return send_off, recv_off, cs, cr
+
+
+def make_plan(num_chunks=1,gemm_kind=MOE_GEMM_GROUPED, sm_gemm=0, comm_ctas=0, tile_m=0):
     p = moe_plan_t()
     p.tile_m = tile_m
     p.num_chunks = num_chunks

@@ -175,6 +175,21 @@ GemmArgs base_args(int epi, int num_ctas) {
   return a;
 }
 
+// All2all layout of one forward on rank c.rank from the global histogram gh
+// [ep, E] (R6): send_off[e] = first send row of expert e (expert-major, local
+// tokens); recv_off[e_l * ep + src] = first recv row of (local expert, source).
+void exchange_layout(const moe_config_t& c, const int32_t* gh, int64_t* send_off, int64_t* recv_off) {
+  const int E = c.num_experts, D = c.ep, E_loc = E / D, me = c.rank;
+  send_off[0] = 0;
+  for (int ex = 0; ex < E; ++ex) send_off[ex + 1] = send_off[ex] + gh[(int64_t)me * E + ex];
+  recv_off[0] = 0;
+  for (int el = 0; el < E_loc; ++el)
+    for (int src = 0; src < D; ++src) {
+      size_t i = (size_t)el * D + src;
+      recv_off[i + 1] = recv_off[i] + gh[(int64_t)src * E + me * E_loc + el];
+    }
+}
+
 // Tile rows for a chunk's expert GEMMs: 256 (CTA pair) unless the plan says
 // otherwise or the chunk's mean rows per expert is small (decode-like load).
 int pick_cta_pair(const moe_plan_t& plan, double mean_rows) {
@@ -382,6 +397,29 @@ moe_status_t moe_layer_destroy(moe_layer_t* L) {
   return MOE_OK;
 }
 
+moe_status_t moe_exchange_layout(const moe_config_t* cfg, const moe_plan_t* plan_in, const int32_t* ghist,
+                                 int64_t* send_off, int64_t* recv_off, int64_t* chunk_send, int64_t* chunk_recv) {
+  int v = validate(cfg);
+  if (v) return (moe_status_t)v;
+  if (!plan_in || !ghist || !send_off || !recv_off) { set_error("null argument"); return MOE_ERR_INVALID; }
+  moe_plan_t plan = *plan_in;
+  int pv = plan_normalise(*cfg, &plan);
+  if (pv) { set_error("invalid plan"); return (moe_status_t)pv; }
+  exchange_layout(*cfg, ghist, send_off, recv_off);
+  const int E = cfg->num_experts, D = cfg->ep, E_loc = E / D, me = cfg->rank;
+  for (int ch = 0; ch < plan.num_chunks; ++ch)
+    for (int peer = 0; peer < D; ++peer) {
+      int64_t s = 0, r = 0;
+      for (int el = plan.group_begin[ch]; el < plan.group_begin[ch + 1]; ++el) {
+        s += ghist[(int64_t)me * E + peer * E_loc + el];   // my pairs for peer's expert el
+        r += ghist[(int64_t)peer * E + me * E_loc + el];   // peer's pairs for my expert el
+      }
+      if (chunk_send) chunk_send[(size_t)ch * D + peer] = s;
+      if (chunk_recv) chunk_recv[(size_t)ch * D + peer] = r;
+    }
+  return MOE_OK;
+}
+
 moe_status_t moe_plan_pipeline(const moe_layer_t* L, int64_t global_tokens, const int32_t* global_hist,
                                moe_plan_t* out) {
   if (!L || !out) return MOE_ERR_INVALID;
@@ -568,13 +606,8 @@ moe_status_t moe_layer_forward(moe_layer_t* L, const void* x, int64_t T, void* y
     const int me = c.rank;
     // send offsets (local, expert-major) and recv layout [e_l][src] (R6)
     std::vector<int64_t> send_off(E + 1, 0);
-    for (int ex = 0; ex < E; ++ex) send_off[ex + 1] = send_off[ex] + gh[(int64_t)me * E + ex];
     std::vector<int64_t> recv_off((size_t)E_loc * D + 1, 0);
-    for (int el = 0; el < E_loc; ++el)
-      for (int src = 0; src < D; ++src) {
-        size_t i = (size_t)el * D + src;
-        recv_off[i + 1] = recv_off[i] + gh[(int64_t)src * E + me * E_loc + el];
-      }
+    exchange_layout(c, gh, send_off.data(), recv_off.data());
     if (recv_off.back() > L->recv_cap) { set_error("recv rows exceed capacity"); return MOE_ERR_CAPACITY; }
     for (int el = 0; el < E_loc; ++el) {
       L->tables_host[el] = (int32_t)recv_off[(size_t)el * D];
