@@ -23,6 +23,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <cstdlib>
 #include <mutex>
 
 #include "gemm.h"
@@ -49,6 +50,7 @@ struct Cfg {
 
 struct KParams {
   int K, N, G, m_single, b_group_rows, b_base;
+  int raster_gm;  // tile order inside a group: blocks of raster_gm m-tiles, m fastest inside a block
   int64_t ldo;
   void* out;
   const float* bias;
@@ -80,18 +82,26 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   return *reinterpret_cast<uint32_t*>(&v);
 }
 
+// Linear tile index -> (group, m-tile, n-tile).  Inside a group, tiles are
+// visited in blocks of `gm` m-tiles: n-tile major across the block, m fastest
+// inside it (gm = 1: plain n-fastest order), so the tiles in flight at once
+// share A rows and B columns in L2.
 template <int CG>
-__device__ __forceinline__ void decode_tile(const SmemTail<CG>& s, int G, int n_tiles, int t, int& g, int& mt,
-                                            int& nt) {
+__device__ __forceinline__ void decode_tile(const SmemTail<CG>& s, int G, int n_tiles, int gm_cfg, int t, int& g,
+                                            int& mt, int& nt) {
   int lo = 0, hi = G - 1;  // largest g with tile_prefix[g] <= t
   while (lo < hi) {
     int mid = (lo + hi + 1) >> 1;
     if (s.tile_prefix[mid] <= t) lo = mid; else hi = mid - 1;
   }
   g = lo;
-  int local = t - s.tile_prefix[g];
-  mt = local / n_tiles;
-  nt = local - mt * n_tiles;
+  const int local = t - s.tile_prefix[g];
+  const int m_tiles = (s.tile_prefix[g + 1] - s.tile_prefix[g]) / n_tiles;
+  const int blk = local / (gm_cfg * n_tiles);
+  const int within = local - blk * gm_cfg * n_tiles;
+  const int gm = min(gm_cfg, m_tiles - blk * gm_cfg);
+  mt = blk * gm_cfg + within % gm;
+  nt = within / gm;
 }
 
 template <int EPI, int CG>
@@ -176,7 +186,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
       uint32_t stage = 0, phase = 0;
       for (int t = unit; t < total; t += num_units) {
         int g, mt, nt;
-        decode_tile(st, G, n_tiles, t, g, mt, nt);
+        decode_tile(st, G, n_tiles, p.raster_gm, t, g, mt, nt);
         const int a_row = st.gstart[g] + mt * C::TILE_M + (int)rank * BM;
         const int b_row0 = (p.b_base + g) * p.b_group_rows + nt * n_out_tile;
         for (int kb = 0; kb < num_kb; ++kb) {
@@ -245,7 +255,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
     uint32_t iter = 0;
     for (int t = unit; t < total; t += num_units, ++iter) {
       int g, mt, nt;
-      decode_tile(st, G, n_tiles, t, g, mt, nt);
+      decode_tile(st, G, n_tiles, p.raster_gm, t, g, mt, nt);
       const uint32_t acc = iter & 1, accph = (iter >> 1) & 1;
       ptx::mbar_wait(ptx::smem_u32(&st.tfull[acc]), accph);
       ptx::tc_fence_after();
@@ -345,6 +355,17 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
   return fn;
 }
 
+// Tile rasterisation block (m-tiles); 4 measured best on DSv2 and Mixtral
+// shapes (tools/gemm_bench.py, profiles/r01_notes.md); EPSMOE_RASTER_GM overrides.
+int raster_gm() {
+  static int v = [] {
+    const char* e = std::getenv("EPSMOE_RASTER_GM");
+    int r = e ? std::atoi(e) : 4;
+    return r < 1 ? 1 : r;
+  }();
+  return v;
+}
+
 // 2D bf16 K-major tensor [rows, K] with a {64, box_rows} box and 128 B swizzle.
 bool make_tmap(CUtensorMap* m, const void* base, int64_t rows, int K, int box_rows) {
   auto enc = get_encode_fn();
@@ -388,6 +409,7 @@ int launch_epi(const GemmArgs& a, cudaStream_t stream) {
   p.m_single = a.m_single;
   p.b_group_rows = a.b_group_rows;
   p.b_base = a.b_base;
+  p.raster_gm = raster_gm();
   p.ldo = a.ldo;
   p.out = a.out;
   p.bias = a.bias;

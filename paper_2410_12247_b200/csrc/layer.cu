@@ -12,6 +12,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -40,6 +41,9 @@ struct moe_layer {
   int32_t* ghist_host = nullptr;    // pinned [ep*E]
   int32_t* tables_host = nullptr;   // pinned [2*E_loc]
   cudaStream_t s_disp = nullptr, s_comb = nullptr;
+  cudaStream_t s_side = nullptr;  // shared experts, concurrent with routing / dispatch
+  cudaEvent_t ev_router = nullptr, ev_shared = nullptr;
+  bool overlap_shared = false;    // EPSMOE_OVERLAP_SHARED=1: shared experts on s_side at ep == 1
   cudaEvent_t ev_hist = nullptr, ev_ready = nullptr, ev_comb_done = nullptr;
   std::vector<cudaEvent_t> ev_disp, ev_gemm;
   ncclComm_t comm_d = nullptr, comm_c = nullptr;
@@ -329,6 +333,13 @@ moe_status_t moe_layer_create(const moe_config_t* cfg, const moe_weights_t* w, c
     return fail(MOE_ERR_CUDA);
   }
   default_cost_model(L->cfg, &L->cost);
+  if (const char* ov = std::getenv("EPSMOE_OVERLAP_SHARED")) L->overlap_shared = std::atoi(ov) != 0;
+  if (cudaStreamCreateWithFlags(&L->s_side, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&L->ev_router, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&L->ev_shared, cudaEventDisableTiming) != cudaSuccess) {
+    set_error("side stream creation failed");
+    return fail(MOE_ERR_CUDA);
+  }
   if (cfg->ep > 1) {
     if (cudaStreamCreateWithFlags(&L->s_disp, cudaStreamNonBlocking) != cudaSuccess ||
         cudaStreamCreateWithFlags(&L->s_comb, cudaStreamNonBlocking) != cudaSuccess ||
@@ -385,6 +396,9 @@ moe_status_t moe_layer_destroy(moe_layer_t* L) {
   if (L->comm_d) ncclCommDestroy(L->comm_d);
   if (L->comm_c) ncclCommDestroy(L->comm_c);
   if (L->s_disp) cudaStreamDestroy(L->s_disp);
+  if (L->s_side) cudaStreamDestroy(L->s_side);
+  for (cudaEvent_t e : {L->ev_router, L->ev_shared})
+    if (e) cudaEventDestroy(e);
   if (L->s_comb) cudaStreamDestroy(L->s_comb);
   for (cudaEvent_t e : {L->ev_hist, L->ev_ready, L->ev_comb_done})
     if (e) cudaEventDestroy(e);
@@ -527,17 +541,13 @@ moe_status_t moe_layer_forward(moe_layer_t* L, const void* x, int64_t T, void* y
   }
   int p1 = prof_rec(L, st);
   prof_mark(L, MOE_STAGE_ROUTER, p0, p1);
-  KERNEL_TRY(launch_gate_topk(L->logits, (int)T, E, k, c.norm_topk, c.routed_scale, override_routing ? 1 : 0,
-                              topk_idx, topk_w, L->range_hist, st));
-  KERNEL_TRY(launch_range_scan(L->range_hist, (int)T, E, L->range_off, L->hist, st));
-  // ---- split (K3): x -> send rows, expert-major (R6)
-  KERNEL_TRY(launch_permute(x, (int)T, H, E, k, topk_idx, L->range_off, L->hist, L->send, L->pos,
-                            L->seg_start, st));
-  prof_mark(L, MOE_STAGE_ROUTE, p1, prof_rec(L, st));
 
-  auto shared_experts = [&]() -> int {
+  // Shared experts depend only on x: they run on s_side, concurrently
+  // with topKGating / split (HBM-bound kernels that co-reside with the GEMM's
+  // CTAs) and, for ep > 1, with the count exchange, host wait and dispatch(0).
+  auto shared_experts = [&](cudaStream_t ss) -> int {
     if (!L->SF || T == 0) return 0;
-    int q0 = prof_rec(L, st);
+    int q0 = prof_rec(L, ss);
     GemmArgs a = base_args(EPI_SWIGLU, num_ctas);
     a.A = x;
     a.a_rows = T;
@@ -549,7 +559,7 @@ moe_status_t moe_layer_forward(moe_layer_t* L, const void* x, int64_t T, void* y
     a.out = L->hs;
     a.ldo = L->SF;
     a.m_single = (int)T;
-    int e = gemm_launch(a, st);
+    int e = gemm_launch(a, ss);
     if (e) return e;
     ++L->last_launches;
     GemmArgs b = base_args(EPI_BF16, num_ctas);
@@ -562,17 +572,38 @@ moe_status_t moe_layer_forward(moe_layer_t* L, const void* x, int64_t T, void* y
     b.out = L->s;
     b.ldo = H;
     b.m_single = (int)T;
-    e = gemm_launch(b, st);
+    e = gemm_launch(b, ss);
     if (!e) ++L->last_launches;
-    prof_mark(L, MOE_STAGE_SHARED, q0, prof_rec(L, st));
+    prof_mark(L, MOE_STAGE_SHARED, q0, prof_rec(L, ss));
     return e;
   };
+  // ep == 1: concurrent shared GEMMs + routing kernels contend for L2 (measured
+  // slower on B200), so they run in stream order unless EPSMOE_OVERLAP_SHARED=1.
+  const bool has_shared = L->SF && T > 0;
+  const bool side = has_shared && (D > 1 || L->overlap_shared);
+  if (side) {
+    CUDA_TRY(cudaEventRecord(L->ev_router, st));
+    CUDA_TRY(cudaStreamWaitEvent(L->s_side, L->ev_router, 0));
+    int e = shared_experts(L->s_side);
+    if (e) { set_error(std::string("shared experts: ") + cudaGetErrorString((cudaError_t)e)); return MOE_ERR_CUDA; }
+    CUDA_TRY(cudaEventRecord(L->ev_shared, L->s_side));
+  } else if (has_shared) {
+    int e = shared_experts(st);
+    if (e) { set_error(std::string("shared experts: ") + cudaGetErrorString((cudaError_t)e)); return MOE_ERR_CUDA; }
+  }
+
+  KERNEL_TRY(launch_gate_topk(L->logits, (int)T, E, k, c.norm_topk, c.routed_scale, override_routing ? 1 : 0,
+                              topk_idx, topk_w, L->range_hist, st));
+  KERNEL_TRY(launch_range_scan(L->range_hist, (int)T, E, L->range_off, L->hist, st));
+  // ---- split (K3): x -> send rows, expert-major (R6)
+  KERNEL_TRY(launch_permute(x, (int)T, H, E, k, topk_idx, L->range_off, L->hist, L->send, L->pos,
+                            L->seg_start, st));
+  prof_mark(L, MOE_STAGE_ROUTE, p1, prof_rec(L, st));
 
   if (D == 1) {
     // ---- EP = 1: no all2all; every chunk is local (C = 0 => PN = 1 is optimal)
     if (!plan_in) plan_compute(c, L->cost, T, nullptr, &plan);
-    int e = shared_experts();
-    if (e) { set_error(std::string("shared experts: ") + cudaGetErrorString((cudaError_t)e)); return MOE_ERR_CUDA; }
+    if (side) CUDA_TRY(cudaStreamWaitEvent(st, L->ev_shared, 0));
     for (int ch = 0; ch < plan.num_chunks; ++ch) {
       int g0 = plan.group_begin[ch], g1 = plan.group_begin[ch + 1];
       // maximal runs of equal kind inside the chunk
@@ -594,8 +625,6 @@ moe_status_t moe_layer_forward(moe_layer_t* L, const void* x, int64_t T, void* y
     NCCL_TRY(ncclAllGather(L->hist, L->ghist, E, ncclInt32, L->comm_d, st));
     CUDA_TRY(cudaMemcpyAsync(L->ghist_host, L->ghist, sizeof(int32_t) * D * E, cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaEventRecord(L->ev_hist, st));
-    int e = shared_experts();  // overlaps the host wait and dispatch(0)
-    if (e) { set_error(std::string("shared experts: ") + cudaGetErrorString((cudaError_t)e)); return MOE_ERR_CUDA; }
     CUDA_TRY(cudaEventSynchronize(L->ev_hist));
     const int32_t* gh = L->ghist_host;
     if (!plan_in) {
@@ -690,6 +719,7 @@ moe_status_t moe_layer_forward(moe_layer_t* L, const void* x, int64_t T, void* y
     if ((s_ = combine_send(PN - 1))) return s_;
     CUDA_TRY(cudaEventRecord(L->ev_comb_done, L->s_comb));
     CUDA_TRY(cudaStreamWaitEvent(st, L->ev_comb_done, 0));
+    if (side) CUDA_TRY(cudaStreamWaitEvent(st, L->ev_shared, 0));
     int c0 = prof_rec(L, st);
     KERNEL_TRY(launch_combine(L->comb, L->SF ? L->s : nullptr, (int)T, H, k, L->pos, topk_w, y, st));
     prof_mark(L, MOE_STAGE_COMBINE, c0, prof_rec(L, st));

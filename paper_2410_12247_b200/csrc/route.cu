@@ -170,7 +170,7 @@ __device__ __forceinline__ int block_exclusive_scan_256(int v, int* sh) {
 // K3 permute (`split`).  seg_start[e] = sum_{e' < e} hist[e'] (send
 // layout expert-major, R6).  One warp per token range; each token's row is
 // read once and written to its k destination rows with 16-byte stores.
-__global__ void __launch_bounds__(WARPS * 32)
+__global__ void __launch_bounds__(WARPS * 32, 2)
 permute_kernel(const __nv_bfloat16* __restrict__ x, int T, int H, int E, int k,
                const int32_t* __restrict__ topk_idx, const int32_t* __restrict__ range_off,
                const int32_t* __restrict__ hist, int R, __nv_bfloat16* __restrict__ send,
@@ -207,20 +207,24 @@ permute_kernel(const __nv_bfloat16* __restrict__ x, int T, int H, int E, int k,
     }
     __syncwarp();
     const uint4* src = reinterpret_cast<const uint4*>(x + (int64_t)t * H);
-    constexpr int MAXV = 32;  // H <= 8192
-    uint4 buf[MAXV];
-#pragma unroll
-    for (int i = 0; i < MAXV; ++i) {
-      int c = lane + 32 * i;
-      if (c < nvec) buf[i] = __ldg(src + c);
-    }
-    for (int j = 0; j < k; ++j) {
-      int d = __shfl_sync(0xffffffffu, dest, j);
-      uint4* dst = reinterpret_cast<uint4*>(send + (int64_t)d * H);
+    // 16 x 16 B per lane in flight per pass (H <= 4096 per pass, <= 2 passes):
+    // keeps the kernel under 128 registers so it co-resides with a GEMM CTA.
+    constexpr int MAXV = 16;
+    for (int base = 0; base < nvec; base += 32 * MAXV) {
+      uint4 buf[MAXV];
 #pragma unroll
       for (int i = 0; i < MAXV; ++i) {
-        int c = lane + 32 * i;
-        if (c < nvec) dst[c] = buf[i];
+        int c = base + lane + 32 * i;
+        if (c < nvec) buf[i] = __ldg(src + c);
+      }
+      for (int j = 0; j < k; ++j) {
+        int d = __shfl_sync(0xffffffffu, dest, j);
+        uint4* dst = reinterpret_cast<uint4*>(send + (int64_t)d * H);
+#pragma unroll
+        for (int i = 0; i < MAXV; ++i) {
+          int c = base + lane + 32 * i;
+          if (c < nvec) dst[c] = buf[i];
+        }
       }
     }
   }
