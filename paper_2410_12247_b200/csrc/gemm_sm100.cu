@@ -56,6 +56,7 @@ struct KParams {
   const float* bias;
   const int32_t* row_start;
   const int32_t* row_count;
+  const int32_t* a_row_index;
 };
 
 template <int CG>
@@ -68,6 +69,7 @@ struct __align__(8) SmemTail {
   int32_t tile_prefix[MAX_G + 1];
   int32_t gstart[MAX_G];
   int32_t gcount[MAX_G];
+  alignas(16) int32_t tok[BM];  // GATHER: physical A rows of the current tile (read as int4)
 };
 
 template <int CG>
@@ -104,7 +106,7 @@ __device__ __forceinline__ void decode_tile(const SmemTail<CG>& s, int G, int n_
   nt = within / gm;
 }
 
-template <int EPI, int CG>
+template <int EPI, int CG, bool GATHER>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
 gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB0,
             const __grid_constant__ CUtensorMap tmB1, const KParams p) {
@@ -182,19 +184,44 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
 
   if (warp == 0) {
     // ===================== TMA producer (each CTA loads its own halves) =====================
-    if (lane == 0) {
-      uint32_t stage = 0, phase = 0;
-      for (int t = unit; t < total; t += num_units) {
-        int g, mt, nt;
-        decode_tile(st, G, n_tiles, p.raster_gm, t, g, mt, nt);
-        const int a_row = st.gstart[g] + mt * C::TILE_M + (int)rank * BM;
-        const int b_row0 = (p.b_base + g) * p.b_group_rows + nt * n_out_tile;
+    // GATHER: the whole warp stages the tile's 128 physical A row indices in
+    // smem; lane 0 then issues 32 tile::gather4 loads per stage.
+    uint32_t stage = 0, phase = 0;
+    for (int t = unit; t < total; t += num_units) {
+      int g, mt, nt;
+      decode_tile(st, G, n_tiles, p.raster_gm, t, g, mt, nt);
+      const int a_row = st.gstart[g] + mt * C::TILE_M + (int)rank * BM;
+      const int b_row0 = (p.b_base + g) * p.b_group_rows + nt * n_out_tile;
+      if constexpr (GATHER) {
+        __syncwarp();
+        const int local0 = mt * C::TILE_M + (int)rank * BM;
+#pragma unroll
+        for (int i = 0; i < BM / 32; ++i) {
+          const int r = lane * (BM / 32) + i;
+          // rows past the group's end load any valid row (their results are not stored)
+          const int src = (local0 + r < st.gcount[g]) ? a_row + r : st.gstart[g];
+          st.tok[r] = p.a_row_index[src];
+        }
+        __syncwarp();
+      }
+      if (lane == 0) {
         for (int kb = 0; kb < num_kb; ++kb) {
           ptx::mbar_wait(ptx::smem_u32(&st.empty[stage]), phase ^ 1);
           const uint32_t fb = ptx::smem_u32(&st.full[stage]);
           const uint32_t a_dst = ptx::smem_u32(sA + stage * C::A_BYTES);
           const uint32_t b_dst = ptx::smem_u32(sB + stage * C::B_BYTES);
-          if constexpr (CG == 1) {
+          if constexpr (GATHER) {
+            if (CG == 1 || rank == 0) ptx::mbar_arrive_expect_tx(fb, CG * (C::A_BYTES + C::B_BYTES));
+            const int4* tk = reinterpret_cast<const int4*>(st.tok);
+#pragma unroll 8
+            for (int i = 0; i < BM / 4; ++i) ptx::tma_gather4<CG>(a_dst + i * 512, &tmA, fb, kb * BK, tk[i]);
+            if constexpr (CG == 1) {
+              ptx::tma_load_2d(b_dst, &tmB0, fb, kb * BK, b_row0);
+              ptx::tma_load_2d(b_dst + C::B_BYTES / 2, &tmB1, fb, kb * BK, b_row0);
+            } else {
+              ptx::tma_load_2d_pair(b_dst, rank == 0 ? &tmB0 : &tmB1, fb, kb * BK, b_row0);
+            }
+          } else if constexpr (CG == 1) {
             ptx::mbar_arrive_expect_tx(fb, C::A_BYTES + C::B_BYTES);
             ptx::tma_load_2d(a_dst, &tmA, fb, kb * BK, a_row);
             if (EPI == EPI_SWIGLU) {
@@ -380,10 +407,10 @@ bool make_tmap(CUtensorMap* m, const void* base, int64_t rows, int K, int box_ro
   return r == CUDA_SUCCESS;
 }
 
-template <int EPI, int CG>
+template <int EPI, int CG, bool GATHER>
 int launch_epi(const GemmArgs& a, cudaStream_t stream) {
   static bool attr_set = false;
-  auto kern = gemm_kernel<EPI, CG>;
+  auto kern = gemm_kernel<EPI, CG, GATHER>;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes<CG>());
     if (e != cudaSuccess) return (int)e;
@@ -395,7 +422,7 @@ int launch_epi(const GemmArgs& a, cudaStream_t stream) {
   }
   CUtensorMap tA, tB0, tB1;
   const int b_box = (EPI == EPI_SWIGLU || CG == 2) ? 128 : 256;
-  if (!make_tmap(&tA, a.A, a.a_rows, a.K, BM)) return (int)cudaErrorInvalidValue;
+  if (!make_tmap(&tA, a.A, a.a_rows, a.K, GATHER ? 1 : BM)) return (int)cudaErrorInvalidValue;
   if (!make_tmap(&tB0, a.B0, a.b_rows, a.K, b_box)) return (int)cudaErrorInvalidValue;
   if (EPI == EPI_SWIGLU) {
     if (!make_tmap(&tB1, a.B1, a.b_rows, a.K, b_box)) return (int)cudaErrorInvalidValue;
@@ -415,6 +442,7 @@ int launch_epi(const GemmArgs& a, cudaStream_t stream) {
   p.bias = a.bias;
   p.row_start = a.row_start;
   p.row_count = a.row_count;
+  p.a_row_index = a.a_row_index;
   int grid = a.num_ctas;
   if (CG == 2) grid &= ~1;
   if (grid < CG) grid = CG;
@@ -437,9 +465,10 @@ int launch_epi(const GemmArgs& a, cudaStream_t stream) {
 template <int CG>
 int launch_cg(const GemmArgs& a, cudaStream_t stream) {
   switch (a.epi) {
-    case EPI_SWIGLU: return launch_epi<EPI_SWIGLU, CG>(a, stream);
-    case EPI_BF16: return launch_epi<EPI_BF16, CG>(a, stream);
-    case EPI_F32: return launch_epi<EPI_F32, CG>(a, stream);
+    case EPI_SWIGLU:
+      return a.a_row_index ? launch_epi<EPI_SWIGLU, CG, true>(a, stream) : launch_epi<EPI_SWIGLU, CG, false>(a, stream);
+    case EPI_BF16: return launch_epi<EPI_BF16, CG, false>(a, stream);
+    case EPI_F32: return launch_epi<EPI_F32, CG, false>(a, stream);
   }
   return (int)cudaErrorInvalidValue;
 }

@@ -31,6 +31,7 @@ struct moe_layer {
   void* wr_pad = nullptr;
   float* logits = nullptr;
   int32_t *topk_idx = nullptr, *pos = nullptr, *range_hist = nullptr, *range_off = nullptr;
+  int32_t* row_token = nullptr;   // [T*k]: token of each send row (gathered GateUp A, ep == 1)
   float* topk_w = nullptr;
   int32_t *hist = nullptr, *seg_start = nullptr, *ghist = nullptr;
   int32_t *recv_start_d = nullptr, *recv_count_d = nullptr;
@@ -44,6 +45,9 @@ struct moe_layer {
   cudaStream_t s_side = nullptr;  // shared experts, concurrent with routing / dispatch
   cudaEvent_t ev_router = nullptr, ev_shared = nullptr;
   bool overlap_shared = false;    // EPSMOE_OVERLAP_SHARED=1: shared experts on s_side at ep == 1
+  bool gather_a = false;          // EPSMOE_GATHER=1: GateUp gathers x rows (tile::gather4) at ep == 1
+                                  // instead of reading a materialised send buffer; measured 3.5x
+                                  // slower GateUp on B200 (32 gather4 per stage), so off by default
   cudaEvent_t ev_hist = nullptr, ev_ready = nullptr, ev_comb_done = nullptr;
   std::vector<cudaEvent_t> ev_disp, ev_gemm;
   ncclComm_t comm_d = nullptr, comm_c = nullptr;
@@ -140,6 +144,7 @@ size_t carve(moe_layer* L, char* base) {
   L->topk_idx = cv.take<int32_t>(T * k);
   L->topk_w = cv.take<float>(T * k);
   L->pos = cv.take<int32_t>(T * k);
+  L->row_token = cv.take<int32_t>(T * k);
   L->range_hist = cv.take<int32_t>(E * R);
   L->range_off = cv.take<int32_t>(E * R);
   L->hist = cv.take<int32_t>(MOE_MAX_EXPERTS + 1);
@@ -205,11 +210,13 @@ int pick_cta_pair(const moe_plan_t& plan, double mean_rows) {
 // ComputeMoE for local experts [g0, g1): GateUpGemm+SiluAct fused,
 // then DownGemm.  Rows of expert g are [row_start[g], +row_count[g]) of A.
 int compute_moe(moe_layer* L, const void* A, int64_t a_rows, const int32_t* row_start, const int32_t* row_count,
-                int g0, int g1, int kind, int num_ctas, int cta_pair, cudaStream_t st) {
+                int g0, int g1, int kind, int num_ctas, int cta_pair, cudaStream_t st,
+                const int32_t* a_row_index = nullptr) {
   const moe_config_t& c = L->cfg;
   GemmArgs g1a = base_args(EPI_SWIGLU, num_ctas);
   g1a.cta_pair = cta_pair;
   g1a.A = A;
+  g1a.a_row_index = a_row_index;
   g1a.a_rows = a_rows;
   g1a.B0 = L->w.w_gate;
   g1a.B1 = L->w.w_up;
@@ -334,6 +341,7 @@ moe_status_t moe_layer_create(const moe_config_t* cfg, const moe_weights_t* w, c
   }
   default_cost_model(L->cfg, &L->cost);
   if (const char* ov = std::getenv("EPSMOE_OVERLAP_SHARED")) L->overlap_shared = std::atoi(ov) != 0;
+  if (const char* gv = std::getenv("EPSMOE_GATHER")) L->gather_a = std::atoi(gv) != 0;
   if (cudaStreamCreateWithFlags(&L->s_side, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreateWithFlags(&L->ev_router, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&L->ev_shared, cudaEventDisableTiming) != cudaSuccess) {
@@ -587,32 +595,37 @@ moe_status_t moe_layer_forward(moe_layer_t* L, const void* x, int64_t T, void* y
     int e = shared_experts(L->s_side);
     if (e) { set_error(std::string("shared experts: ") + cudaGetErrorString((cudaError_t)e)); return MOE_ERR_CUDA; }
     CUDA_TRY(cudaEventRecord(L->ev_shared, L->s_side));
-  } else if (has_shared) {
-    int e = shared_experts(st);
-    if (e) { set_error(std::string("shared experts: ") + cudaGetErrorString((cudaError_t)e)); return MOE_ERR_CUDA; }
   }
 
   KERNEL_TRY(launch_gate_topk(L->logits, (int)T, E, k, c.norm_topk, c.routed_scale, override_routing ? 1 : 0,
                               topk_idx, topk_w, L->range_hist, st));
   KERNEL_TRY(launch_range_scan(L->range_hist, (int)T, E, L->range_off, L->hist, st));
-  // ---- split (K3): x -> send rows, expert-major (R6)
-  KERNEL_TRY(launch_permute(x, (int)T, H, E, k, topk_idx, L->range_off, L->hist, L->send, L->pos,
-                            L->seg_start, st));
+  // ---- split (K3): x -> send rows, expert-major (R6).  At ep == 1 the send
+  // buffer is only the GateUp GEMM's A operand, so by default the split is
+  // index-only and the GEMM gathers x's rows with TMA tile::gather4.
+  const bool gather = (D == 1) && L->gather_a && T > 0;
+  KERNEL_TRY(launch_permute(x, (int)T, H, E, k, topk_idx, L->range_off, L->hist, gather ? nullptr : L->send,
+                            L->pos, L->seg_start, gather ? L->row_token : nullptr, st));
   prof_mark(L, MOE_STAGE_ROUTE, p1, prof_rec(L, st));
+  if (has_shared && !side) {
+    int e = shared_experts(st);
+    if (e) { set_error(std::string("shared experts: ") + cudaGetErrorString((cudaError_t)e)); return MOE_ERR_CUDA; }
+  }
 
   if (D == 1) {
     // ---- EP = 1: no all2all; every chunk is local (C = 0 => PN = 1 is optimal)
     if (!plan_in) plan_compute(c, L->cost, T, nullptr, &plan);
     if (side) CUDA_TRY(cudaStreamWaitEvent(st, L->ev_shared, 0));
-    for (int ch = 0; ch < plan.num_chunks; ++ch) {
+    for (int ch = 0; T > 0 && ch < plan.num_chunks; ++ch) {
       int g0 = plan.group_begin[ch], g1 = plan.group_begin[ch + 1];
       // maximal runs of equal kind inside the chunk
       int a = g0;
       while (a < g1) {
         int b = a + 1;
         while (b < g1 && plan.expert_kind[b] == plan.expert_kind[a]) ++b;
-        int err = compute_moe(L, L->send, L->send_cap, L->seg_start, L->hist, a, b, plan.expert_kind[a], num_ctas,
-                              pick_cta_pair(plan, (double)T * k / E), st);
+        int err = compute_moe(L, gather ? x : L->send, gather ? T : L->send_cap, L->seg_start, L->hist, a, b,
+                              plan.expert_kind[a], num_ctas, pick_cta_pair(plan, (double)T * k / E), st,
+                              gather ? L->row_token : nullptr);
         if (err) { set_error(std::string("ComputeMoE: ") + cudaGetErrorString((cudaError_t)err)); return MOE_ERR_CUDA; }
         a = b;
       }

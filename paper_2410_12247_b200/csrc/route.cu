@@ -174,7 +174,7 @@ __global__ void __launch_bounds__(WARPS * 32, 2)
 permute_kernel(const __nv_bfloat16* __restrict__ x, int T, int H, int E, int k,
                const int32_t* __restrict__ topk_idx, const int32_t* __restrict__ range_off,
                const int32_t* __restrict__ hist, int R, __nv_bfloat16* __restrict__ send,
-               int32_t* __restrict__ pos, int32_t* __restrict__ seg_start_out) {
+               int32_t* __restrict__ pos, int32_t* __restrict__ seg_start_out, int32_t* __restrict__ row_token) {
   __shared__ int32_t seg_s[256];
   __shared__ int32_t scan_tmp[8];
   __shared__ int32_t off_s[WARPS][256];
@@ -199,6 +199,7 @@ permute_kernel(const __nv_bfloat16* __restrict__ x, int T, int H, int E, int k,
       int e = topk_idx[(int64_t)t * k + lane];
       dest = off_s[warp][e];
       pos[(int64_t)t * k + lane] = dest;
+      if (row_token) row_token[dest] = t;
     }
     __syncwarp();
     if (lane < k) {
@@ -206,6 +207,7 @@ permute_kernel(const __nv_bfloat16* __restrict__ x, int T, int H, int E, int k,
       off_s[warp][e] = dest + 1;  // experts of one token are distinct
     }
     __syncwarp();
+    if (send == nullptr) continue;  // index-only split: the GEMM gathers rows of x itself
     const uint4* src = reinterpret_cast<const uint4*>(x + (int64_t)t * H);
     // 16 x 16 B per lane in flight per pass (H <= 4096 per pass, <= 2 passes):
     // keeps the kernel under 128 registers so it co-resides with a GEMM CTA.
@@ -307,11 +309,12 @@ int launch_range_scan(const int32_t* range_hist, int T, int E, int32_t* range_of
 }
 
 int launch_permute(const void* x, int T, int H, int E, int k, const int32_t* topk_idx, const int32_t* range_off,
-                   const int32_t* hist, void* send, int32_t* pos, int32_t* seg_start, cudaStream_t st) {
+                   const int32_t* hist, void* send, int32_t* pos, int32_t* seg_start, int32_t* row_token,
+                   cudaStream_t st) {
   int R = num_ranges(T);
   int blocks = R == 0 ? 1 : (R + WARPS - 1) / WARPS;
   permute_kernel<<<blocks, WARPS * 32, 0, st>>>((const __nv_bfloat16*)x, T, H, E, k, topk_idx, range_off, hist,
-                                                R, (__nv_bfloat16*)send, pos, seg_start);
+                                                R, (__nv_bfloat16*)send, pos, seg_start, row_token);
   return (int)cudaGetLastError();
 }
 

@@ -153,6 +153,23 @@ def test_chunked_equals_unchunked_and_kinds():
         assert torch.equal(v, ys[0])
 
 
+@pytest.mark.parametrize("tile_m", [128, 256])
+def test_gathered_gateup_equals_materialised_split(tile_m, monkeypatch):
+    """ep == 1: GateUp reading x through TMA tile::gather4 == reading the
+    materialised expert-major send buffer, bit for bit."""
+    kw, k, norm = CASES["mid_shared"]
+    inp = Inputs(seed=12, **kw)
+    x = dev_bf16(inp.x)
+    ys = []
+    for g in ("0", "1"):
+        monkeypatch.setenv("EPSMOE_GATHER", g)
+        L = layer_from_inputs(inp, k, norm)
+        ys.append(L.forward(x, plan=make_plan(1, MOE_GEMM_GROUPED, tile_m=tile_m)).clone())
+        torch.cuda.synchronize()
+        L.close()
+    assert torch.equal(ys[0], ys[1])
+
+
 def test_fig_eps_overview_explicit_routing():
     fx = json.load(open(os.path.join(GOLDEN, "fig_eps_overview.json")))
     idx = np.array(fx["routing"], np.int32)
