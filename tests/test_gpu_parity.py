@@ -186,6 +186,24 @@ def test_fig_eps_overview_explicit_routing():
     assert_close(to_f32(y), ref["y"], "fixture")
 
 
+def test_calibrated_cost_model_drives_plan():
+    """moe_layer_calibrate measures GEMM ms per expert vs rows for both kinds
+    (the X2/X3 analog on B200); the plan then follows the measured model."""
+    inp = Inputs(E=16, k=4, H=512, F=384, T=2000, seed=4)
+    L = layer_from_inputs(inp, 4, 0, max_tokens=8192)
+    m = L.calibrate()
+    assert 3 <= m.n_points <= 12
+    pts = list(m.m_points[:m.n_points])
+    assert pts == sorted(pts)
+    for kind in (0, 1):
+        ms = list(m.gemm_ms[kind][:m.n_points])
+        assert all(v > 0 for v in ms)
+        assert ms[-1] > ms[0]                     # more rows, more time
+    p = L.plan(8192)
+    assert p.num_chunks == 1                      # ep == 1: nothing to overlap (P:404)
+    assert all(p.expert_kind[e] in (1, 2) for e in range(16))
+
+
 def test_empty_and_single_token():
     inp = Inputs(E=8, k=2, H=64, F=128, T=1, seed=3)
     L = layer_from_inputs(inp, 2, 1, max_tokens=64)
