@@ -168,6 +168,15 @@ moe_status_t moe_layer_create(const moe_config_t* cfg, const moe_weights_t* w,
 
 moe_status_t moe_layer_destroy(moe_layer_t* layer);
 
+/* In-process EP group for tests on ONE GPU: the ep ranks are ep layer objects
+ * of one process, each driven by its own host thread; the all2all becomes
+ * host-rendezvous + device-to-device copies (same forward code as NCCL).
+ * moe_layer_create_local replaces moe_layer_create's NCCL ids with `group`. */
+moe_status_t moe_local_group_create(int32_t ep, void** group);
+moe_status_t moe_local_group_destroy(void* group);
+moe_status_t moe_layer_create_local(const moe_config_t* cfg, const moe_weights_t* w, void* group,
+                                    void* workspace, size_t workspace_bytes, moe_layer_t** out);
+
 /* ------------------------------------------------------------------ planner */
 
 /* Pure, host-only, deterministic: the expert pipeline scheduler.

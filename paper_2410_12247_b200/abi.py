@@ -74,6 +74,10 @@ _SIGS = {
     "moe_layer_create": (C.c_int, [C.POINTER(moe_config_t), C.POINTER(moe_weights_t), C.c_void_p, C.c_void_p,
                                    C.c_void_p, C.c_size_t, C.POINTER(C.c_void_p)]),
     "moe_layer_destroy": (C.c_int, [C.c_void_p]),
+    "moe_local_group_create": (C.c_int, [C.c_int32, C.POINTER(C.c_void_p)]),
+    "moe_local_group_destroy": (C.c_int, [C.c_void_p]),
+    "moe_layer_create_local": (C.c_int, [C.POINTER(moe_config_t), C.POINTER(moe_weights_t), C.c_void_p,
+                                         C.c_void_p, C.c_size_t, C.POINTER(C.c_void_p)]),
     "moe_plan_compute": (C.c_int, [C.POINTER(moe_config_t), C.POINTER(moe_cost_model_t), C.c_int64,
                                    C.c_void_p, C.POINTER(moe_plan_t)]),
     "moe_plan_pipeline": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.POINTER(moe_plan_t)]),

@@ -51,6 +51,7 @@ struct Cfg {
 struct KParams {
   int K, N, G, m_single, b_group_rows, b_base;
   int raster_gm;  // tile order inside a group: blocks of raster_gm m-tiles, m fastest inside a block
+  int tma_hint;   // CTA-pair loads: 0 no L2 hint, 1 evict_normal, 2 evict_normal A / evict_last B
   int64_t ldo;
   void* out;
   const float* bias;
@@ -187,6 +188,8 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
     // GATHER: the whole warp stages the tile's 128 physical A row indices in
     // smem; lane 0 then issues 32 tile::gather4 loads per stage.
     uint32_t stage = 0, phase = 0;
+    const uint64_t pol_a = ptx::policy_evict_normal();
+    const uint64_t pol_b = p.tma_hint == 2 ? ptx::policy_evict_last() : ptx::policy_evict_normal();
     for (int t = unit; t < total; t += num_units) {
       int g, mt, nt;
       decode_tile(st, G, n_tiles, p.raster_gm, t, g, mt, nt);
@@ -233,11 +236,16 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
           } else {
             // the leader's full barrier counts both CTAs' bytes
             if (rank == 0) ptx::mbar_arrive_expect_tx(fb, 2 * (C::A_BYTES + C::B_BYTES));
-            ptx::tma_load_2d_pair(a_dst, &tmA, fb, kb * BK, a_row);
-            if (EPI == EPI_SWIGLU)  // CTA0: gate rows -> acc cols [0,128); CTA1: up rows -> [128,256)
-              ptx::tma_load_2d_pair(b_dst, rank == 0 ? &tmB0 : &tmB1, fb, kb * BK, b_row0);
-            else
-              ptx::tma_load_2d_pair(b_dst, &tmB0, fb, kb * BK, b_row0 + (int)rank * C::B_ROWS);
+            const void* tb = (EPI == EPI_SWIGLU && rank == 1) ? (const void*)&tmB1 : (const void*)&tmB0;
+            // SwiGLU: CTA0 gate rows -> acc cols [0,128); CTA1 up rows -> [128,256)
+            const int brow = (EPI == EPI_SWIGLU) ? b_row0 : b_row0 + (int)rank * C::B_ROWS;
+            if (p.tma_hint == 0) {
+              ptx::tma_load_2d_pair(a_dst, &tmA, fb, kb * BK, a_row);
+              ptx::tma_load_2d_pair(b_dst, tb, fb, kb * BK, brow);
+            } else {
+              ptx::tma_load_2d_pair_hint(a_dst, &tmA, fb, kb * BK, a_row, pol_a);
+              ptx::tma_load_2d_pair_hint(b_dst, tb, fb, kb * BK, brow, pol_b);
+            }
           }
           if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
         }
@@ -382,6 +390,11 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
   return fn;
 }
 
+int env_int(const char* name, int dflt) {
+  const char* e = std::getenv(name);
+  return e ? std::atoi(e) : dflt;
+}
+
 // Tile rasterisation block (m-tiles); 4 measured best on DSv2 and Mixtral
 // shapes (tools/gemm_bench.py, profiles/r01_notes.md); EPSMOE_RASTER_GM overrides.
 int raster_gm() {
@@ -437,6 +450,7 @@ int launch_epi(const GemmArgs& a, cudaStream_t stream) {
   p.b_group_rows = a.b_group_rows;
   p.b_base = a.b_base;
   p.raster_gm = raster_gm();
+  p.tma_hint = env_int("EPSMOE_TMA_HINT", 0);
   p.ldo = a.ldo;
   p.out = a.out;
   p.bias = a.bias;

@@ -21,6 +21,7 @@
 #include "gemm.h"
 #include "internal.h"
 #include "route.h"
+#include "transport.h"
 
 struct moe_layer {
   moe_config_t cfg;
@@ -50,7 +51,7 @@ struct moe_layer {
                                   // slower GateUp on B200 (32 gather4 per stage), so off by default
   cudaEvent_t ev_hist = nullptr, ev_ready = nullptr, ev_comb_done = nullptr;
   std::vector<cudaEvent_t> ev_disp, ev_gemm;
-  ncclComm_t comm_d = nullptr, comm_c = nullptr;
+  epsmoe::Transport* tr = nullptr;  // all2all transport (NCCL, or in-process for tests), ep > 1
   moe_cost_model_t cost;
   int last_launches = 0;
   // per-stage device timing (moe_layer_set_profiling)
@@ -86,6 +87,11 @@ using namespace epsmoe;
       return MOE_ERR_CUDA;                                                                \
     }                                                                                     \
     ++L->last_launches;                                                                   \
+  } while (0)
+#define TR_TRY(expr)                                                                      \
+  do {                                                                                    \
+    int _r = (expr);                                                                      \
+    if (_r != 0) return (moe_status_t)_r;                                                 \
   } while (0)
 #define NCCL_TRY(expr)                                                                    \
   do {                                                                                    \
@@ -295,8 +301,20 @@ moe_status_t moe_plan_compute(const moe_config_t* cfg, const moe_cost_model_t* c
   return (moe_status_t)plan_compute(*cfg, *cost, global_tokens, global_hist, out);
 }
 
-moe_status_t moe_layer_create(const moe_config_t* cfg, const moe_weights_t* w, const void* uid_d,
-                              const void* uid_c, void* workspace, size_t workspace_bytes, moe_layer_t** out) {
+moe_status_t moe_local_group_create(int32_t ep, void** out) {
+  if (!out || ep < 1) { set_error("bad argument"); return MOE_ERR_INVALID; }
+  *out = new epsmoe::LocalGroup(ep);
+  return MOE_OK;
+}
+
+moe_status_t moe_local_group_destroy(void* group) {
+  delete static_cast<epsmoe::LocalGroup*>(group);
+  return MOE_OK;
+}
+
+static moe_status_t create_impl(const moe_config_t* cfg, const moe_weights_t* w, const void* uid_d,
+                                const void* uid_c, epsmoe::LocalGroup* group, void* workspace,
+                                size_t workspace_bytes, moe_layer_t** out) {
   if (!out || !w) { set_error("null argument"); return MOE_ERR_INVALID; }
   *out = nullptr;
   int v = validate(cfg);
@@ -306,7 +324,11 @@ moe_status_t moe_layer_create(const moe_config_t* cfg, const moe_weights_t* w, c
     set_error("missing shared-expert weights");
     return MOE_ERR_INVALID;
   }
-  if (cfg->ep > 1 && (!uid_d || !uid_c)) { set_error("ep > 1 needs two NCCL unique ids"); return MOE_ERR_INVALID; }
+  if (cfg->ep > 1 && !group && (!uid_d || !uid_c)) {
+    set_error("ep > 1 needs two NCCL unique ids");
+    return MOE_ERR_INVALID;
+  }
+  if (group && group->ep != cfg->ep) { set_error("local group size != ep"); return MOE_ERR_INVALID; }
   moe_layer* L = new moe_layer();
   L->cfg = *cfg;
   L->w = *w;
@@ -363,33 +385,39 @@ moe_status_t moe_layer_create(const moe_config_t* cfg, const moe_weights_t* w, c
       cudaEventCreateWithFlags(&L->ev_disp[i], cudaEventDisableTiming);
       cudaEventCreateWithFlags(&L->ev_gemm[i], cudaEventDisableTiming);
     }
-    ncclUniqueId id_d, id_c;
-    std::memcpy(&id_d, uid_d, sizeof(id_d));
-    std::memcpy(&id_c, uid_c, sizeof(id_c));
-    ncclConfig_t ncfg = NCCL_CONFIG_INITIALIZER;
-    ncfg.blocking = 1;
-    ncclResult_t r1 = ncclCommInitRankConfig(&L->comm_d, cfg->ep, id_d, cfg->rank, &ncfg);
-    ncclResult_t r2 = r1 == ncclSuccess ? ncclCommInitRankConfig(&L->comm_c, cfg->ep, id_c, cfg->rank, &ncfg) : r1;
-    if (r1 != ncclSuccess || r2 != ncclSuccess) {
-      set_error(std::string("ncclCommInitRankConfig: ") + ncclGetErrorString(r1 != ncclSuccess ? r1 : r2));
-      return fail(MOE_ERR_NCCL);
-    }
-    // every rank must agree on the shape (MOE_ERR_MISMATCH)
-    int64_t sig[8] = {cfg->num_experts, cfg->top_k, cfg->hidden, cfg->ffn, cfg->num_shared, cfg->shared_ffn,
-                      cfg->norm_topk, (int64_t)(cfg->routed_scale * 1e6)};
-    int64_t* d_sig = nullptr;
-    if (cudaMalloc(&d_sig, sizeof(sig) * (cfg->ep + 1)) != cudaSuccess) return fail(MOE_ERR_CUDA);
-    cudaMemcpy(d_sig, sig, sizeof(sig), cudaMemcpyHostToDevice);
-    ncclResult_t r3 = ncclAllGather(d_sig, d_sig + 8, 8, ncclInt64, L->comm_d, 0);
-    std::vector<int64_t> all(8 * cfg->ep);
-    cudaMemcpy(all.data(), d_sig + 8, sizeof(int64_t) * 8 * cfg->ep, cudaMemcpyDeviceToHost);
-    cudaFree(d_sig);
-    if (r3 != ncclSuccess) return fail(MOE_ERR_NCCL);
-    for (int r = 0; r < cfg->ep; ++r)
-      if (std::memcmp(all.data() + 8 * r, sig, sizeof(sig)) != 0) {
-        set_error("config mismatch across ranks");
-        return fail(MOE_ERR_MISMATCH);
+    if (group) {
+      L->tr = new epsmoe::LocalTransport(group, cfg->rank);
+    } else {
+      ncclUniqueId id_d, id_c;
+      std::memcpy(&id_d, uid_d, sizeof(id_d));
+      std::memcpy(&id_c, uid_c, sizeof(id_c));
+      ncclConfig_t ncfg = NCCL_CONFIG_INITIALIZER;
+      ncfg.blocking = 1;
+      ncclComm_t cd = nullptr, cc = nullptr;
+      ncclResult_t r1 = ncclCommInitRankConfig(&cd, cfg->ep, id_d, cfg->rank, &ncfg);
+      ncclResult_t r2 = r1 == ncclSuccess ? ncclCommInitRankConfig(&cc, cfg->ep, id_c, cfg->rank, &ncfg) : r1;
+      L->tr = new epsmoe::NcclTransport(cd, cc);
+      if (r1 != ncclSuccess || r2 != ncclSuccess) {
+        set_error(std::string("ncclCommInitRankConfig: ") + ncclGetErrorString(r1 != ncclSuccess ? r1 : r2));
+        return fail(MOE_ERR_NCCL);
       }
+      // every rank must agree on the shape (MOE_ERR_MISMATCH)
+      int32_t sig[8] = {cfg->num_experts, cfg->top_k, cfg->hidden, cfg->ffn, cfg->num_shared, cfg->shared_ffn,
+                        cfg->norm_topk, (int32_t)(cfg->routed_scale * 1e6f)};
+      int32_t* d_sig = nullptr;
+      if (cudaMalloc(&d_sig, sizeof(sig) * (cfg->ep + 1)) != cudaSuccess) return fail(MOE_ERR_CUDA);
+      cudaMemcpy(d_sig, sig, sizeof(sig), cudaMemcpyHostToDevice);
+      int r3 = L->tr->allgather_i32(d_sig, d_sig + 8, 8, 0);
+      std::vector<int32_t> all(8 * cfg->ep);
+      cudaMemcpy(all.data(), d_sig + 8, sizeof(int32_t) * 8 * cfg->ep, cudaMemcpyDeviceToHost);
+      cudaFree(d_sig);
+      if (r3) return fail((moe_status_t)r3);
+      for (int r = 0; r < cfg->ep; ++r)
+        if (std::memcmp(all.data() + 8 * r, sig, sizeof(sig)) != 0) {
+          set_error("config mismatch across ranks");
+          return fail(MOE_ERR_MISMATCH);
+        }
+    }
   }
   if (cudaDeviceSynchronize() != cudaSuccess) {
     set_error(std::string("create: ") + cudaGetErrorString(cudaGetLastError()));
@@ -399,10 +427,21 @@ moe_status_t moe_layer_create(const moe_config_t* cfg, const moe_weights_t* w, c
   return MOE_OK;
 }
 
+moe_status_t moe_layer_create(const moe_config_t* cfg, const moe_weights_t* w, const void* uid_d,
+                              const void* uid_c, void* workspace, size_t workspace_bytes, moe_layer_t** out) {
+  return create_impl(cfg, w, uid_d, uid_c, nullptr, workspace, workspace_bytes, out);
+}
+
+moe_status_t moe_layer_create_local(const moe_config_t* cfg, const moe_weights_t* w, void* group, void* workspace,
+                                    size_t workspace_bytes, moe_layer_t** out) {
+  if (!group) { set_error("null group"); return MOE_ERR_INVALID; }
+  return create_impl(cfg, w, nullptr, nullptr, static_cast<epsmoe::LocalGroup*>(group), workspace,
+                     workspace_bytes, out);
+}
+
 moe_status_t moe_layer_destroy(moe_layer_t* L) {
   if (!L) return MOE_OK;
-  if (L->comm_d) ncclCommDestroy(L->comm_d);
-  if (L->comm_c) ncclCommDestroy(L->comm_c);
+  delete L->tr;
   if (L->s_disp) cudaStreamDestroy(L->s_disp);
   if (L->s_side) cudaStreamDestroy(L->s_side);
   for (cudaEvent_t e : {L->ev_router, L->ev_shared})
@@ -635,7 +674,7 @@ moe_status_t moe_layer_forward(moe_layer_t* L, const void* x, int64_t T, void* y
     prof_mark(L, MOE_STAGE_COMBINE, c0, prof_rec(L, st));
   } else {
     // ---- EP > 1: count exchange (C3), plan, chunked dispatch / compute / combine
-    NCCL_TRY(ncclAllGather(L->hist, L->ghist, E, ncclInt32, L->comm_d, st));
+    TR_TRY(L->tr->allgather_i32(L->hist, L->ghist, E, st));
     CUDA_TRY(cudaMemcpyAsync(L->ghist_host, L->ghist, sizeof(int32_t) * D * E, cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaEventRecord(L->ev_hist, st));
     CUDA_TRY(cudaEventSynchronize(L->ev_hist));
@@ -665,19 +704,19 @@ moe_status_t moe_layer_forward(moe_layer_t* L, const void* x, int64_t T, void* y
     auto dispatch = [&](int ch) -> moe_status_t {
       int g0 = plan.group_begin[ch], g1 = plan.group_begin[ch + 1];
       int d0 = prof_rec(L, L->s_disp);
-      NCCL_TRY(ncclGroupStart());
+      TR_TRY(L->tr->group_start(0));
       for (int peer = 0; peer < D; ++peer)
         for (int el = g0; el < g1; ++el) {
           int ex = peer * E_loc + el;
           int64_t n_send = gh[(int64_t)me * E + ex];
           if (n_send)
-            NCCL_TRY(ncclSend((char*)L->send + send_off[ex] * row_bytes, n_send * H, ncclBfloat16, peer, L->comm_d, L->s_disp));
+            TR_TRY(L->tr->send((char*)L->send + send_off[ex] * row_bytes, n_send * row_bytes, peer, 0, L->s_disp));
           int64_t n_recv = gh[(int64_t)peer * E + me * E_loc + el];
           if (n_recv)
-            NCCL_TRY(ncclRecv((char*)L->recv + recv_off[(size_t)el * D + peer] * row_bytes, n_recv * H, ncclBfloat16,
-                              peer, L->comm_d, L->s_disp));
+            TR_TRY(L->tr->recv((char*)L->recv + recv_off[(size_t)el * D + peer] * row_bytes, n_recv * row_bytes, peer,
+                               0, L->s_disp));
         }
-      NCCL_TRY(ncclGroupEnd());
+      TR_TRY(L->tr->group_end(0, L->s_disp));
       prof_mark(L, MOE_STAGE_DISPATCH, d0, prof_rec(L, L->s_disp));
       CUDA_TRY(cudaEventRecord(L->ev_disp[ch], L->s_disp));
       return MOE_OK;
@@ -686,20 +725,19 @@ moe_status_t moe_layer_forward(moe_layer_t* L, const void* x, int64_t T, void* y
       int g0 = plan.group_begin[ch], g1 = plan.group_begin[ch + 1];
       CUDA_TRY(cudaStreamWaitEvent(L->s_comb, L->ev_gemm[ch], 0));
       int b0 = prof_rec(L, L->s_comb);
-      NCCL_TRY(ncclGroupStart());
+      TR_TRY(L->tr->group_start(1));
       for (int peer = 0; peer < D; ++peer)
         for (int el = g0; el < g1; ++el) {
           int64_t n_back = gh[(int64_t)peer * E + me * E_loc + el];
           if (n_back)
-            NCCL_TRY(ncclSend((char*)L->o + recv_off[(size_t)el * D + peer] * row_bytes, n_back * H, ncclBfloat16, peer,
-                              L->comm_c, L->s_comb));
+            TR_TRY(L->tr->send((char*)L->o + recv_off[(size_t)el * D + peer] * row_bytes, n_back * row_bytes, peer, 1,
+                               L->s_comb));
           int ex = peer * E_loc + el;
           int64_t n_home = gh[(int64_t)me * E + ex];
           if (n_home)
-            NCCL_TRY(ncclRecv((char*)L->comb + send_off[ex] * row_bytes, n_home * H, ncclBfloat16, peer, L->comm_c,
-                              L->s_comb));
+            TR_TRY(L->tr->recv((char*)L->comb + send_off[ex] * row_bytes, n_home * row_bytes, peer, 1, L->s_comb));
         }
-      NCCL_TRY(ncclGroupEnd());
+      TR_TRY(L->tr->group_end(1, L->s_comb));
       prof_mark(L, MOE_STAGE_COMB_A2A, b0, prof_rec(L, L->s_comb));
       return MOE_OK;
     };

@@ -1,0 +1,131 @@
+// Transports for the EP all2all (see transport.h).  Return codes: 0 = ok,
+// MOE_ERR_NCCL / MOE_ERR_CUDA on failure (message via set_error).
+#include "transport.h"
+
+#include <string>
+
+#include "../../include/epsmoe.h"
+#include "internal.h"
+
+namespace epsmoe {
+
+// ------------------------------------------------------------------ NCCL
+NcclTransport::~NcclTransport() {
+  for (auto c : comm_)
+    if (c) ncclCommDestroy(c);
+}
+
+static int nccl_err(ncclResult_t r, const char* what) {
+  if (r == ncclSuccess) return 0;
+  set_error(std::string(what) + ": " + ncclGetErrorString(r));
+  return MOE_ERR_NCCL;
+}
+
+int NcclTransport::allgather_i32(const int32_t* send, int32_t* recv, size_t count, cudaStream_t st) {
+  return nccl_err(ncclAllGather(send, recv, count, ncclInt32, comm_[0], st), "ncclAllGather");
+}
+int NcclTransport::group_start(int) { return nccl_err(ncclGroupStart(), "ncclGroupStart"); }
+int NcclTransport::send(const void* buf, size_t bytes, int peer, int channel, cudaStream_t st) {
+  return nccl_err(ncclSend(buf, bytes, ncclUint8, peer, comm_[channel], st), "ncclSend");
+}
+int NcclTransport::recv(void* buf, size_t bytes, int peer, int channel, cudaStream_t st) {
+  return nccl_err(ncclRecv(buf, bytes, ncclUint8, peer, comm_[channel], st), "ncclRecv");
+}
+int NcclTransport::group_end(int, cudaStream_t) { return nccl_err(ncclGroupEnd(), "ncclGroupEnd"); }
+
+// ------------------------------------------------------------------ local
+LocalGroup::LocalGroup(int n) : ep(n), sends(n), recvs(n), gather_src(n), ev_ready(n), ev_done(n) {
+  for (int r = 0; r < n; ++r) {
+    cudaEventCreateWithFlags(&ev_ready[r], cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&ev_done[r], cudaEventDisableTiming);
+  }
+}
+LocalGroup::~LocalGroup() {
+  for (int r = 0; r < ep; ++r) {
+    cudaEventDestroy(ev_ready[r]);
+    cudaEventDestroy(ev_done[r]);
+  }
+}
+void LocalGroup::barrier() {
+  std::unique_lock<std::mutex> lk(mu);
+  uint64_t gen = generation;
+  if (++arrived == ep) {
+    arrived = 0;
+    ++generation;
+    cv.notify_all();
+  } else {
+    cv.wait(lk, [&] { return generation != gen; });
+  }
+}
+
+static int cuda_err(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return 0;
+  set_error(std::string(what) + ": " + cudaGetErrorString(e));
+  return MOE_ERR_CUDA;
+}
+
+int LocalTransport::allgather_i32(const int32_t* send, int32_t* recv, size_t count, cudaStream_t st) {
+  LocalGroup& g = *g_;
+  g.gather_src[rank_] = send;
+  if (int e = cuda_err(cudaEventRecord(g.ev_ready[rank_], st), "cudaEventRecord")) return e;
+  g.barrier();
+  for (int p = 0; p < g.ep; ++p) {
+    if (int e = cuda_err(cudaStreamWaitEvent(st, g.ev_ready[p], 0), "cudaStreamWaitEvent")) return e;
+    if (int e = cuda_err(cudaMemcpyAsync(recv + (size_t)p * count, g.gather_src[p], count * sizeof(int32_t),
+                                         cudaMemcpyDeviceToDevice, st),
+                         "cudaMemcpyAsync"))
+      return e;
+  }
+  if (int e = cuda_err(cudaEventRecord(g.ev_done[rank_], st), "cudaEventRecord")) return e;
+  g.barrier();
+  for (int p = 0; p < g.ep; ++p)  // sources stay untouched until every reader copied them
+    if (int e = cuda_err(cudaStreamWaitEvent(st, g.ev_done[p], 0), "cudaStreamWaitEvent")) return e;
+  g.barrier();
+  return 0;
+}
+
+int LocalTransport::group_start(int) {
+  g_->sends[rank_].clear();
+  g_->recvs[rank_].clear();
+  return 0;
+}
+int LocalTransport::send(const void* buf, size_t bytes, int peer, int, cudaStream_t) {
+  g_->sends[rank_].push_back({buf, nullptr, bytes, peer});
+  return 0;
+}
+int LocalTransport::recv(void* buf, size_t bytes, int peer, int, cudaStream_t) {
+  g_->recvs[rank_].push_back({nullptr, buf, bytes, peer});
+  return 0;
+}
+
+int LocalTransport::group_end(int, cudaStream_t st) {
+  LocalGroup& g = *g_;
+  if (int e = cuda_err(cudaEventRecord(g.ev_ready[rank_], st), "cudaEventRecord")) return e;
+  g.barrier();  // every rank has posted its ops and recorded its ready event
+  std::vector<size_t> next(g.ep, 0);
+  for (const auto& rv : g.recvs[rank_]) {
+    // k-th recv from peer p matches p's k-th send to this rank (NCCL p2p order)
+    const auto& ps = g.sends[rv.peer];
+    size_t& i = next[rv.peer];
+    while (i < ps.size() && ps[i].peer != rank_) ++i;
+    if (i >= ps.size() || ps[i].bytes != rv.bytes) {
+      set_error("local transport: unmatched recv from rank " + std::to_string(rv.peer));
+      g.barrier();
+      g.barrier();
+      return MOE_ERR_MISMATCH;
+    }
+    if (int e = cuda_err(cudaStreamWaitEvent(st, g.ev_ready[rv.peer], 0), "cudaStreamWaitEvent")) return e;
+    if (int e = cuda_err(cudaMemcpyAsync(rv.dst, ps[i].src, rv.bytes, cudaMemcpyDeviceToDevice, st),
+                         "cudaMemcpyAsync"))
+      return e;
+    ++i;
+  }
+  if (int e = cuda_err(cudaEventRecord(g.ev_done[rank_], st), "cudaEventRecord")) return e;
+  g.barrier();  // all copies enqueued
+  for (int p = 0; p < g.ep; ++p)  // a sender's buffer is reusable once its readers copied it
+    if (int e = cuda_err(cudaStreamWaitEvent(st, g.ev_done[p], 0), "cudaStreamWaitEvent")) return e;
+  g.barrier();  // nobody re-records ev_done before every rank waited on it
+  return 0;
+}
+
+}  // namespace epsmoe

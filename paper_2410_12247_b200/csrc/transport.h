@@ -1,0 +1,87 @@
+// All2all transport behind the EP layer.
+//
+//   NcclTransport  — production: two NCCL communicators over NVLink (channel 0 =
+//                    dispatch, channel 1 = combine) so both phases can be in
+//                    flight; grouped ncclSend/ncclRecv; ncclAllGather of counts.
+//   LocalTransport — test transport: the ep ranks are ep layer objects in ONE
+//                    process on ONE GPU, each driven by its own host thread.
+//                    Every group end is a host rendezvous; each posted recv is
+//                    matched to the peer's send (same order) and executed as a
+//                    device-to-device cudaMemcpyAsync on the receiver's stream,
+//                    event-chained to the sender.  It lets the very same EP
+//                    forward code (tables, chunk DAG, events) run on one B200.
+#pragma once
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <condition_variable>
+#include <cstdint>
+#include <mutex>
+#include <vector>
+
+namespace epsmoe {
+
+class Transport {
+ public:
+  virtual ~Transport() = default;
+  // recv[r * count + i] = send_of_rank_r[i]; stream-ordered on `st`.
+  virtual int allgather_i32(const int32_t* send, int32_t* recv, size_t count, cudaStream_t st) = 0;
+  virtual int group_start(int channel) = 0;
+  virtual int send(const void* buf, size_t bytes, int peer, int channel, cudaStream_t st) = 0;
+  virtual int recv(void* buf, size_t bytes, int peer, int channel, cudaStream_t st) = 0;
+  virtual int group_end(int channel, cudaStream_t st) = 0;
+  virtual const char* name() const = 0;
+};
+
+class NcclTransport : public Transport {
+ public:
+  NcclTransport(ncclComm_t d, ncclComm_t c) : comm_{d, c} {}
+  ~NcclTransport() override;
+  int allgather_i32(const int32_t* send, int32_t* recv, size_t count, cudaStream_t st) override;
+  int group_start(int channel) override;
+  int send(const void* buf, size_t bytes, int peer, int channel, cudaStream_t st) override;
+  int recv(void* buf, size_t bytes, int peer, int channel, cudaStream_t st) override;
+  int group_end(int channel, cudaStream_t st) override;
+  const char* name() const override { return "nccl"; }
+
+ private:
+  ncclComm_t comm_[2];
+};
+
+// Shared rendezvous state of the ep local ranks (moe_local_group_create).
+struct LocalGroup {
+  explicit LocalGroup(int ep);
+  ~LocalGroup();
+  void barrier();
+  struct Op {
+    const void* src;
+    void* dst;
+    size_t bytes;
+    int peer;
+  };
+  int ep;
+  std::mutex mu;
+  std::condition_variable cv;
+  int arrived = 0;
+  uint64_t generation = 0;
+  std::vector<std::vector<Op>> sends, recvs;  // [rank] ops posted in the current group
+  std::vector<const void*> gather_src;        // [rank] allgather source pointers
+  std::vector<cudaEvent_t> ev_ready, ev_done; // [rank]
+};
+
+class LocalTransport : public Transport {
+ public:
+  LocalTransport(LocalGroup* g, int rank) : g_(g), rank_(rank) {}
+  int allgather_i32(const int32_t* send, int32_t* recv, size_t count, cudaStream_t st) override;
+  int group_start(int channel) override;
+  int send(const void* buf, size_t bytes, int peer, int channel, cudaStream_t st) override;
+  int recv(void* buf, size_t bytes, int peer, int channel, cudaStream_t st) override;
+  int group_end(int channel, cudaStream_t st) override;
+  const char* name() const override { return "local"; }
+
+ private:
+  LocalGroup* g_;
+  int rank_;
+};
+
+}  // namespace epsmoe

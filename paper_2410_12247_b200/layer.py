@@ -17,6 +17,23 @@ def _ptr(t):
     return None if t is None else C.c_void_p(t.data_ptr())
 
 
+class LocalGroup:
+    """In-process EP group (moe_local_group_create): `ep` MoELayer ranks on one
+    GPU, each forward driven from its own host thread (tests only)."""
+
+    def __init__(self, ep: int):
+        self.ep = ep
+        h = C.c_void_p()
+        abi.check(abi.lib().moe_local_group_create(ep, C.byref(h)), "moe_local_group_create")
+        self.handle = h
+
+    def __del__(self):
+        try:
+            abi.lib().moe_local_group_destroy(self.handle)
+        except Exception:
+            pass
+
+
 class MoELayer:
     """weights: dict of DEVICE tensors (bf16): w_router [E,H], w_gate / w_up
     [E_loc,F,H], w_down [E_loc,H,F], optional ws_gate / ws_up [S*Fs,H],
@@ -24,7 +41,7 @@ class MoELayer:
 
     def __init__(self, E, k, H, F, weights, S=0, Fs=0, ep=1, rank=0, max_tokens=1, norm_topk=0,
                  routed_scale=1.0, uid_dispatch: bytes | None = None, uid_combine: bytes | None = None,
-                 device=None):
+                 device=None, local_group: "LocalGroup | None" = None):
         self.lib = abi.lib()
         self.cfg = abi.make_config(E, k, H, F, S, Fs, ep, rank, max_tokens, norm_topk, routed_scale)
         self.E, self.k, self.H, self.F, self.S, self.Fs, self.ep, self.rank = E, k, H, F, S, Fs, ep, rank
@@ -41,9 +58,15 @@ class MoELayer:
         ud = C.create_string_buffer(uid_dispatch, 128) if uid_dispatch is not None else None
         uc = C.create_string_buffer(uid_combine, 128) if uid_combine is not None else None
         with torch.cuda.device(self.device):
-            abi.check(self.lib.moe_layer_create(C.byref(self.cfg), C.byref(w), ud, uc,
-                                                C.c_void_p(self.workspace.data_ptr()), nbytes, C.byref(h)),
-                      "moe_layer_create")
+            if local_group is not None:
+                self.local_group = local_group  # keep alive
+                abi.check(self.lib.moe_layer_create_local(C.byref(self.cfg), C.byref(w), local_group.handle,
+                                                          C.c_void_p(self.workspace.data_ptr()), nbytes, C.byref(h)),
+                          "moe_layer_create_local")
+            else:
+                abi.check(self.lib.moe_layer_create(C.byref(self.cfg), C.byref(w), ud, uc,
+                                                    C.c_void_p(self.workspace.data_ptr()), nbytes, C.byref(h)),
+                          "moe_layer_create")
         self.handle = h
 
     # ------------------------------------------------------------------

@@ -1,0 +1,122 @@
+"""EP > 1 on one B200: `ep` rank-layers in one process, each forward driven by
+its own host thread, all2all through the in-process transport (host
+rendezvous + device copies).  The forward code is the NCCL path's: count
+allgather, host plan, moe_exchange_layout tables, Algorithm 1's chunk DAG on
+three streams, per-(peer, expert) dispatch/combine messages.
+
+Checks: per-rank histograms, permutation and plan vs the oracle's EP
+simulation; EP = D output == EP = 1 output bit for bit (R6: every expert sees
+the same rows in the same order at any D); chunked == unchunked; y vs oracle."""
+import threading
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from gen import Inputs
+from paper_2410_12247_b200 import MOE_GEMM_DENSE, MOE_GEMM_GROUPED, LocalGroup, MoELayer, make_plan
+
+from .gpu_util import assert_close, dev_bf16, to_f32
+
+pytestmark = pytest.mark.gpu
+
+
+def _ep_forward(inp, k, norm, D, plan=None, skew_bias=None):
+    E, H, F, T = inp.E, inp.H, inp.F, inp.T
+    E_loc = E // D
+    start = oracle.token_shards(T, D)
+    group = LocalGroup(D)
+    layers, xs = [], []
+    for r in range(D):
+        w = dict(w_router=dev_bf16(inp.w_router), w_gate=dev_bf16(inp.w_gate[r * E_loc:(r + 1) * E_loc]),
+                 w_up=dev_bf16(inp.w_up[r * E_loc:(r + 1) * E_loc]),
+                 w_down=dev_bf16(inp.w_down[r * E_loc:(r + 1) * E_loc]))
+        if inp.S:
+            w.update(ws_gate=dev_bf16(inp.ws_gate), ws_up=dev_bf16(inp.ws_up), ws_down=dev_bf16(inp.ws_down))
+        if skew_bias is not None:
+            w["router_bias"] = torch.from_numpy(skew_bias).cuda()
+        T_loc = int(start[r + 1] - start[r])
+        layers.append(MoELayer(E, k, H, F, w, S=inp.S, Fs=inp.Fs, ep=D, rank=r, max_tokens=max(T_loc, 1),
+                               norm_topk=norm, local_group=group))
+        xs.append(dev_bf16(inp.x[start[r]:start[r + 1]]))
+    ys, bufs, errs = [None] * D, [None] * D, []
+
+    def worker(r):
+        try:
+            torch.cuda.set_device(0)
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                d, b = layers[r].debug_buffers(xs[r].shape[0])
+                ys[r] = layers[r].forward(xs[r], plan=plan, stream=s, debug=d)
+                s.synchronize()
+                bufs[r] = b
+        except Exception as e:  # pragma: no cover
+            errs.append(repr(e))
+
+    th = [threading.Thread(target=worker, args=(r,), daemon=True) for r in range(D)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=120)
+    assert not errs, errs
+    assert all(not t.is_alive() for t in th), "EP forward deadlocked"
+    y = torch.cat(ys).float().cpu().numpy()
+    for L in layers:
+        L.close()
+    return y, bufs
+
+
+def _ep1_forward(inp, k, norm, plan=None, skew_bias=None):
+    w = dict(w_router=dev_bf16(inp.w_router), w_gate=dev_bf16(inp.w_gate), w_up=dev_bf16(inp.w_up),
+             w_down=dev_bf16(inp.w_down))
+    if inp.S:
+        w.update(ws_gate=dev_bf16(inp.ws_gate), ws_up=dev_bf16(inp.ws_up), ws_down=dev_bf16(inp.ws_down))
+    if skew_bias is not None:
+        w["router_bias"] = torch.from_numpy(skew_bias).cuda()
+    L = MoELayer(inp.E, k, inp.H, inp.F, w, S=inp.S, Fs=inp.Fs, max_tokens=inp.T, norm_topk=norm)
+    y = L.forward(dev_bf16(inp.x), plan=plan)
+    torch.cuda.synchronize()
+    out = y.float().cpu().numpy()
+    L.close()
+    return out
+
+
+@pytest.mark.parametrize("D,N,kind,tile_m", [(2, 1, MOE_GEMM_GROUPED, 256), (2, 3, MOE_GEMM_GROUPED, 128),
+                                             (4, 2, MOE_GEMM_DENSE, 256), (4, 4, MOE_GEMM_GROUPED, 256),
+                                             (8, 1, MOE_GEMM_GROUPED, 128), (8, 2, MOE_GEMM_DENSE, 128)])
+def test_ep_equals_ep1_and_oracle(D, N, kind, tile_m):
+    inp = Inputs(E=16, k=4, H=256, F=256, S=1, Fs=128, T=997, seed=40 + D, grid=True)
+    plan = make_plan(N, kind, tile_m=tile_m)
+    y, bufs = _ep_forward(inp, 4, 0, D, plan)
+    y1 = _ep1_forward(inp, 4, 0, make_plan(1, kind, tile_m=tile_m))
+    assert np.array_equal(y, y1)                     # EP = D == EP = 1, bit-exact
+    ref = oracle.moe_layer(inp.x, inp.w_router, inp.w_gate, inp.w_up, inp.w_down, k=4, norm_topk=0,
+                           ws_gate_bits=inp.ws_gate, ws_up_bits=inp.ws_up, ws_down_bits=inp.ws_down, D=D, N=N)
+    lay = ref["layout"]
+    for r in range(D):
+        assert np.array_equal(bufs[r]["global_hist"], lay["hist"])          # count allgather
+        assert np.array_equal(bufs[r]["pos"].cpu().numpy(), lay["pos"][r])  # split on each rank
+        assert bufs[r]["plan_used"].num_chunks == N
+    assert_close(y, ref["y"], f"EP{D} N{N}")
+
+
+def test_ep_planner_auto_and_skew():
+    """No plan given: every rank derives the same plan from the allgathered
+    histogram (skewed routing, hot experts scattered over ranks)."""
+    from gen import router_skew_bias
+    inp = Inputs(E=32, k=4, H=256, F=256, T=1500, seed=9)
+    bias = router_skew_bias(32, 1.0)
+    y, bufs = _ep_forward(inp, 4, 1, 4, plan=None, skew_bias=bias)
+    plans = [bytes(b["plan_used"]) for b in bufs]
+    assert all(p == plans[0] for p in plans)
+    gh = bufs[0]["global_hist"]
+    assert gh.max() > 4 * gh.mean()                  # the skew is real
+    y1 = _ep1_forward(inp, 4, 1, plan=make_plan(1, MOE_GEMM_GROUPED, tile_m=int(bufs[0]["plan_used"].tile_m)),
+                      skew_bias=bias)
+    ref = oracle.moe_layer(inp.x, inp.w_router, inp.w_gate, inp.w_up, inp.w_down, k=4, norm_topk=1,
+                           router_bias=bias, D=4)
+    idx_ok = (ref["idx"] == np.concatenate([b["topk_idx"].cpu().numpy() for b in bufs])).all(axis=1)
+    assert idx_ok.mean() > 0.99
+    assert_close(y[idx_ok], ref["y"][idx_ok], "EP4 skew")
+    assert_close(y1[idx_ok], ref["y"][idx_ok], "EP1 skew")
