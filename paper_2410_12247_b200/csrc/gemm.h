@@ -37,6 +37,8 @@ struct GemmArgs {
   int cta_pair;            // 1: 256-row tiles on CTA pairs (cta_group::2); 0: 128-row tiles
   const int32_t* a_row_index;  // optional gather: logical A row r is physical row a_row_index[r] of A
                                // (TMA tile::gather4; EPI_SWIGLU only).  nullptr = contiguous A.
+  int32_t* tile_counter;       // device int32[2], zero-initialised, for dynamic tile tickets; launches
+                               // that may run concurrently need distinct counters (nullptr = shared)
 };
 
 // Launch on `stream`.  Returns a cudaError_t-compatible code (0 = success).

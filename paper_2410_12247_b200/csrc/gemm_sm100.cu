@@ -8,7 +8,7 @@
 //           TMA-loads its 128 rows of A and half (128 rows) of B, the leader
 //           CTA issues M=256 MMAs that read both CTAs' smem and write each
 //           CTA's own TMEM; 6 x 32 KB stages per CTA.  Per MAC this halves B's
-//           smem/L2 traffic (the paper's DenseGemm regime: large per-expert M).
+//           smem/L2 traffic.
 //
 // One kernel family serves every GEMM of the layer:
 //   GateUpGemm + SiluAct  EPI_SWIGLU: the 256 accumulator columns
@@ -16,13 +16,22 @@
 //        boxes; no weight repacking); epilogue h = bf16(silu(g) * u).
 //   DownGemm                  EPI_BF16:  o = bf16(acc).
 //   Router                    EPI_F32:   logits = fp32(acc) + beta.
-// Group row counts are read from device memory, so no host round trip sizes
-// the launch (persistent grid over a device-computed tile prefix).
+//
+// Tile scheduling: tiles are numbered group-major (expert), then in blocks of
+// RASTER m-tiles (n-major across a block) so that tiles in flight together
+// share A rows and B columns in L2.  By default tiles are handed out
+// dynamically: the leader CTA's producer takes the next ticket from a global
+// atomic counter and broadcasts it (smem queue + mbarriers; DSMEM to the peer
+// CTA), so the tiles processed at any moment stay contiguous in the order
+// even when units drift — which keeps their shared operands L2-resident.
+// Group row counts are read from device memory: no host round trip sizes the
+// launch.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdlib>
 #include <mutex>
 
@@ -38,6 +47,7 @@ constexpr int BK = 64;          // K per stage (one 128 B swizzle atom of bf16)
 constexpr int MAX_G = 256;
 constexpr int NUM_THREADS = 192;  // w0 TMA, w1 MMA + TMEM owner, w2..5 epilogue
 constexpr int TMEM_COLS = 512;    // 2 x 256-column fp32 accumulators
+constexpr int TQ = 4;             // tile-ticket queue depth
 
 template <int CG>
 struct Cfg {
@@ -46,18 +56,22 @@ struct Cfg {
   static constexpr int A_BYTES = BM * BK * 2;         // 16 KB
   static constexpr int B_BYTES = B_ROWS * BK * 2;     // 32 KB (CG=1) / 16 KB (CG=2)
   static constexpr int STAGES = (CG == 1) ? 4 : 6;
+  // consumers of a ticket that must release it before the slot is refilled:
+  // MMA (1) + own epilogue warps (4) [+ peer producer (1) + peer epilogue (4)]
+  static constexpr int TQ_CONSUMERS = (CG == 1) ? 5 : 10;
 };
 
 struct KParams {
   int K, N, G, m_single, b_group_rows, b_base;
   int raster_gm;  // tile order inside a group: blocks of raster_gm m-tiles, m fastest inside a block
-  int tma_hint;   // CTA-pair loads: 0 no L2 hint, 1 evict_normal, 2 evict_normal A / evict_last B
+  int dynamic;    // 1: dynamic tile tickets (tile_counter), 0: static round robin
   int64_t ldo;
   void* out;
   const float* bias;
   const int32_t* row_start;
   const int32_t* row_count;
   const int32_t* a_row_index;
+  int32_t* tile_counter;  // [2]: next ticket, CTAs finished (reset by the last CTA)
 };
 
 template <int CG>
@@ -66,6 +80,9 @@ struct __align__(8) SmemTail {
   uint64_t empty[Cfg<CG>::STAGES];
   uint64_t tfull[2];
   uint64_t tempty[2];
+  uint64_t qfull[TQ];
+  uint64_t qempty[TQ];
+  int32_t tq[TQ];
   uint32_t tmem_holder;
   int32_t tile_prefix[MAX_G + 1];
   int32_t gstart[MAX_G];
@@ -87,8 +104,7 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
 
 // Linear tile index -> (group, m-tile, n-tile).  Inside a group, tiles are
 // visited in blocks of `gm` m-tiles: n-tile major across the block, m fastest
-// inside it (gm = 1: plain n-fastest order), so the tiles in flight at once
-// share A rows and B columns in L2.
+// inside it (gm = 1: plain n-fastest order).
 template <int CG>
 __device__ __forceinline__ void decode_tile(const SmemTail<CG>& s, int G, int n_tiles, int gm_cfg, int t, int& g,
                                             int& mt, int& nt) {
@@ -106,6 +122,71 @@ __device__ __forceinline__ void decode_tile(const SmemTail<CG>& s, int G, int n_
   mt = blk * gm_cfg + within % gm;
   nt = within / gm;
 }
+
+// Tile-ticket stream shared by every role of a CTA (pair).  The fetcher (the
+// leader's producer lane) takes tickets and publishes them; every other role
+// consumes them in the same order.  Static mode needs no communication.
+template <int CG>
+struct Tickets {
+  SmemTail<CG>* st;
+  const KParams* p;
+  int total, unit, num_units;
+  uint32_t rank;
+  uint32_t slot = 0, phase = 0;
+  int static_next;
+  int prefetched = -2;  // fetcher: ticket taken one tile ahead (hides the atomic's latency)
+
+  __device__ Tickets(SmemTail<CG>* s, const KParams* pp, int tot, int u, int nu, uint32_t r)
+      : st(s), p(pp), total(tot), unit(u), num_units(nu), rank(r), static_next(u) {}
+
+  __device__ __forceinline__ void advance() {
+    if (++slot == TQ) { slot = 0; phase ^= 1; }
+  }
+  // Fetcher side (one thread): returns the next tile or -1.
+  __device__ __forceinline__ int fetch() {
+    if (!p->dynamic) {
+      int t = static_next;
+      static_next += num_units;
+      return t < total ? t : -1;
+    }
+    int t = (prefetched == -2) ? atomicAdd(p->tile_counter, 1) : prefetched;
+    if (t >= total) t = -1;
+    // next ticket in flight while this tile's loads are issued (-1 stays -1)
+    prefetched = (t < 0) ? -1 : atomicAdd(p->tile_counter, 1);
+    ptx::mbar_wait(ptx::smem_u32(&st->qempty[slot]), phase ^ 1);  // releases are relaxed: no acquire needed
+    st->tq[slot] = t;
+    ptx::mbar_arrive(ptx::smem_u32(&st->qfull[slot]));
+    if constexpr (CG == 2) {
+      ptx::st_cluster_u32(ptx::mapa(ptx::smem_u32(&st->tq[slot]), 1), (uint32_t)t);
+      ptx::mbar_arrive_cluster(ptx::mapa(ptx::smem_u32(&st->qfull[slot]), 1));
+    }
+    advance();
+    return t;
+  }
+  // Consumer side: `arrive` = this thread releases the ticket for its role.
+  __device__ __forceinline__ int consume(bool arrive) {
+    if (!p->dynamic) {
+      int t = static_next;
+      static_next += num_units;
+      return t < total ? t : -1;
+    }
+    if (CG == 2 && rank != 0)
+      ptx::mbar_wait_cluster(ptx::smem_u32(&st->qfull[slot]), phase);  // ticket written by the leader (DSMEM)
+    else
+      ptx::mbar_wait(ptx::smem_u32(&st->qfull[slot]), phase);
+    const int t = st->tq[slot];
+    if (arrive) release(slot);
+    advance();
+    return t;
+  }
+  // Release a consumed ticket slot on the fetcher's qempty barrier.
+  __device__ __forceinline__ void release(uint32_t s) {
+    if constexpr (CG == 2)
+      ptx::mbar_arrive_cluster_relaxed(ptx::mapa(ptx::smem_u32(&st->qempty[s]), 0));
+    else
+      ptx::mbar_arrive(ptx::smem_u32(&st->qempty[s]));
+  }
+};
 
 template <int EPI, int CG, bool GATHER>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
@@ -141,6 +222,10 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
     for (int i = 0; i < 2; ++i) {
       ptx::mbar_init(ptx::smem_u32(&st.tfull[i]), 1);
       ptx::mbar_init(ptx::smem_u32(&st.tempty[i]), 4 * CG);  // one arrive per epilogue warp (both CTAs)
+    }
+    for (int i = 0; i < TQ; ++i) {
+      ptx::mbar_init(ptx::smem_u32(&st.qfull[i]), 1);
+      ptx::mbar_init(ptx::smem_u32(&st.qempty[i]), C::TQ_CONSUMERS);
     }
     ptx::fence_barrier_init();
   }
@@ -182,15 +267,19 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
   ptx::tc_fence_after();
   const uint32_t tmem_base = st.tmem_holder;
   const int total = st.tile_prefix[G];
+  Tickets<CG> tk(&st, &p, total, unit, num_units, rank);
 
   if (warp == 0) {
     // ===================== TMA producer (each CTA loads its own halves) =====================
+    // The leader's lane 0 fetches tickets; the peer's lane 0 consumes them.
     // GATHER: the whole warp stages the tile's 128 physical A row indices in
     // smem; lane 0 then issues 32 tile::gather4 loads per stage.
     uint32_t stage = 0, phase = 0;
-    const uint64_t pol_a = ptx::policy_evict_normal();
-    const uint64_t pol_b = p.tma_hint == 2 ? ptx::policy_evict_last() : ptx::policy_evict_normal();
-    for (int t = unit; t < total; t += num_units) {
+    while (true) {
+      int t = 0;
+      if (lane == 0) t = (rank == 0) ? tk.fetch() : tk.consume(true);
+      t = __shfl_sync(0xffffffffu, t, 0);
+      if (t < 0) break;
       int g, mt, nt;
       decode_tile(st, G, n_tiles, p.raster_gm, t, g, mt, nt);
       const int a_row = st.gstart[g] + mt * C::TILE_M + (int)rank * BM;
@@ -213,20 +302,17 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
           const uint32_t fb = ptx::smem_u32(&st.full[stage]);
           const uint32_t a_dst = ptx::smem_u32(sA + stage * C::A_BYTES);
           const uint32_t b_dst = ptx::smem_u32(sB + stage * C::B_BYTES);
+          if (CG == 1 || rank == 0) ptx::mbar_arrive_expect_tx(fb, CG * (C::A_BYTES + C::B_BYTES));
           if constexpr (GATHER) {
-            if (CG == 1 || rank == 0) ptx::mbar_arrive_expect_tx(fb, CG * (C::A_BYTES + C::B_BYTES));
-            const int4* tk = reinterpret_cast<const int4*>(st.tok);
+            const int4* tkr = reinterpret_cast<const int4*>(st.tok);
 #pragma unroll 8
-            for (int i = 0; i < BM / 4; ++i) ptx::tma_gather4<CG>(a_dst + i * 512, &tmA, fb, kb * BK, tk[i]);
-            if constexpr (CG == 1) {
-              ptx::tma_load_2d(b_dst, &tmB0, fb, kb * BK, b_row0);
-              ptx::tma_load_2d(b_dst + C::B_BYTES / 2, &tmB1, fb, kb * BK, b_row0);
-            } else {
-              ptx::tma_load_2d_pair(b_dst, rank == 0 ? &tmB0 : &tmB1, fb, kb * BK, b_row0);
-            }
+            for (int i = 0; i < BM / 4; ++i) ptx::tma_gather4<CG>(a_dst + i * 512, &tmA, fb, kb * BK, tkr[i]);
           } else if constexpr (CG == 1) {
-            ptx::mbar_arrive_expect_tx(fb, C::A_BYTES + C::B_BYTES);
             ptx::tma_load_2d(a_dst, &tmA, fb, kb * BK, a_row);
+          } else {
+            ptx::tma_load_2d_pair(a_dst, &tmA, fb, kb * BK, a_row);
+          }
+          if constexpr (CG == 1) {
             if (EPI == EPI_SWIGLU) {
               ptx::tma_load_2d(b_dst, &tmB0, fb, kb * BK, b_row0);
               ptx::tma_load_2d(b_dst + C::B_BYTES / 2, &tmB1, fb, kb * BK, b_row0);
@@ -234,18 +320,10 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
               ptx::tma_load_2d(b_dst, &tmB0, fb, kb * BK, b_row0);
             }
           } else {
-            // the leader's full barrier counts both CTAs' bytes
-            if (rank == 0) ptx::mbar_arrive_expect_tx(fb, 2 * (C::A_BYTES + C::B_BYTES));
-            const void* tb = (EPI == EPI_SWIGLU && rank == 1) ? (const void*)&tmB1 : (const void*)&tmB0;
             // SwiGLU: CTA0 gate rows -> acc cols [0,128); CTA1 up rows -> [128,256)
+            const void* tb = (EPI == EPI_SWIGLU && rank == 1) ? (const void*)&tmB1 : (const void*)&tmB0;
             const int brow = (EPI == EPI_SWIGLU) ? b_row0 : b_row0 + (int)rank * C::B_ROWS;
-            if (p.tma_hint == 0) {
-              ptx::tma_load_2d_pair(a_dst, &tmA, fb, kb * BK, a_row);
-              ptx::tma_load_2d_pair(b_dst, tb, fb, kb * BK, brow);
-            } else {
-              ptx::tma_load_2d_pair_hint(a_dst, &tmA, fb, kb * BK, a_row, pol_a);
-              ptx::tma_load_2d_pair_hint(b_dst, tb, fb, kb * BK, brow, pol_b);
-            }
+            ptx::tma_load_2d_pair(b_dst, tb, fb, kb * BK, brow);
           }
           if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
         }
@@ -256,7 +334,9 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
     if (lane == 0 && rank == 0) {
       constexpr uint32_t idesc = ptx::idesc_bf16_f32(C::TILE_M, BN);
       uint32_t stage = 0, phase = 0, iter = 0;
-      for (int t = unit; t < total; t += num_units, ++iter) {
+      while (true) {
+        const int t = tk.consume(true);
+        if (t < 0) break;
         const uint32_t acc = iter & 1, accph = (iter >> 1) & 1;
         ptx::mbar_wait(ptx::smem_u32(&st.tempty[acc]), accph ^ 1);
         ptx::tc_fence_after();
@@ -280,6 +360,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
         }
         if constexpr (CG == 1) ptx::mma_commit(ptx::smem_u32(&st.tfull[acc]));
         else ptx::mma_commit_pair(ptx::smem_u32(&st.tfull[acc]), 0x3);
+        ++iter;
       }
     }
   } else {
@@ -288,7 +369,11 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
     const uint32_t tempty_leader0 = (CG == 2) ? ptx::mapa(ptx::smem_u32(&st.tempty[0]), 0) : 0;
     const uint32_t tempty_leader1 = (CG == 2) ? ptx::mapa(ptx::smem_u32(&st.tempty[1]), 0) : 0;
     uint32_t iter = 0;
-    for (int t = unit; t < total; t += num_units, ++iter) {
+    while (true) {
+      const int t = tk.consume(false);
+      __syncwarp();
+      if (lane == 0 && p.dynamic) tk.release((tk.slot + TQ - 1) % TQ);  // once per warp
+      if (t < 0) break;
       int g, mt, nt;
       decode_tile(st, G, n_tiles, p.raster_gm, t, g, mt, nt);
       const uint32_t acc = iter & 1, accph = (iter >> 1) & 1;
@@ -363,8 +448,11 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
       __syncwarp();
       if (lane == 0) {
         if constexpr (CG == 1) ptx::mbar_arrive(ptx::smem_u32(&st.tempty[acc]));
-        else ptx::mbar_arrive_cluster(acc ? tempty_leader1 : tempty_leader0);
+        // relaxed: the TMEM reads are ordered by tcgen05.wait::ld + fence::before_thread_sync;
+        // the tile's global stores need not complete before the accumulator is reused
+        else ptx::mbar_arrive_cluster_relaxed(acc ? tempty_leader1 : tempty_leader0);
       }
+      ++iter;
     }
   }
 
@@ -373,6 +461,15 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
   if constexpr (CG == 2) ptx::cluster_sync();  // no CTA leaves while its peer may still signal it
   ptx::tc_fence_after();
   if (warp == 1) ptx::tmem_dealloc<TMEM_COLS, CG>(tmem_base);
+  if (p.dynamic && threadIdx.x == 0) {
+    // the last CTA to finish resets the ticket counter for the next launch
+    __threadfence();
+    if (atomicAdd(p.tile_counter + 1, 1) == (int)gridDim.x - 1) {
+      p.tile_counter[0] = 0;
+      p.tile_counter[1] = 0;
+      __threadfence();
+    }
+  }
 }
 
 // ------------------------------------------------------------------ host side
@@ -396,14 +493,25 @@ int env_int(const char* name, int dflt) {
 }
 
 // Tile rasterisation block (m-tiles); 4 measured best on DSv2 and Mixtral
-// shapes (tools/gemm_bench.py, profiles/r01_notes.md); EPSMOE_RASTER_GM overrides.
+// shapes (tools/gemm_bench.py); EPSMOE_RASTER_GM overrides.
 int raster_gm() {
-  static int v = [] {
-    const char* e = std::getenv("EPSMOE_RASTER_GM");
-    int r = e ? std::atoi(e) : 4;
-    return r < 1 ? 1 : r;
-  }();
+  static int v = std::max(1, env_int("EPSMOE_RASTER_GM", 4));
   return v;
+}
+int dynamic_sched() {
+  static int v = env_int("EPSMOE_DYN_SCHED", 1);
+  return v;
+}
+
+// Fallback ticket counter for launches without a caller-owned one (the
+// moe_gemm_grouped test hook; stream-serialised use only).
+int32_t* ticket_counter(int) {
+  static int32_t* base = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    if (cudaMalloc(&base, 2 * sizeof(int32_t)) == cudaSuccess) cudaMemset(base, 0, 2 * sizeof(int32_t));
+  });
+  return base;
 }
 
 // 2D bf16 K-major tensor [rows, K] with a {64, box_rows} box and 128 B swizzle.
@@ -427,10 +535,6 @@ int launch_epi(const GemmArgs& a, cudaStream_t stream) {
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes<CG>());
     if (e != cudaSuccess) return (int)e;
-    if (CG == 2) {
-      e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 0);
-      (void)e;
-    }
     attr_set = true;
   }
   CUtensorMap tA, tB0, tB1;
@@ -450,13 +554,15 @@ int launch_epi(const GemmArgs& a, cudaStream_t stream) {
   p.b_group_rows = a.b_group_rows;
   p.b_base = a.b_base;
   p.raster_gm = raster_gm();
-  p.tma_hint = env_int("EPSMOE_TMA_HINT", 0);
   p.ldo = a.ldo;
   p.out = a.out;
   p.bias = a.bias;
   p.row_start = a.row_start;
   p.row_count = a.row_count;
   p.a_row_index = a.a_row_index;
+  // Launches that may run concurrently must use different counters (caller's).
+  p.tile_counter = a.tile_counter ? a.tile_counter : ticket_counter(0);
+  p.dynamic = (dynamic_sched() && p.tile_counter) ? 1 : 0;
   int grid = a.num_ctas;
   if (CG == 2) grid &= ~1;
   if (grid < CG) grid = CG;

@@ -17,11 +17,28 @@ namespace {
 
 constexpr int WARPS = 8;
 constexpr int MAX_EPL = 8;  // E <= 256: logits per lane
+constexpr int MAX_K = 8;    // top_k <= 8
 
-struct Cand {
-  float v;
-  int e;
-};
+// Streaming 16-byte accesses for the HBM-bound kernels: L1 no-allocate, L2
+// evict-first, so the activations they stream (GBs per layer) do not evict
+// the concurrently running GEMMs' operand tiles from L2.
+__device__ __forceinline__ uint64_t evict_first_policy() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint4 ld_stream(const uint4* ptr, uint64_t pol) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(ptr), "l"(pol));
+  return r;
+}
+__device__ __forceinline__ void st_stream(uint4* ptr, const uint4& v, uint64_t pol) {
+  asm volatile("st.global.L1::no_allocate.L2::cache_hint.v4.u32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(ptr), "r"(v.x),
+               "r"(v.y), "r"(v.z), "r"(v.w), "l"(pol)
+               : "memory");
+}
 __device__ __forceinline__ bool better(float av, int ae, float bv, int be) {
   return av > bv || (av == bv && ae < be);
 }
@@ -193,6 +210,7 @@ permute_kernel(const __nv_bfloat16* __restrict__ x, int T, int H, int E, int k,
   __syncwarp();
   const int nvec = H >> 3;  // uint4 = 8 bf16
   const int t_end = min(T, (r + 1) * RANGE_T);
+  const uint64_t pol = evict_first_policy();
   for (int t = r * RANGE_T; t < t_end; ++t) {
     int dest = 0;
     if (lane < k) {
@@ -217,7 +235,7 @@ permute_kernel(const __nv_bfloat16* __restrict__ x, int T, int H, int E, int k,
 #pragma unroll
       for (int i = 0; i < MAXV; ++i) {
         int c = base + lane + 32 * i;
-        if (c < nvec) buf[i] = __ldg(src + c);
+        if (c < nvec) buf[i] = ld_stream(src + c, pol);
       }
       for (int j = 0; j < k; ++j) {
         int d = __shfl_sync(0xffffffffu, dest, j);
@@ -225,7 +243,7 @@ permute_kernel(const __nv_bfloat16* __restrict__ x, int T, int H, int E, int k,
 #pragma unroll
         for (int i = 0; i < MAXV; ++i) {
           int c = base + lane + 32 * i;
-          if (c < nvec) dst[c] = buf[i];
+          if (c < nvec) st_stream(dst + c, buf[i], pol);
         }
       }
     }
@@ -249,10 +267,24 @@ combine_kernel(const __nv_bfloat16* __restrict__ o, const __nv_bfloat16* __restr
     pw = topk_w[(int64_t)t * k + lane];
   }
   const int nvec = H >> 3;
+  const uint64_t pol = evict_first_policy();
+  const uint4* orow[MAX_K];
+  float wj[MAX_K];
+#pragma unroll
+  for (int j = 0; j < MAX_K; ++j) {
+    const int row = __shfl_sync(0xffffffffu, prow, j < k ? j : 0);
+    orow[j] = reinterpret_cast<const uint4*>(o + (int64_t)row * H);
+    wj[j] = __shfl_sync(0xffffffffu, pw, j < k ? j : 0);
+  }
   for (int c = lane; c < nvec; c += 32) {
+    // all k rows in flight first, then the fmaf chain in slot order (R4)
+    uint4 ov[MAX_K];
+#pragma unroll
+    for (int j = 0; j < MAX_K; ++j)
+      if (j < k) ov[j] = ld_stream(orow[j] + c, pol);
     float acc[8];
     if (s) {
-      uint4 sv = __ldg(reinterpret_cast<const uint4*>(s + (int64_t)t * H) + c);
+      uint4 sv = ld_stream(reinterpret_cast<const uint4*>(s + (int64_t)t * H) + c, pol);
       const __nv_bfloat16* sb = reinterpret_cast<const __nv_bfloat16*>(&sv);
 #pragma unroll
       for (int i = 0; i < 8; ++i) acc[i] = __bfloat162float(sb[i]);
@@ -260,20 +292,19 @@ combine_kernel(const __nv_bfloat16* __restrict__ o, const __nv_bfloat16* __restr
 #pragma unroll
       for (int i = 0; i < 8; ++i) acc[i] = 0.f;
     }
-    uint4 ov[8];
-    for (int j = 0; j < k; ++j) {
-      int row = __shfl_sync(0xffffffffu, prow, j);
-      ov[j & 7] = __ldg(reinterpret_cast<const uint4*>(o + (int64_t)row * H) + c);
-      float w = __shfl_sync(0xffffffffu, pw, j);
-      const __nv_bfloat16* ob = reinterpret_cast<const __nv_bfloat16*>(&ov[j & 7]);
 #pragma unroll
-      for (int i = 0; i < 8; ++i) acc[i] = __fmaf_rn(w, __bfloat162float(ob[i]), acc[i]);
+    for (int j = 0; j < MAX_K; ++j) {
+      if (j < k) {
+        const __nv_bfloat16* ob = reinterpret_cast<const __nv_bfloat16*>(&ov[j]);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc[i] = __fmaf_rn(wj[j], __bfloat162float(ob[i]), acc[i]);
+      }
     }
     uint4 outv;
     __nv_bfloat162* ob2 = reinterpret_cast<__nv_bfloat162*>(&outv);
 #pragma unroll
     for (int i = 0; i < 4; ++i) ob2[i] = __floats2bfloat162_rn(acc[2 * i], acc[2 * i + 1]);
-    reinterpret_cast<uint4*>(y + (int64_t)t * H)[c] = outv;
+    st_stream(reinterpret_cast<uint4*>(y + (int64_t)t * H) + c, outv, pol);
   }
 }
 
