@@ -88,6 +88,7 @@ struct __align__(8) SmemTail {
   int32_t gstart[MAX_G];
   int32_t gcount[MAX_G];
   alignas(16) int32_t tok[BM];  // GATHER: physical A rows of the current tile (read as int4)
+  alignas(16) uint8_t stage_out[4][32 * 64];   // per epilogue warp: 32 rows x 32 bf16, XOR-swizzled
 };
 
 template <int CG>
@@ -100,6 +101,28 @@ __device__ __forceinline__ float silu_f32(float g) { return g / (1.0f + expf(-g)
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&v);
+}
+
+// Coalesced epilogue store of one warp's 32 rows x 32 bf16 columns: each lane
+// holds its row's 64 B (pk), the warp transposes through a 16-B-chunk XOR-
+// swizzled smem tile (conflict-free both ways), then 4 lanes write each row's
+// 64 B as two full 32-B sectors (8 rows per instruction) instead of 32
+// scattered 16-B pieces.  Rows >= vr (past the group's end) are not written.
+__device__ __forceinline__ void store_chunk(const uint32_t (&pk)[16], uint8_t* stg, __nv_bfloat16* out_row0,
+                                            int64_t ldo, int vr, int lane) {
+  uint4* srow = reinterpret_cast<uint4*>(stg + lane * 64);
+  const int sw = (lane >> 1) & 3;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) srow[j ^ sw] = make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
+  __syncwarp();
+  const int j = lane & 3;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int r = i * 8 + (lane >> 2);
+    const uint4 v = reinterpret_cast<const uint4*>(stg + r * 64)[j ^ ((r >> 1) & 3)];
+    if (r < vr) reinterpret_cast<uint4*>(out_row0 + (int64_t)r * ldo)[j] = v;
+  }
+  __syncwarp();
 }
 
 // Linear tile index -> (group, m-tile, n-tile).  Inside a group, tiles are
@@ -383,45 +406,36 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
       const bool valid = local_row < st.gcount[g];
       const int64_t grow = (int64_t)st.gstart[g] + local_row;
       const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
+      // rows of this warp's 32-row slice that belong to the group
+      const int vr = max(0, min(32, st.gcount[g] - (local_row - lane)));
+      uint8_t* stg = st.stage_out[q];
       if (EPI == EPI_SWIGLU) {
-        __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(p.out) + grow * p.ldo + nt * 128;
+        __nv_bfloat16* out0 = reinterpret_cast<__nv_bfloat16*>(p.out) + (grow - lane) * p.ldo + nt * 128;
 #pragma unroll 1
-        for (int c = 0; c < 4; ++c) {
-          uint32_t gr[32], ur[32];
+        for (int c = 0; c < 4; ++c) {  // 4 x 32 output columns
+          uint32_t gr[32], ur[32], pk[16];
           ptx::tmem_ld32(taddr + c * 32, gr);
           ptx::tmem_ld32(taddr + 128 + c * 32, ur);
           ptx::tmem_wait_ld();
-          uint32_t pk[16];
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
             float g0 = __uint_as_float(gr[2 * i]), g1 = __uint_as_float(gr[2 * i + 1]);
             float u0 = __uint_as_float(ur[2 * i]), u1 = __uint_as_float(ur[2 * i + 1]);
             pk[i] = pack_bf16(silu_f32(g0) * u0, silu_f32(g1) * u1);
           }
-          if (valid) {
-            uint4* dst = reinterpret_cast<uint4*>(out + c * 32);
-#pragma unroll
-            for (int v = 0; v < 4; ++v)
-              dst[v] = make_uint4(pk[4 * v], pk[4 * v + 1], pk[4 * v + 2], pk[4 * v + 3]);
-          }
+          store_chunk(pk, stg, out0 + c * 32, p.ldo, vr, lane);
         }
       } else if (EPI == EPI_BF16) {
-        __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(p.out) + grow * p.ldo;
+        __nv_bfloat16* out0 = reinterpret_cast<__nv_bfloat16*>(p.out) + (grow - lane) * p.ldo + nt * BN;
 #pragma unroll 1
         for (int c = 0; c < BN / 32; ++c) {
-          uint32_t r[32];
+          if (nt * BN + c * 32 >= p.N) break;  // N is a multiple of 32 (warp-uniform)
+          uint32_t r[32], pk[16];
           ptx::tmem_ld32(taddr + c * 32, r);
           ptx::tmem_wait_ld();
-          const int col = nt * BN + c * 32;
-          if (valid && col < p.N) {
-            uint4* dst = reinterpret_cast<uint4*>(out + col);
 #pragma unroll
-            for (int v = 0; v < 4; ++v)
-              dst[v] = make_uint4(pack_bf16(__uint_as_float(r[8 * v + 0]), __uint_as_float(r[8 * v + 1])),
-                                  pack_bf16(__uint_as_float(r[8 * v + 2]), __uint_as_float(r[8 * v + 3])),
-                                  pack_bf16(__uint_as_float(r[8 * v + 4]), __uint_as_float(r[8 * v + 5])),
-                                  pack_bf16(__uint_as_float(r[8 * v + 6]), __uint_as_float(r[8 * v + 7])));
-          }
+          for (int i = 0; i < 16; ++i) pk[i] = pack_bf16(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1]));
+          store_chunk(pk, stg, out0 + c * 32, p.ldo, vr, lane);
         }
       } else {
         float* out = reinterpret_cast<float*>(p.out) + grow * p.ldo;

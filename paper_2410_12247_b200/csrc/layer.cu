@@ -650,13 +650,14 @@ moe_status_t moe_layer_forward(moe_layer_t* L, const void* x, int64_t T, void* y
 
   KERNEL_TRY(launch_gate_topk(L->logits, (int)T, E, k, c.norm_topk, c.routed_scale, override_routing ? 1 : 0,
                               topk_idx, topk_w, L->range_hist, st));
-  KERNEL_TRY(launch_range_scan(L->range_hist, (int)T, E, L->range_off, L->hist, st));
+  KERNEL_TRY(launch_range_scan(L->range_hist, (int)T, E, L->range_off, L->hist, L->seg_start, st));
+  ++L->last_launches;  // range scan + expert scan
   // ---- split (K3): x -> send rows, expert-major (R6).  At ep == 1 the send
   // buffer is only the GateUp GEMM's A operand, so by default the split is
   // index-only and the GEMM gathers x's rows with TMA tile::gather4.
   const bool gather = (D == 1) && L->gather_a && T > 0;
-  KERNEL_TRY(launch_permute(x, (int)T, H, E, k, topk_idx, L->range_off, L->hist, gather ? nullptr : L->send,
-                            L->pos, L->seg_start, gather ? L->row_token : nullptr, st));
+  KERNEL_TRY(launch_permute(x, (int)T, H, E, k, topk_idx, L->range_off, L->seg_start, gather ? nullptr : L->send,
+                            L->pos, gather ? L->row_token : nullptr, st));
   prof_mark(L, MOE_STAGE_ROUTE, p1, prof_rec(L, st));
   if (has_shared && !side) {
     int e = shared_experts(st);

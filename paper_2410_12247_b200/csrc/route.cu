@@ -15,7 +15,8 @@
 namespace epsmoe {
 namespace {
 
-constexpr int WARPS = 8;
+constexpr int WARPS = 8;    // combine
+constexpr int WARPS_R = 4;  // gate / permute: small blocks (4 KB smem) that co-reside with GEMM CTAs
 constexpr int MAX_EPL = 8;  // E <= 256: logits per lane
 constexpr int MAX_K = 8;    // top_k <= 8
 
@@ -47,13 +48,13 @@ __device__ __forceinline__ bool better(float av, int ae, float bv, int be) {
 // in order.  idx = k largest logits (ties -> lower expert id, R2); p = softmax
 // over all E in fp32; w_j = p_{idx_j} (/ sum_j p_{idx_j} if norm_topk) * scale.
 // Also writes the range's expert histogram range_hist[e * R + r].
-__global__ void __launch_bounds__(WARPS * 32)
+__global__ void __launch_bounds__(WARPS_R * 32)
 gate_topk_kernel(const float* __restrict__ logits, int T, int E, int k, int norm_topk, float scale,
                  int override_routing, int32_t* __restrict__ topk_idx, float* __restrict__ topk_w,
                  int32_t* __restrict__ range_hist, int R) {
-  __shared__ int32_t hist_s[WARPS][256];
+  __shared__ int32_t hist_s[WARPS_R][256];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int r = blockIdx.x * WARPS + warp;
+  const int r = blockIdx.x * WARPS_R + warp;
   for (int e = lane; e < E; e += 32) hist_s[warp][e] = 0;
   __syncwarp();
   if (r < R) {
@@ -184,29 +185,28 @@ __device__ __forceinline__ int block_exclusive_scan_256(int v, int* sh) {
   return base + incl - v;
 }
 
-// K3 permute (`split`).  seg_start[e] = sum_{e' < e} hist[e'] (send
-// layout expert-major, R6).  One warp per token range; each token's row is
+// seg_start[e] = sum_{e' < e} hist[e'] (send layout expert-major, R6), [E] = total.
+__global__ void __launch_bounds__(256) seg_scan_kernel(const int32_t* __restrict__ hist, int E,
+                                                       int32_t* __restrict__ seg_start) {
+  __shared__ int32_t scan_tmp[8];
+  int hv = (threadIdx.x < E) ? hist[threadIdx.x] : 0;
+  int ex = block_exclusive_scan_256(hv, scan_tmp);
+  if (threadIdx.x < E) seg_start[threadIdx.x] = ex;
+  if (threadIdx.x == 255) seg_start[E] = ex + hv;
+}
+
+// K3 permute (`split`).  One warp per token range; each token's row is
 // read once and written to its k destination rows with 16-byte stores.
-__global__ void __launch_bounds__(WARPS * 32, 2)
+__global__ void __launch_bounds__(WARPS_R * 32, 4)
 permute_kernel(const __nv_bfloat16* __restrict__ x, int T, int H, int E, int k,
                const int32_t* __restrict__ topk_idx, const int32_t* __restrict__ range_off,
-               const int32_t* __restrict__ hist, int R, __nv_bfloat16* __restrict__ send,
-               int32_t* __restrict__ pos, int32_t* __restrict__ seg_start_out, int32_t* __restrict__ row_token) {
-  __shared__ int32_t seg_s[256];
-  __shared__ int32_t scan_tmp[8];
-  __shared__ int32_t off_s[WARPS][256];
+               const int32_t* __restrict__ seg_start, int R, __nv_bfloat16* __restrict__ send,
+               int32_t* __restrict__ pos, int32_t* __restrict__ row_token) {
+  __shared__ int32_t off_s[WARPS_R][256];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  {
-    int hv = (threadIdx.x < E) ? hist[threadIdx.x] : 0;
-    int ex = block_exclusive_scan_256(hv, scan_tmp);
-    if (threadIdx.x < E) seg_s[threadIdx.x] = ex;
-    if (blockIdx.x == 0 && threadIdx.x < E) seg_start_out[threadIdx.x] = ex;
-    if (blockIdx.x == 0 && threadIdx.x == WARPS * 32 - 1) seg_start_out[E] = ex + hv;  // total
-  }
-  __syncthreads();
-  const int r = blockIdx.x * WARPS + warp;
+  const int r = blockIdx.x * WARPS_R + warp;
   if (r >= R) return;
-  for (int e = lane; e < E; e += 32) off_s[warp][e] = seg_s[e] + range_off[(int64_t)e * R + r];
+  for (int e = lane; e < E; e += 32) off_s[warp][e] = seg_start[e] + range_off[(int64_t)e * R + r];
   __syncwarp();
   const int nvec = H >> 3;  // uint4 = 8 bf16
   const int t_end = min(T, (r + 1) * RANGE_T);
@@ -326,26 +326,31 @@ int launch_gate_topk(const float* logits, int T, int E, int k, int norm_topk, fl
                      int32_t* topk_idx, float* topk_w, int32_t* range_hist, cudaStream_t st) {
   int R = num_ranges(T);
   if (R == 0) return 0;
-  gate_topk_kernel<<<(R + WARPS - 1) / WARPS, WARPS * 32, 0, st>>>(logits, T, E, k, norm_topk, scale,
-                                                                   override_routing, topk_idx, topk_w,
-                                                                   range_hist, R);
+  gate_topk_kernel<<<(R + WARPS_R - 1) / WARPS_R, WARPS_R * 32, 0, st>>>(logits, T, E, k, norm_topk, scale,
+                                                                         override_routing, topk_idx, topk_w,
+                                                                         range_hist, R);
   return (int)cudaGetLastError();
 }
 
-int launch_range_scan(const int32_t* range_hist, int T, int E, int32_t* range_off, int32_t* hist, cudaStream_t st) {
+int launch_range_scan(const int32_t* range_hist, int T, int E, int32_t* range_off, int32_t* hist,
+                      int32_t* seg_start, cudaStream_t st) {
   int R = num_ranges(T);
-  if (R == 0) return (int)cudaMemsetAsync(hist, 0, sizeof(int32_t) * E, st);
-  range_scan_kernel<<<E, 1024, 0, st>>>(range_hist, R, range_off, hist);
+  if (R == 0) {
+    cudaError_t e = cudaMemsetAsync(hist, 0, sizeof(int32_t) * E, st);
+    if (e != cudaSuccess) return (int)e;
+  } else {
+    range_scan_kernel<<<E, 1024, 0, st>>>(range_hist, R, range_off, hist);
+  }
+  seg_scan_kernel<<<1, 256, 0, st>>>(hist, E, seg_start);
   return (int)cudaGetLastError();
 }
 
 int launch_permute(const void* x, int T, int H, int E, int k, const int32_t* topk_idx, const int32_t* range_off,
-                   const int32_t* hist, void* send, int32_t* pos, int32_t* seg_start, int32_t* row_token,
-                   cudaStream_t st) {
+                   const int32_t* seg_start, void* send, int32_t* pos, int32_t* row_token, cudaStream_t st) {
   int R = num_ranges(T);
-  int blocks = R == 0 ? 1 : (R + WARPS - 1) / WARPS;
-  permute_kernel<<<blocks, WARPS * 32, 0, st>>>((const __nv_bfloat16*)x, T, H, E, k, topk_idx, range_off, hist,
-                                                R, (__nv_bfloat16*)send, pos, seg_start, row_token);
+  if (R == 0) return 0;
+  permute_kernel<<<(R + WARPS_R - 1) / WARPS_R, WARPS_R * 32, 0, st>>>(
+      (const __nv_bfloat16*)x, T, H, E, k, topk_idx, range_off, seg_start, R, (__nv_bfloat16*)send, pos, row_token);
   return (int)cudaGetLastError();
 }
 

@@ -10,11 +10,12 @@ constexpr int RANGE_T = 32;  // tokens per deterministic counting range (one war
 int num_ranges(int64_t T);
 int launch_gate_topk(const float* logits, int T, int E, int k, int norm_topk, float scale, int override_routing,
                      int32_t* topk_idx, float* topk_w, int32_t* range_hist, cudaStream_t st);
+// per-range offsets, per-expert totals (hist) and expert segment starts (seg_start[E+1])
 int launch_range_scan(const int32_t* range_hist, int T, int E, int32_t* range_off, int32_t* hist,
-                      cudaStream_t st);
+                      int32_t* seg_start, cudaStream_t st);
 int launch_permute(const void* x, int T, int H, int E, int k, const int32_t* topk_idx, const int32_t* range_off,
-                   const int32_t* hist, void* send, int32_t* pos, int32_t* seg_start, int32_t* row_token,
-                   cudaStream_t st);  // send == nullptr: index-only (pos, seg_start, row_token)
+                   const int32_t* seg_start, void* send, int32_t* pos, int32_t* row_token,
+                   cudaStream_t st);  // send == nullptr: index-only (pos, row_token)
 int launch_combine(const void* o, const void* s, int T, int H, int k, const int32_t* pos, const float* topk_w,
                    void* y, cudaStream_t st);
 int launch_pad_rows(const void* src, int rows, int H, void* dst, int rows_pad, cudaStream_t st);
