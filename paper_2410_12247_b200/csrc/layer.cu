@@ -45,6 +45,8 @@ struct moe_layer {
   int32_t* tables_host = nullptr;   // pinned [2*E_loc]
   cudaStream_t s_disp = nullptr, s_comb = nullptr;
   cudaStream_t s_side = nullptr;  // shared experts, concurrent with routing / dispatch
+  cudaStream_t s_h2d = nullptr, s_d2h = nullptr;  // forward_host copy streams
+  cudaEvent_t ev_host_start = nullptr, ev_in[4] = {}, ev_out[4] = {};
   cudaEvent_t ev_router = nullptr, ev_shared = nullptr;
   bool overlap_shared = true;     // shared experts on s_side, concurrent with routing (EPSMOE_OVERLAP_SHARED=0: in order)
   bool gather_a = false;          // EPSMOE_GATHER=1: GateUp gathers x rows (tile::gather4) at ep == 1
@@ -373,6 +375,18 @@ static moe_status_t create_impl(const moe_config_t* cfg, const moe_weights_t* w,
   default_cost_model(L->cfg, &L->cost);
   if (const char* ov = std::getenv("EPSMOE_OVERLAP_SHARED")) L->overlap_shared = std::atoi(ov) != 0;
   if (const char* gv = std::getenv("EPSMOE_GATHER")) L->gather_a = std::atoi(gv) != 0;
+  if (cudaStreamCreateWithFlags(&L->s_h2d, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&L->s_d2h, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&L->ev_host_start, cudaEventDisableTiming) != cudaSuccess) {
+    set_error("copy stream creation failed");
+    return fail(MOE_ERR_CUDA);
+  }
+  for (int i = 0; i < 4; ++i)
+    if (cudaEventCreateWithFlags(&L->ev_in[i], cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&L->ev_out[i], cudaEventDisableTiming) != cudaSuccess) {
+      set_error("event creation failed");
+      return fail(MOE_ERR_CUDA);
+    }
   if (cudaStreamCreateWithFlags(&L->s_side, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreateWithFlags(&L->ev_router, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&L->ev_shared, cudaEventDisableTiming) != cudaSuccess) {
@@ -453,6 +467,13 @@ moe_status_t moe_layer_destroy(moe_layer_t* L) {
   delete L->tr;
   if (L->s_disp) cudaStreamDestroy(L->s_disp);
   if (L->s_side) cudaStreamDestroy(L->s_side);
+  if (L->s_h2d) cudaStreamDestroy(L->s_h2d);
+  if (L->s_d2h) cudaStreamDestroy(L->s_d2h);
+  if (L->ev_host_start) cudaEventDestroy(L->ev_host_start);
+  for (int i = 0; i < 4; ++i) {
+    if (L->ev_in[i]) cudaEventDestroy(L->ev_in[i]);
+    if (L->ev_out[i]) cudaEventDestroy(L->ev_out[i]);
+  }
   for (cudaEvent_t e : {L->ev_router, L->ev_shared})
     if (e) cudaEventDestroy(e);
   if (L->s_comb) cudaStreamDestroy(L->s_comb);
@@ -820,11 +841,30 @@ moe_status_t moe_layer_forward_host(moe_layer_t* L, const void* x_host, int64_t 
                                     const moe_plan_t* plan, void* stream_v) {
   if (!L || T < 0 || T > L->cfg.max_tokens) { set_error("bad argument"); return MOE_ERR_INVALID; }
   cudaStream_t st = (cudaStream_t)stream_v;
-  size_t bytes = (size_t)T * L->cfg.hidden * 2;
-  CUDA_TRY(cudaMemcpyAsync(L->x_dev, x_host, bytes, cudaMemcpyHostToDevice, st));
-  moe_status_t s = moe_layer_forward(L, L->x_dev, T, L->y_dev, plan, stream_v, nullptr);
-  if (s) return s;
-  CUDA_TRY(cudaMemcpyAsync(y_host, L->y_dev, bytes, cudaMemcpyDeviceToHost, st));
+  const int64_t row = (int64_t)L->cfg.hidden * 2;
+  // y_t depends only on x_t, so the batch is processed in token
+  // slices: the H2D copy of slice s+1 and the D2H copy of slice s-1 run on
+  // their own streams while the layer computes slice s.  The slice count is a
+  // function of max_tokens (identical on every rank: each slice's forward is
+  // a collective when ep > 1), chosen so slices keep >= 16K tokens.
+  const int S = (int)std::max<int64_t>(1, std::min<int64_t>(4, L->cfg.max_tokens / 16384));
+  const int64_t per = (T + S - 1) / S;
+  CUDA_TRY(cudaEventRecord(L->ev_host_start, st));  // x_dev / y_dev free once prior work on st is done
+  CUDA_TRY(cudaStreamWaitEvent(L->s_h2d, L->ev_host_start, 0));
+  for (int s = 0; s < S; ++s) {
+    const int64_t t0 = std::min(T, s * per), n = std::min(T, t0 + per) - t0;
+    char* xd = (char*)L->x_dev + t0 * row;
+    char* yd = (char*)L->y_dev + t0 * row;
+    if (n) CUDA_TRY(cudaMemcpyAsync(xd, (const char*)x_host + t0 * row, n * row, cudaMemcpyHostToDevice, L->s_h2d));
+    CUDA_TRY(cudaEventRecord(L->ev_in[s], L->s_h2d));
+    CUDA_TRY(cudaStreamWaitEvent(st, L->ev_in[s], 0));
+    moe_status_t rs = moe_layer_forward(L, xd, n, yd, plan, stream_v, nullptr);
+    if (rs) return rs;
+    CUDA_TRY(cudaEventRecord(L->ev_out[s], st));
+    CUDA_TRY(cudaStreamWaitEvent(L->s_d2h, L->ev_out[s], 0));
+    if (n) CUDA_TRY(cudaMemcpyAsync((char*)y_host + t0 * row, yd, n * row, cudaMemcpyDeviceToHost, L->s_d2h));
+  }
+  CUDA_TRY(cudaStreamSynchronize(L->s_d2h));
   CUDA_TRY(cudaStreamSynchronize(st));
   return MOE_OK;
 }

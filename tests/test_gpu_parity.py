@@ -217,6 +217,20 @@ def test_empty_and_single_token():
     assert y0.shape[0] == 0
 
 
+def test_forward_host_sliced_pipeline_matches_device():
+    """forward_host splits big batches into token slices (copies overlap the
+    layer); rows are independent, so the result equals the one-shot forward."""
+    inp = Inputs(E=8, k=2, H=64, F=128, S=1, Fs=128, T=50001, seed=6)
+    L = layer_from_inputs(inp, 2, 1, max_tokens=65536)
+    x = dev_bf16(inp.x)
+    y = L.forward(x)
+    xh = x.cpu().pin_memory()
+    yh = torch.zeros_like(xh).pin_memory()
+    L.forward_host(xh, yh)
+    torch.cuda.synchronize()
+    assert torch.equal(yh, y.cpu())
+
+
 def test_forward_host_matches_device():
     kw, k, norm = CASES["mid_shared"]
     inp = Inputs(seed=8, **kw)
