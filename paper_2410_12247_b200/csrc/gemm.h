@@ -39,6 +39,8 @@ struct GemmArgs {
                                // (TMA tile::gather4; EPI_SWIGLU only).  nullptr = contiguous A.
   int32_t* tile_counter;       // device int32[2], zero-initialised, for dynamic tile tickets; launches
                                // that may run concurrently need distinct counters (nullptr = shared)
+  int row_mode;                // 0: all rows of each group; 1: only the first floor(n/256)*256 rows
+                               // (bulk); 2: only the rows after them (remainder, < 256)
 };
 
 // Launch on `stream`.  Returns a cudaError_t-compatible code (0 = success).

@@ -65,6 +65,7 @@ struct KParams {
   int K, N, G, m_single, b_group_rows, b_base;
   int raster_gm;  // tile order inside a group: blocks of raster_gm m-tiles, m fastest inside a block
   int dynamic;    // 1: dynamic tile tickets (tile_counter), 0: static round robin
+  int row_mode;   // 0 all rows, 1 bulk (multiple of 256), 2 remainder (see GemmArgs)
   int64_t ldo;
   void* out;
   const float* bias;
@@ -234,8 +235,13 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
 
   // ---- group table: start rows, counts, tile prefix (warp-parallel scan)
   for (int g = threadIdx.x; g < G; g += NUM_THREADS) {
-    st.gcount[g] = p.row_count ? p.row_count[g] : p.m_single;
-    st.gstart[g] = p.row_start ? p.row_start[g] : 0;
+    int cnt = p.row_count ? p.row_count[g] : p.m_single;
+    int start = p.row_start ? p.row_start[g] : 0;
+    const int bulk = cnt & ~255;
+    if (p.row_mode == 1) cnt = bulk;
+    else if (p.row_mode == 2) { start += bulk; cnt -= bulk; }
+    st.gcount[g] = cnt;
+    st.gstart[g] = start;
   }
   if (threadIdx.x == 0) {
     for (int i = 0; i < C::STAGES; ++i) {
@@ -574,6 +580,7 @@ int launch_epi(const GemmArgs& a, cudaStream_t stream) {
   p.row_start = a.row_start;
   p.row_count = a.row_count;
   p.a_row_index = a.a_row_index;
+  p.row_mode = a.row_mode;
   // Launches that may run concurrently must use different counters (caller's).
   p.tile_counter = a.tile_counter ? a.tile_counter : ticket_counter(0);
   p.dynamic = (dynamic_sched() && p.tile_counter) ? 1 : 0;

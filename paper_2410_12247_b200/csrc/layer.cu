@@ -49,6 +49,8 @@ struct moe_layer {
   cudaEvent_t ev_host_start = nullptr, ev_in[4] = {}, ev_out[4] = {};
   cudaEvent_t ev_router = nullptr, ev_shared = nullptr;
   bool overlap_shared = true;     // shared experts on s_side, concurrent with routing (EPSMOE_OVERLAP_SHARED=0: in order)
+  bool split_rem = false;         // EPSMOE_SPLIT_REM=1: expert GEMMs as bulk on CTA pairs + remainder rows on
+                                  // single CTAs; measured 1-3% slower than padding (DSv2, Mixtral), so off
   bool gather_a = false;          // EPSMOE_GATHER=1: GateUp gathers x rows (tile::gather4) at ep == 1
                                   // instead of reading a materialised send buffer; measured 3.5x
                                   // slower GateUp on B200 (32 gather4 per stage), so off by default
@@ -249,6 +251,10 @@ int compute_moe(moe_layer* L, const void* A, int64_t a_rows, const int32_t* row_
   g2a.N = c.hidden;
   g2a.out = L->o;
   g2a.ldo = c.hidden;
+  // CTA-pair tiles cover each expert's first floor(M/256)*256 rows; with
+  // split_rem the remaining < 256 rows go to a second launch on 128-row
+  // single-CTA tiles (halves the M padding: ~64 instead of ~128 rows/expert).
+  const bool split = cta_pair && L->split_rem;
   auto run = [&](int a, int b) -> int {
     int stage = MOE_STAGE_GATEUP;
     for (GemmArgs* ga : {&g1a, &g2a}) {
@@ -257,10 +263,14 @@ int compute_moe(moe_layer* L, const void* A, int64_t a_rows, const int32_t* row_
       ga->row_start = row_start + a;
       ga->row_count = row_count + a;
       int p0 = prof_rec(L, st);
-      int e = gemm_launch(*ga, st);
-      if (e) return e;
+      for (int part = 0; part < (split ? 2 : 1); ++part) {
+        ga->row_mode = split ? 1 + part : 0;
+        ga->cta_pair = (split && part == 1) ? 0 : cta_pair;
+        int e = gemm_launch(*ga, st);
+        if (e) return e;
+        ++L->last_launches;
+      }
       prof_mark(L, stage, p0, prof_rec(L, st));
-      ++L->last_launches;
       stage = MOE_STAGE_DOWN;
     }
     return 0;
@@ -375,6 +385,7 @@ static moe_status_t create_impl(const moe_config_t* cfg, const moe_weights_t* w,
   default_cost_model(L->cfg, &L->cost);
   if (const char* ov = std::getenv("EPSMOE_OVERLAP_SHARED")) L->overlap_shared = std::atoi(ov) != 0;
   if (const char* gv = std::getenv("EPSMOE_GATHER")) L->gather_a = std::atoi(gv) != 0;
+  if (const char* sv = std::getenv("EPSMOE_SPLIT_REM")) L->split_rem = std::atoi(sv) != 0;
   if (cudaStreamCreateWithFlags(&L->s_h2d, cudaStreamNonBlocking) != cudaSuccess ||
       cudaStreamCreateWithFlags(&L->s_d2h, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreateWithFlags(&L->ev_host_start, cudaEventDisableTiming) != cudaSuccess) {
