@@ -18,6 +18,7 @@ paper-only tier) on a bounded token sample of the same workload.
 from __future__ import annotations
 
 import argparse
+import datetime
 import json
 import os
 import statistics
@@ -38,7 +39,7 @@ FALLBACK_PEAKS = dict(hbm_gbs=6650.0, bf16_tflops=1590.0, bf16_tflops_sustained=
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--steps", type=int, default=50)
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--config", default="dsv2")
     p.add_argument("--skew", type=float, default=0.0)
@@ -74,7 +75,7 @@ def peak_tflops(peaks):
 
 # ---------------------------------------------------------------- clocks
 class ClockSampler:
-    FIELDS = "index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active," \
+    FIELDS = "timestamp,index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active," \
              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown," \
              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap"
 
@@ -87,11 +88,15 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.gpu_index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "200"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+                 "-lms", "100"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
         except Exception:
             self.proc = None
 
-    def stop(self):
+    def mark(self):
+        """Host time at which the timed region starts / ends (samples outside are dropped)."""
+        return time.time()
+
+    def stop(self, t0=None, t1=None):
         if self.proc is None:
             return None
         self.proc.terminate()
@@ -102,8 +107,14 @@ class ClockSampler:
         rows = []
         for line in open(self.path):
             parts = [s.strip() for s in line.split(",")]
-            if len(parts) >= 9:
-                rows.append(parts)
+            if len(parts) >= 10:
+                try:
+                    ts = datetime.datetime.strptime(parts[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+                except ValueError:
+                    continue
+                if t0 is not None and not (t0 <= ts <= t1):
+                    continue
+                rows.append(parts[1:])
         os.unlink(self.path)
         if not rows:
             return None
@@ -180,7 +191,8 @@ def host_cores():
 
 
 def cpu_baseline(cfg, seed, skew, sample=0):
-    n = sample or {"tiny": 256, "dsv2_lite": 16, "mixtral": 4, "dsv2": 8}.get(cfg["name"], 8)
+    # sized for ~10-20 s of oracle work on a 16-core host (the contract's bounded sample)
+    n = sample or {"tiny": 256, "dsv2_lite": 256, "mixtral": 24, "dsv2": 48}.get(cfg["name"], 32)
     inp, ew, cache = oracle_sample(cfg, seed, n, 0, skew, device_gen=True)
     dt = run_oracle_timed(cfg, inp, ew, cache)
     return {"value": n / dt, "unit": UNIT, "cores": host_cores(), "kind": "oracle",
@@ -304,6 +316,7 @@ def ours(args, cfg):
     ev1 = torch.cuda.Event(enable_timing=True)
     stage_sum, stage_cnt = {}, {}
     launches = 0
+    t_start = clocks.mark()
     ev0.record(stream)
     for _ in range(args.steps):
         layer.forward(x, y, plan=plan)
@@ -313,9 +326,10 @@ def ours(args, cfg):
             stage_cnt[name] = stage_cnt.get(name, 0) + cnt
     ev1.record(stream)
     torch.cuda.synchronize()
+    t_end = clocks.mark()
     if D > 1:
         dist.barrier()
-    clk = clocks.stop()
+    clk = clocks.stop(t_start, t_end)
     layer.set_profiling(False)
     ms_total = ev0.elapsed_time(ev1)
     t = torch.tensor([ms_total], dtype=torch.float64, device=dev)
