@@ -192,7 +192,8 @@ def host_cores():
 
 def cpu_baseline(cfg, seed, skew, sample=0):
     # sized for ~10-20 s of oracle work on a 16-core host (the contract's bounded sample)
-    n = sample or {"tiny": 256, "dsv2_lite": 256, "mixtral": 24, "dsv2": 48}.get(cfg["name"], 32)
+    n = sample or {"tiny": 256, "dsv2_lite": 256, "mixtral": 24, "dsv2": 48, "dsv2_decode": 48,
+                   "mixtral_decode": 24}.get(cfg["name"], 32)
     inp, ew, cache = oracle_sample(cfg, seed, n, 0, skew, device_gen=True)
     dt = run_oracle_timed(cfg, inp, ew, cache)
     return {"value": n / dt, "unit": UNIT, "cores": host_cores(), "kind": "oracle",
@@ -204,7 +205,8 @@ def reference_arm(args, cfg):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    n = args.cpu_sample or {"tiny": 64, "dsv2_lite": 4, "mixtral": 1, "dsv2": 2}.get(cfg["name"], 2)
+    n = args.cpu_sample or {"tiny": 64, "dsv2_lite": 4, "mixtral": 1, "dsv2": 2, "dsv2_decode": 2,
+                             "mixtral_decode": 1}.get(cfg["name"], 2)
     inp, ew, cache = oracle_sample(cfg, args.seed, n, 0, args.skew)
     times = []
     for i in range(args.warmup + args.steps):
@@ -375,11 +377,22 @@ def ours(args, cfg):
         recv = int(ghist[:, r * E_loc:(r + 1) * E_loc].sum() - ghist[r, r * E_loc:(r + 1) * E_loc].sum())
         a2a_bytes.append(2.0 * H * 2 * max(sent, recv))
     nvl = float(peaks.get("nvlink_gbs", FALLBACK_PEAKS["nvlink_gbs"]))
-    t_roof = max(max(flops_rank) / (ptf * 1e12), max(a2a_bytes) / (nvl * 1e9) if D > 1 else 0.0) * 1e3
-    layer_roofline = {"bound": "tensor" if max(flops_rank) / (ptf * 1e12) >= max(a2a_bytes) / (nvl * 1e9) else "nvlink",
-                      "t_roof_ms": t_roof, "t_layer_ms": ms_step, "frac": t_roof / ms_step,
+    hbm = float(peaks.get("hbm_gbs", FALLBACK_PEAKS["hbm_gbs"]))
+    # HBM floor (decode-regime batches are weight-streaming): every activated expert's weights, the
+    # router and shared weights read once, x read and y written once (per rank)
+    active = [int((ghist[:, r * E_loc:(r + 1) * E_loc].sum(axis=0) > 0).sum()) for r in range(D)]
+    hbm_bytes = [2.0 * (3 * H * F * a + 3 * H * SF + E * H + 2 * H * int(starts[r + 1] - starts[r]))
+                 for r, a in enumerate(active)]
+    t_f = max(flops_rank) / (ptf * 1e12)
+    t_n = max(a2a_bytes) / (nvl * 1e9) if D > 1 else 0.0
+    t_h = max(hbm_bytes) / (hbm * 1e9)
+    t_roof = max(t_f, t_n, t_h) * 1e3
+    bound = "tensor" if t_f >= max(t_n, t_h) else ("nvlink" if t_n >= t_h else "hbm")
+    layer_roofline = {"bound": bound, "t_roof_ms": t_roof, "t_layer_ms": ms_step, "frac": t_roof / ms_step,
                       "flops_max_rank": max(flops_rank), "a2a_bytes_max_rank": max(a2a_bytes),
-                      "achieved_tflops": max(flops_rank) / (ms_step / 1e3) / 1e12}
+                      "hbm_bytes_max_rank": max(hbm_bytes), "active_experts": active,
+                      "achieved_tflops": max(flops_rank) / (ms_step / 1e3) / 1e12,
+                      "achieved_hbm_gbs": max(hbm_bytes) / (ms_step / 1e3) / 1e9}
 
     # ---- e2e through the public host-buffer entry point (H2D + layer + D2H per step)
     xh = x.cpu().pin_memory()

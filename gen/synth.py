@@ -128,6 +128,9 @@ CONFIGS = {
     "mixtral": dict(E=8, k=2, H=4096, F=14336, S=0, Fs=0, T=16384, norm_topk=1),
     "dsv2_lite": dict(E=64, k=6, H=2048, F=1408, S=2, Fs=1408, T=32768, norm_topk=0),
     "dsv2": dict(E=160, k=6, H=5120, F=1536, S=2, Fs=1536, T=65536, norm_topk=0),
+    # decode-regime batch (A22, NEXT-4; Table I's bs=256): weight-streaming, HBM-bound
+    "dsv2_decode": dict(E=160, k=6, H=5120, F=1536, S=2, Fs=1536, T=256, norm_topk=0),
+    "mixtral_decode": dict(E=8, k=2, H=4096, F=14336, S=0, Fs=0, T=256, norm_topk=1),
 }
 
 

@@ -671,7 +671,9 @@ moe_status_t moe_layer_forward(moe_layer_t* L, const void* x, int64_t T, void* y
   // ep == 1: the routing kernels stream with L2 evict-first hints, so they
   // co-run with the shared GEMMs (measured ~1% faster per layer than in order).
   const bool has_shared = L->SF && T > 0;
-  const bool side = has_shared && (D > 1 || L->overlap_shared);
+  // (small decode batches: the routing kernels are latency-bound and a concurrent
+  // persistent GEMM only delays them, so they stay in order below 8K tokens)
+  const bool side = has_shared && (D > 1 || (L->overlap_shared && T >= 8192));
   if (side) {
     CUDA_TRY(cudaEventRecord(L->ev_router, st));
     CUDA_TRY(cudaStreamWaitEvent(L->s_side, L->ev_router, 0));
