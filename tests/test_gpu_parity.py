@@ -217,6 +217,52 @@ def test_empty_and_single_token():
     assert y0.shape[0] == 0
 
 
+def test_cuda_graph_capture_replay():
+    """ep == 1 forward has no host synchronisation: it captures into a CUDA
+    graph (side stream + events included) and replays bit-identically."""
+    kw, k, norm = CASES["mid_shared"]
+    inp = Inputs(seed=19, **kw)
+    L = layer_from_inputs(inp, k, norm)
+    x = dev_bf16(inp.x)
+    ref = L.forward(x).clone()
+    plan = make_plan(1, MOE_GEMM_GROUPED)
+    y = torch.empty_like(x)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        L.forward(x, y, plan=plan, stream=s)          # warm-up outside capture
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        L.forward(x, y, plan=plan)
+    y.zero_()
+    for _ in range(3):
+        g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(y, ref)
+
+
+@pytest.mark.parametrize("E,k,H,F,T", [(256, 8, 8192, 128, 300), (2, 1, 64, 128, 33)])
+def test_extreme_shapes(E, k, H, F, T):
+    """Limits of the ABI: 256 experts, top-8, hidden 8192; and the degenerate
+    2-expert top-1 layer (norm_topk -> weight 1)."""
+    inp = Inputs(E=E, k=k, H=H, F=F, T=T, seed=23, grid=True)
+    L, y, b = _run_layer(inp, k, 1)
+    ref = oracle.moe_layer(inp.x, inp.w_router, inp.w_gate, inp.w_up, inp.w_down, k=k, norm_topk=1)
+    assert np.array_equal(b["topk_idx"].cpu().numpy(), ref["idx"])
+    assert np.array_equal(b["pos"].cpu().numpy(), ref["layout"]["pos"][0])
+    assert_close(to_f32(y), ref["y"], f"E{E} k{k} H{H}")
+
+
+def test_capacity_and_invalid_errors():
+    from paper_2410_12247_b200 import EpsMoeError
+    inp = Inputs(E=8, k=2, H=64, F=128, T=40, seed=2)
+    L = layer_from_inputs(inp, 2, 1, max_tokens=16)
+    with pytest.raises(EpsMoeError, match="CAPACITY"):
+        L.forward(dev_bf16(inp.x))
+
+
 def test_forward_host_sliced_pipeline_matches_device():
     """forward_host splits big batches into token slices (copies overlap the
     layer); rows are independent, so the result equals the one-shot forward."""
