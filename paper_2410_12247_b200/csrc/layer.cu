@@ -51,6 +51,8 @@ struct moe_layer {
   bool overlap_shared = true;     // shared experts on s_side, concurrent with routing (EPSMOE_OVERLAP_SHARED=0: in order)
   bool split_rem = false;         // EPSMOE_SPLIT_REM=1: expert GEMMs as bulk on CTA pairs + remainder rows on
                                   // single CTAs; measured 1-3% slower than padding (DSv2, Mixtral), so off
+  int comm_ctas = 0;              // ep > 1: NCCL maxCTAs per communicator (EPSMOE_COMM_CTAS, default 8);
+                                  // the persistent GEMM grid leaves 2*comm_ctas SMs free for them
   bool gather_a = false;          // EPSMOE_GATHER=1: GateUp gathers x rows (tile::gather4) at ep == 1
                                   // instead of reading a materialised send buffer; measured 3.5x
                                   // slower GateUp on B200 (32 gather4 per stage), so off by default
@@ -386,6 +388,10 @@ static moe_status_t create_impl(const moe_config_t* cfg, const moe_weights_t* w,
   if (const char* ov = std::getenv("EPSMOE_OVERLAP_SHARED")) L->overlap_shared = std::atoi(ov) != 0;
   if (const char* gv = std::getenv("EPSMOE_GATHER")) L->gather_a = std::atoi(gv) != 0;
   if (const char* sv = std::getenv("EPSMOE_SPLIT_REM")) L->split_rem = std::atoi(sv) != 0;
+  if (cfg->ep > 1) {
+    const char* cv = std::getenv("EPSMOE_COMM_CTAS");
+    L->comm_ctas = std::max(1, std::min(32, cv ? std::atoi(cv) : 8));
+  }
   if (cudaStreamCreateWithFlags(&L->s_h2d, cudaStreamNonBlocking) != cudaSuccess ||
       cudaStreamCreateWithFlags(&L->s_d2h, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreateWithFlags(&L->ev_host_start, cudaEventDisableTiming) != cudaSuccess) {
@@ -427,6 +433,8 @@ static moe_status_t create_impl(const moe_config_t* cfg, const moe_weights_t* w,
       std::memcpy(&id_c, uid_c, sizeof(id_c));
       ncclConfig_t ncfg = NCCL_CONFIG_INITIALIZER;
       ncfg.blocking = 1;
+      ncfg.maxCTAs = L->comm_ctas;  // the paper's comm-SM control
+      ncfg.minCTAs = std::min(L->comm_ctas, 2);
       ncclComm_t cd = nullptr, cc = nullptr;
       ncclResult_t r1 = ncclCommInitRankConfig(&cd, cfg->ep, id_d, cfg->rank, &ncfg);
       ncclResult_t r2 = r1 == ncclSuccess ? ncclCommInitRankConfig(&cc, cfg->ep, id_c, cfg->rank, &ncfg) : r1;
@@ -525,7 +533,12 @@ moe_status_t moe_exchange_layout(const moe_config_t* cfg, const moe_plan_t* plan
 moe_status_t moe_plan_pipeline(const moe_layer_t* L, int64_t global_tokens, const int32_t* global_hist,
                                moe_plan_t* out) {
   if (!L || !out) return MOE_ERR_INVALID;
-  return (moe_status_t)plan_compute(L->cfg, L->cost, global_tokens, global_hist, out);
+  int r = plan_compute(L->cfg, L->cost, global_tokens, global_hist, out);
+  if (r == MOE_OK && L->cfg.ep > 1) {  // SM partition of this layer (NEXT-1)
+    out->comm_ctas = L->comm_ctas;
+    out->sm_gemm = L->num_sms - 2 * L->comm_ctas;
+  }
+  return (moe_status_t)r;
 }
 
 moe_status_t moe_layer_set_cost_model(moe_layer_t* L, const moe_cost_model_t* cost) {
@@ -609,7 +622,11 @@ moe_status_t moe_layer_forward(moe_layer_t* L, const void* x, int64_t T, void* y
     int pv = plan_normalise(c, &plan);
     if (pv) { set_error("invalid plan"); return (moe_status_t)pv; }
   }
-  int num_ctas = (plan_in && plan.sm_gemm > 0) ? std::min(plan.sm_gemm, L->num_sms) : L->num_sms;
+  // GEMM SM budget (A15, Table IV): a persistent GEMM owns every SM
+  // it runs on (~220 KB smem), so at ep > 1 it must leave SMs for the two
+  // communicators' kernels or the all2all could not overlap it at all.
+  const int default_ctas = (D > 1) ? L->num_sms - 2 * L->comm_ctas : L->num_sms;
+  int num_ctas = (plan_in && plan.sm_gemm > 0) ? std::min(plan.sm_gemm, L->num_sms) : default_ctas;
 
   // ---- Router (K1) + topKGating (K2) + histogram
   int p0 = prof_rec(L, st);
@@ -845,7 +862,11 @@ moe_status_t moe_layer_forward(moe_layer_t* L, const void* x, int64_t T, void* y
         std::memcpy(dbg->global_hist_host, L->ghist_host, sizeof(int32_t) * D * E);
       }
     }
-    if (dbg->plan_used) *dbg->plan_used = plan;
+    if (dbg->plan_used) {
+      *dbg->plan_used = plan;
+      dbg->plan_used->sm_gemm = num_ctas;
+      if (D > 1) dbg->plan_used->comm_ctas = L->comm_ctas;
+    }
   }
   return MOE_OK;
 }

@@ -98,6 +98,9 @@ def test_ep_equals_ep1_and_oracle(D, N, kind, tile_m):
         assert np.array_equal(bufs[r]["global_hist"], lay["hist"])          # count allgather
         assert np.array_equal(bufs[r]["pos"].cpu().numpy(), lay["pos"][r])  # split on each rank
         assert bufs[r]["plan_used"].num_chunks == N
+        # SM partition (NEXT-1): the GEMM grid leaves 2 x comm_ctas SMs to the all2all
+        pu = bufs[r]["plan_used"]
+        assert pu.comm_ctas == 8 and pu.sm_gemm == torch.cuda.get_device_properties(0).multi_processor_count - 16
     assert_close(y, ref["y"], f"EP{D} N{N}")
 
 
