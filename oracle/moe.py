@@ -91,6 +91,45 @@ def silu_f32(g: np.ndarray) -> np.ndarray:
 
 
 # ----------------------------------------------------------------------------
+# FP8 dispatch payload (Table II "FP8" column P:312/331; NEXT-2, R15).
+# ----------------------------------------------------------------------------
+
+E4M3_MAX = 448.0
+FP8_BLOCK = 128
+
+
+def fp8_block_exponent(amax: float) -> int:
+    """Smallest s with amax / 2^s <= 448 (power-of-two block scale, R15).
+    amax = m 2^e with 1 <= m < 2 and 448 = 1.75 2^8, so s = e-8 if m <= 1.75
+    else e-7; clamped to s >= -126 (2^s a normal fp32).  amax == 0 -> -126."""
+    if amax == 0.0:
+        return -126
+    m, e = np.frexp(np.float64(amax))       # amax = m 2^e, 0.5 <= m < 1
+    m, e = 2.0 * m, int(e) - 1               # 1 <= m < 2
+    return max(-126, e - 8 if m <= 1.75 else e - 7)
+
+
+def fp8_dispatch_roundtrip(x_bits: np.ndarray) -> np.ndarray:
+    """The value an expert receives for a row dispatched in FP8 (R15):
+    per 128-column block, s = fp8_block_exponent(max|x|), q = e4m3_rne(x 2^-s)
+    (never saturates: |x 2^-s| <= 448), x' = q 2^s (exact in bf16).
+    Returns bf16 bit patterns.  e4m3 rounding uses torch's float8_e4m3fn cast
+    (a library routine; RNE)."""
+    import torch
+    x = bf16_bits_to_f64(x_bits)
+    out = np.empty_like(x)
+    rows, cols = x.shape
+    for b0 in range(0, cols, FP8_BLOCK):
+        blk = x[:, b0:b0 + FP8_BLOCK]
+        for r in range(rows):
+            s = fp8_block_exponent(float(np.abs(blk[r]).max()))
+            v = blk[r] * np.float64(2.0) ** (-s)                 # exact (power of two)
+            q = torch.from_numpy(v.astype(np.float32)).to(torch.float8_e4m3fn).to(torch.float64).numpy()
+            out[r, b0:b0 + FP8_BLOCK] = q * np.float64(2.0) ** s
+    return bf16_value_to_bits(out.astype(np.float32))
+
+
+# ----------------------------------------------------------------------------
 # Step 1: Router (Alg. 1 line `index <- Router(input)`, P:565).
 # ----------------------------------------------------------------------------
 
@@ -305,11 +344,12 @@ def combine(s, o_slots, w, mode="contract"):
 def moe_layer(x_bits, w_router_bits, w_gate_bits, w_up_bits, w_down_bits, k, norm_topk,
               ws_gate_bits=None, ws_up_bits=None, ws_down_bits=None, router_bias=None,
               routed_scale=1.0, D=1, N=1, token_slices=1, mode="contract",
-              topk_override=None):
+              topk_override=None, dispatch_fp8=False):
     """Full layer over all T tokens.  Weights are indexed by global expert id.
 
     topk_override = (idx, w) replaces Router + topKGating (explicit routing,
-    used by the fig:eps_overview fixture).
+    used by the fig:eps_overview fixture).  dispatch_fp8: every dispatched row
+    travels as FP8 (fp8_dispatch_roundtrip, R15); shared experts see x.
     """
     T, H = x_bits.shape
     E = w_gate_bits.shape[0]
@@ -328,14 +368,16 @@ def moe_layer(x_bits, w_router_bits, w_gate_bits, w_up_bits, w_down_bits, k, nor
     start = lay["token_start"]
     gb = chunk_groups(E_loc, N)
 
-    # Send buffers (split): row pos[r][t,j] of rank r holds x[t].
+    # Send buffers (split): row pos[r][t,j] of rank r holds x[t]
+    # (or its FP8 round trip when the dispatch payload is FP8).
+    x_disp = fp8_dispatch_roundtrip(x_bits) if dispatch_fp8 else x_bits
     send = []
     for r in range(D):
         buf = np.zeros((int(lay["send_start"][r, E]), H), dtype=np.uint16)
         p = lay["pos"][r]
         for t in range(p.shape[0]):
             for j in range(k):
-                buf[p[t, j]] = x_bits[start[r] + t]
+                buf[p[t, j]] = x_disp[start[r] + t]
         send.append(buf)
 
     # Dispatch -> ComputeMoE -> combine, chunk by chunk.  The
@@ -379,18 +421,19 @@ def moe_layer(x_bits, w_router_bits, w_gate_bits, w_up_bits, w_down_bits, k, nor
 
 
 def moe_tokens(x_bits, w_router_bits, expert_weights, k, norm_topk, shared=None,
-               router_bias=None, routed_scale=1.0, mode="contract"):
+               router_bias=None, routed_scale=1.0, mode="contract", dispatch_fp8=False):
     """y for an arbitrary subset of tokens (y_t depends only on x_t and the
     weights).  expert_weights: callable e -> (Wg, Wu, Wd) bits.
     Used for sampled parity at the full BASELINE sizes."""
     logits = router_logits(x_bits, w_router_bits, router_bias, mode)
     idx, w = topk_gating(logits, k, norm_topk, routed_scale, mode)
     T, H = x_bits.shape
+    x_disp = fp8_dispatch_roundtrip(x_bits) if dispatch_fp8 else x_bits
     o_slots = np.zeros((T, k, H), dtype=np.float64 if mode == "exact" else np.float32)
     for e in np.unique(idx):
         tok, slot = np.nonzero(idx == e)
         wg, wu, wd = expert_weights(int(e))
-        o_slots[tok, slot] = expert_ffn(x_bits[tok], wg, wu, wd, mode)
+        o_slots[tok, slot] = expert_ffn(x_disp[tok], wg, wu, wd, mode)
     if shared is not None:
         s = expert_ffn(x_bits, *shared, mode)
     else:

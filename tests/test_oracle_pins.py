@@ -301,7 +301,74 @@ def test_moe_tokens_matches_moe_layer_subset():
 
 
 # --------------------------------------------------------------------------
-# 7. Pipeline-number rule: closed form vs grid argmax
+# 7. FP8 dispatch payload (NEXT-2, R15)
+# --------------------------------------------------------------------------
+
+def _e4m3_values():
+    """All finite OCP e4m3 (fn) values from the format definition: sign, 4-bit
+    exponent (bias 7), 3-bit mantissa, subnormals at exponent 0; S.1111.111 is NaN."""
+    vals = []
+    for code in range(256):
+        s, e, m = code >> 7, (code >> 3) & 15, code & 7
+        if e == 15 and m == 7:
+            continue
+        v = (m / 8.0) * 2.0 ** -6 if e == 0 else (1 + m / 8.0) * 2.0 ** (e - 7)
+        vals.append((-v if s else v, m))
+    return vals
+
+
+def test_fp8_block_exponent_closed_form():
+    assert oracle.fp8_block_exponent(448.0) == 0
+    assert oracle.fp8_block_exponent(449.0) == 1
+    assert oracle.fp8_block_exponent(1.0) == -8
+    rng = np.random.default_rng(4)
+    for a in np.exp(rng.uniform(-20, 20, 2000)):
+        s = oracle.fp8_block_exponent(float(a))
+        assert a / 2.0 ** s <= 448.0 < a / 2.0 ** (s - 1)
+
+
+def test_fp8_roundtrip_vs_format_definition():
+    """Brute force: every element of the round trip is the nearest e4m3 value
+    (ties to even mantissa) of x 2^-s, times 2^s."""
+    vals = _e4m3_values()
+    grid = np.array([v for v, _ in vals])
+    mant = np.array([m for _, m in vals])
+    inp = Inputs(E=1, k=1, H=256, F=128, T=12, seed=8)
+    x = oracle.bf16_bits_to_f64(inp.x)
+    x[3, :128] *= 1e-3          # a block with a very different scale
+    x[5, 128:] = 0.0            # an all-zero block
+    xb = oracle.bf16_value_to_bits(x.astype(np.float32))
+    got = oracle.bf16_bits_to_f64(oracle.fp8_dispatch_roundtrip(xb))
+    x = oracle.bf16_bits_to_f64(xb)
+    for r in range(12):
+        for b0 in (0, 128):
+            blk = x[r, b0:b0 + 128]
+            s = oracle.fp8_block_exponent(float(np.abs(blk).max()))
+            for c, v in enumerate(blk * 2.0 ** (-s)):
+                d = np.abs(grid - v)
+                cand = np.nonzero(d == d.min())[0]
+                best = cand[0] if len(cand) == 1 else cand[np.argmin(mant[cand] & 1)]
+                assert got[r, b0 + c] == grid[best] * 2.0 ** s, (r, b0 + c)
+    # idempotent, bf16-exact, relative error <= 2^-4 on normal e4m3 values
+    again = oracle.fp8_dispatch_roundtrip(oracle.bf16_value_to_bits(got.astype(np.float32)))
+    assert np.array_equal(oracle.bf16_bits_to_f64(again), got)
+
+
+def test_fp8_dispatch_layer_band():
+    inp = Inputs(E=8, k=2, H=256, F=128, S=1, Fs=128, T=48, seed=5)
+    args = (inp.x, inp.w_router, inp.w_gate, inp.w_up, inp.w_down)
+    kw = dict(k=2, norm_topk=1, ws_gate_bits=inp.ws_gate, ws_up_bits=inp.ws_up, ws_down_bits=inp.ws_down)
+    y = oracle.moe_layer(*args, **kw)["y"]
+    y8 = oracle.moe_layer(*args, dispatch_fp8=True, **kw)
+    rel = np.abs(y8["y"] - y).sum() / np.abs(y).sum()
+    assert 1e-3 < rel < 5e-2              # e4m3 carries 3 mantissa bits
+    assert np.array_equal(y8["idx"], oracle.moe_layer(*args, **kw)["idx"])   # routing sees x, not x'
+    # chunked / EP invariance holds in FP8 mode too
+    assert np.array_equal(oracle.moe_layer(*args, dispatch_fp8=True, D=2, N=2, **kw)["y"], y8["y"])
+
+
+# --------------------------------------------------------------------------
+# 8. Pipeline-number rule (P:408-425): closed form vs grid argmax
 # --------------------------------------------------------------------------
 
 def test_pn_closed_form_example():
