@@ -69,6 +69,10 @@ typedef struct {
   int32_t norm_topk;    /* 1: renormalise the top-k weights (Mixtral); 0: raw
                            softmax probabilities (DeepSeek)             (R1)  */
   float routed_scale;   /* multiplies routed weights (1.0)                    */
+  int32_t dispatch_fp8; /* 1: routed rows travel as FP8 e4m3 with one power-of-
+                           two scale per 128 columns (Table II "FP8", P:312,
+                           P:331; NEXT-2, R15); experts see the exact dequant;
+                           needs hidden % 128 == 0.  0: bf16 payload.        */
 } moe_config_t;
 
 /* Caller-owned device weights (bf16, K-major), valid for the layer's life.

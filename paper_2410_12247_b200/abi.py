@@ -28,7 +28,7 @@ class moe_config_t(C.Structure):
     _fields_ = [("num_experts", C.c_int32), ("top_k", C.c_int32), ("hidden", C.c_int32),
                 ("ffn", C.c_int32), ("num_shared", C.c_int32), ("shared_ffn", C.c_int32),
                 ("ep", C.c_int32), ("rank", C.c_int32), ("max_tokens", C.c_int64),
-                ("norm_topk", C.c_int32), ("routed_scale", C.c_float)]
+                ("norm_topk", C.c_int32), ("routed_scale", C.c_float), ("dispatch_fp8", C.c_int32)]
 
 
 class moe_weights_t(C.Structure):
@@ -127,8 +127,9 @@ def check(status: int, what: str = "") -> None:
         raise EpsMoeError(f"{what}: {STATUS.get(status, status)}: {msg}")
 
 
-def make_config(E, k, H, F, S=0, Fs=0, ep=1, rank=0, max_tokens=1, norm_topk=0, routed_scale=1.0):
-    return moe_config_t(E, k, H, F, S, Fs, ep, rank, max_tokens, norm_topk, routed_scale)
+def make_config(E, k, H, F, S=0, Fs=0, ep=1, rank=0, max_tokens=1, norm_topk=0, routed_scale=1.0,
+                dispatch_fp8=0):
+    return moe_config_t(E, k, H, F, S, Fs, ep, rank, max_tokens, norm_topk, routed_scale, dispatch_fp8)
 
 
 def plan_compute(cfg: moe_config_t, global_tokens: int, global_hist=None, cost: moe_cost_model_t | None = None):

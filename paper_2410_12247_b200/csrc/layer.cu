@@ -39,6 +39,8 @@ struct moe_layer {
   int32_t *recv_start_d = nullptr, *recv_count_d = nullptr;
   void *send = nullptr, *recv = nullptr, *h = nullptr, *o = nullptr, *comb = nullptr;
   void *hs = nullptr, *s = nullptr;
+  void *sendq = nullptr, *recvq = nullptr;  // ep > 1 && dispatch_fp8: packed FP8 rows (pitch qpitch)
+  int qpitch = 0;
   void *x_dev = nullptr, *y_dev = nullptr;  // staging for forward_host
   // host
   int32_t* ghist_host = nullptr;    // pinned [ep*E]
@@ -136,6 +138,7 @@ int validate(const moe_config_t* c) {
   else if (c->ffn < 128 || c->ffn % 128) why = "ffn must be a positive multiple of 128";
   else if (c->num_shared < 0 || (c->num_shared > 0 && ((int64_t)c->num_shared * c->shared_ffn) % 128))
     why = "num_shared * shared_ffn must be a multiple of 128";
+  else if (c->dispatch_fp8 && c->hidden % 128) why = "dispatch_fp8 needs hidden % 128 == 0";
   else if (c->max_tokens < 1) why = "max_tokens must be >= 1";
   if (!why.empty()) { set_error("invalid config: " + why); return MOE_ERR_INVALID; }
   return MOE_OK;
@@ -171,6 +174,11 @@ size_t carve(moe_layer* L, char* base) {
   L->h = cv.take<uint16_t>(L->gemm_rows_cap * F);
   L->o = cv.take<uint16_t>(L->gemm_rows_cap * H);
   L->comb = (D == 1) ? nullptr : cv.take<uint16_t>(L->send_cap * H);
+  L->qpitch = fp8_row_pitch((int)H);
+  if (D > 1 && c.dispatch_fp8) {
+    L->sendq = cv.take<uint8_t>(L->send_cap * L->qpitch);
+    L->recvq = cv.take<uint8_t>(L->recv_cap * L->qpitch);
+  }
   L->hs = SF ? cv.take<uint16_t>(T * SF) : nullptr;
   L->s = SF ? cv.take<uint16_t>(T * H) : nullptr;
   L->x_dev = cv.take<uint16_t>(T * H);
@@ -706,9 +714,11 @@ moe_status_t moe_layer_forward(moe_layer_t* L, const void* x, int64_t T, void* y
   // ---- split (K3): x -> send rows, expert-major (R6).  At ep == 1 the send
   // buffer is only the GateUp GEMM's A operand, so by default the split is
   // index-only and the GEMM gathers x's rows with TMA tile::gather4.
-  const bool gather = (D == 1) && L->gather_a && T > 0;
+  const bool fp8 = c.dispatch_fp8 != 0;
+  const bool gather = (D == 1) && L->gather_a && T > 0 && !fp8;
   KERNEL_TRY(launch_permute(x, (int)T, H, E, k, topk_idx, L->range_off, L->seg_start, gather ? nullptr : L->send,
-                            L->pos, gather ? L->row_token : nullptr, st));
+                            L->pos, gather ? L->row_token : nullptr, fp8 ? (D == 1 ? 1 : 2) : 0, L->sendq,
+                            L->qpitch, st));
   prof_mark(L, MOE_STAGE_ROUTE, p1, prof_rec(L, st));
   if (has_shared && !side) {
     int e = shared_experts(st);
@@ -765,6 +775,10 @@ moe_status_t moe_layer_forward(moe_layer_t* L, const void* x, int64_t T, void* y
     CUDA_TRY(cudaStreamWaitEvent(L->s_disp, L->ev_ready, 0));
     CUDA_TRY(cudaStreamWaitEvent(L->s_comb, L->ev_ready, 0));
     const size_t row_bytes = (size_t)H * 2;
+    // dispatch payload: bf16 rows, or packed FP8 rows (NEXT-2) dequantised per chunk on arrival
+    char* dsend = fp8 ? (char*)L->sendq : (char*)L->send;
+    char* drecv = fp8 ? (char*)L->recvq : (char*)L->recv;
+    const size_t drow = fp8 ? (size_t)L->qpitch : row_bytes;
     auto dispatch = [&](int ch) -> moe_status_t {
       int g0 = plan.group_begin[ch], g1 = plan.group_begin[ch + 1];
       int d0 = prof_rec(L, L->s_disp);
@@ -773,12 +787,10 @@ moe_status_t moe_layer_forward(moe_layer_t* L, const void* x, int64_t T, void* y
         for (int el = g0; el < g1; ++el) {
           int ex = peer * E_loc + el;
           int64_t n_send = gh[(int64_t)me * E + ex];
-          if (n_send)
-            TR_TRY(L->tr->send((char*)L->send + send_off[ex] * row_bytes, n_send * row_bytes, peer, 0, L->s_disp));
+          if (n_send) TR_TRY(L->tr->send(dsend + send_off[ex] * drow, n_send * drow, peer, 0, L->s_disp));
           int64_t n_recv = gh[(int64_t)peer * E + me * E_loc + el];
           if (n_recv)
-            TR_TRY(L->tr->recv((char*)L->recv + recv_off[(size_t)el * D + peer] * row_bytes, n_recv * row_bytes, peer,
-                               0, L->s_disp));
+            TR_TRY(L->tr->recv(drecv + recv_off[(size_t)el * D + peer] * drow, n_recv * drow, peer, 0, L->s_disp));
         }
       TR_TRY(L->tr->group_end(0, L->s_disp));
       prof_mark(L, MOE_STAGE_DISPATCH, d0, prof_rec(L, L->s_disp));
@@ -808,6 +820,10 @@ moe_status_t moe_layer_forward(moe_layer_t* L, const void* x, int64_t T, void* y
     auto compute = [&](int ch) -> moe_status_t {
       int g0 = plan.group_begin[ch], g1 = plan.group_begin[ch + 1];
       CUDA_TRY(cudaStreamWaitEvent(st, L->ev_disp[ch], 0));
+      if (fp8) {  // the chunk's received rows are contiguous in the recv layout (R6)
+        const int64_t r0 = recv_off[(size_t)g0 * D], r1 = recv_off[(size_t)g1 * D];
+        KERNEL_TRY(launch_dequant_rows(drecv + r0 * drow, r1 - r0, H, L->qpitch, (char*)L->recv + r0 * row_bytes, st));
+      }
       int a = g0;
       while (a < g1) {
         int b = a + 1;

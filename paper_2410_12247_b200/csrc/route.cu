@@ -6,6 +6,8 @@
 // tokens, one warp per range, so every per-expert offset is a deterministic
 // prefix sum: no atomics decide any row index.
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <cuda_fp8.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -195,13 +197,71 @@ __global__ void __launch_bounds__(256) seg_scan_kernel(const int32_t* __restrict
   if (threadIdx.x == 255) seg_start[E] = ex + hv;
 }
 
+// ---- FP8 dispatch payload (NEXT-2, R15): per 128-column block a power-of-two
+// scale 2^s with s the smallest integer such that max|x| / 2^s <= 448; values
+// x 2^-s are rounded to e4m3 (RNE, never saturating); the receiver's x' = q 2^s
+// is exact in bf16.  One uint4 = 8 bf16 = 1/16 of a block; the 16 uint4 of a
+// block sit in 16 consecutive lanes (a half warp) of the permute's copy loop.
+__device__ __forceinline__ int fp8_block_exp(float amax) {
+  const uint32_t b = __float_as_uint(amax);
+  if (amax == 0.f || (b >> 23) == 0) return -126;  // zero / subnormal block
+  const int e = (int)(b >> 23) - 127;
+  const int s = ((b & 0x7FFFFFu) <= 0x600000u) ? e - 8 : e - 7;  // mantissa <= 1.75 ?
+  return max(-126, s);
+}
+__device__ __forceinline__ float pow2f(int s) { return __uint_as_float((uint32_t)(127 + s) << 23); }
+
+// 8 bf16 -> 8 e4m3 bytes of x * inv (inv = 2^-s, exact)
+__device__ __forceinline__ uint2 quant8(const uint4& v, float inv) {
+  const __nv_bfloat162* p = reinterpret_cast<const __nv_bfloat162*>(&v);
+  uint32_t w[2];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    float2 a = __bfloat1622float2(p[2 * h]), b = __bfloat1622float2(p[2 * h + 1]);
+    __nv_fp8x2_storage_t qa = __nv_cvt_float2_to_fp8x2(make_float2(a.x * inv, a.y * inv), __NV_SATFINITE, __NV_E4M3);
+    __nv_fp8x2_storage_t qb = __nv_cvt_float2_to_fp8x2(make_float2(b.x * inv, b.y * inv), __NV_SATFINITE, __NV_E4M3);
+    w[h] = (uint32_t)qa | ((uint32_t)qb << 16);
+  }
+  return make_uint2(w[0], w[1]);
+}
+// 8 e4m3 bytes -> 8 bf16 of q * scale (exact)
+__device__ __forceinline__ uint4 dequant8(const uint2& q, float scale) {
+  uint4 out;
+  __nv_bfloat162* o = reinterpret_cast<__nv_bfloat162*>(&out);
+  const uint32_t w[2] = {q.x, q.y};
+#pragma unroll
+  for (int h = 0; h < 2; ++h)
+#pragma unroll
+    for (int part = 0; part < 2; ++part) {
+      __half2_raw hr = __nv_cvt_fp8x2_to_halfraw2((__nv_fp8x2_storage_t)(w[h] >> (16 * part)), __NV_E4M3);
+      float2 f = __half22float2(*reinterpret_cast<__half2*>(&hr));
+      o[2 * h + part] = __floats2bfloat162_rn(f.x * scale, f.y * scale);
+    }
+  return out;
+}
+__device__ __forceinline__ float amax8(const uint4& v) {
+  const __nv_bfloat162* p = reinterpret_cast<const __nv_bfloat162*>(&v);
+  float m = 0.f;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    float2 f = __bfloat1622float2(p[i]);
+    m = fmaxf(m, fmaxf(fabsf(f.x), fabsf(f.y)));
+  }
+  return m;
+}
+
 // K3 permute (`split`).  One warp per token range; each token's row is
 // read once and written to its k destination rows with 16-byte stores.
+// fp8: 0 = bf16 rows; 1 = bf16 rows of the FP8 round trip (ep == 1: the
+// values experts see when the payload is FP8); 2 = packed FP8 rows of `qpitch`
+// bytes (H e4m3 bytes, then H/128 int8 block exponents) into `sendq`.
+template <int fp8>
 __global__ void __launch_bounds__(WARPS_R * 32, 4)
 permute_kernel(const __nv_bfloat16* __restrict__ x, int T, int H, int E, int k,
                const int32_t* __restrict__ topk_idx, const int32_t* __restrict__ range_off,
                const int32_t* __restrict__ seg_start, int R, __nv_bfloat16* __restrict__ send,
-               int32_t* __restrict__ pos, int32_t* __restrict__ row_token) {
+               int32_t* __restrict__ pos, int32_t* __restrict__ row_token, uint8_t* __restrict__ sendq,
+               int qpitch) {
   __shared__ int32_t off_s[WARPS_R][256];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int r = blockIdx.x * WARPS_R + warp;
@@ -225,7 +285,7 @@ permute_kernel(const __nv_bfloat16* __restrict__ x, int T, int H, int E, int k,
       off_s[warp][e] = dest + 1;  // experts of one token are distinct
     }
     __syncwarp();
-    if (send == nullptr) continue;  // index-only split: the GEMM gathers rows of x itself
+    if (send == nullptr && fp8 != 2) continue;  // index-only split: the GEMM gathers rows of x itself
     const uint4* src = reinterpret_cast<const uint4*>(x + (int64_t)t * H);
     // 16 x 16 B per lane in flight per pass (H <= 4096 per pass, <= 2 passes):
     // keeps the kernel under 128 registers so it co-resides with a GEMM CTA.
@@ -237,6 +297,40 @@ permute_kernel(const __nv_bfloat16* __restrict__ x, int T, int H, int E, int k,
         int c = base + lane + 32 * i;
         if (c < nvec) buf[i] = ld_stream(src + c, pol);
       }
+      if constexpr (fp8 != 0) {
+        // per-block exponent: amax over the half warp holding the block's 16 uint4
+        int sexp[MAXV];
+#pragma unroll
+        for (int i = 0; i < MAXV; ++i) {
+          float m = (base + lane + 32 * i < nvec) ? amax8(buf[i]) : 0.f;
+#pragma unroll
+          for (int off = 8; off > 0; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
+          sexp[i] = fp8_block_exp(m);
+        }
+        if (fp8 == 1) {
+#pragma unroll
+          for (int i = 0; i < MAXV; ++i)
+            if (base + lane + 32 * i < nvec) buf[i] = dequant8(quant8(buf[i], pow2f(-sexp[i])), pow2f(sexp[i]));
+        } else {
+          uint2 q[MAXV];
+#pragma unroll
+          for (int i = 0; i < MAXV; ++i)
+            if (base + lane + 32 * i < nvec) q[i] = quant8(buf[i], pow2f(-sexp[i]));
+          for (int j = 0; j < k; ++j) {
+            int d = __shfl_sync(0xffffffffu, dest, j);
+            uint8_t* row = sendq + (int64_t)d * qpitch;
+#pragma unroll
+            for (int i = 0; i < MAXV; ++i) {
+              const int c = base + lane + 32 * i;
+              if (c < nvec) {
+                reinterpret_cast<uint2*>(row)[c] = q[i];
+                if ((lane & 15) == 0) row[H + (c >> 4)] = (uint8_t)(int8_t)sexp[i];
+              }
+            }
+          }
+          continue;
+        }
+      }
       for (int j = 0; j < k; ++j) {
         int d = __shfl_sync(0xffffffffu, dest, j);
         uint4* dst = reinterpret_cast<uint4*>(send + (int64_t)d * H);
@@ -247,6 +341,23 @@ permute_kernel(const __nv_bfloat16* __restrict__ x, int T, int H, int E, int k,
         }
       }
     }
+  }
+}
+
+// Receiver side of the FP8 dispatch: rows [0, rows) of packed FP8 rows (pitch
+// qpitch) -> bf16 rows (pitch H), x' = q 2^s exactly.  One warp per row.
+__global__ void __launch_bounds__(256) dequant_rows_kernel(const uint8_t* __restrict__ q, int64_t rows, int H,
+                                                           int qpitch, __nv_bfloat16* __restrict__ out) {
+  const int64_t row = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (row >= rows) return;
+  const int lane = threadIdx.x & 31;
+  const uint8_t* src = q + row * qpitch;
+  uint4* dst = reinterpret_cast<uint4*>(out + row * H);
+  const int nvec = H >> 3;
+  for (int c = lane; c < nvec; c += 32) {
+    const uint2 v = reinterpret_cast<const uint2*>(src)[c];
+    const int s = (int)(int8_t)src[H + (c >> 4)];
+    dst[c] = dequant8(v, pow2f(s));
   }
 }
 
@@ -346,11 +457,30 @@ int launch_range_scan(const int32_t* range_hist, int T, int E, int32_t* range_of
 }
 
 int launch_permute(const void* x, int T, int H, int E, int k, const int32_t* topk_idx, const int32_t* range_off,
-                   const int32_t* seg_start, void* send, int32_t* pos, int32_t* row_token, cudaStream_t st) {
+                   const int32_t* seg_start, void* send, int32_t* pos, int32_t* row_token, int fp8, void* sendq,
+                   int qpitch, cudaStream_t st) {
   int R = num_ranges(T);
   if (R == 0) return 0;
-  permute_kernel<<<(R + WARPS_R - 1) / WARPS_R, WARPS_R * 32, 0, st>>>(
-      (const __nv_bfloat16*)x, T, H, E, k, topk_idx, range_off, seg_start, R, (__nv_bfloat16*)send, pos, row_token);
+  const dim3 grid((R + WARPS_R - 1) / WARPS_R), block(WARPS_R * 32);
+  auto xb = (const __nv_bfloat16*)x;
+  auto sb = (__nv_bfloat16*)send;
+  auto qb = (uint8_t*)sendq;
+  if (fp8 == 0)
+    permute_kernel<0><<<grid, block, 0, st>>>(xb, T, H, E, k, topk_idx, range_off, seg_start, R, sb, pos, row_token,
+                                              qb, qpitch);
+  else if (fp8 == 1)
+    permute_kernel<1><<<grid, block, 0, st>>>(xb, T, H, E, k, topk_idx, range_off, seg_start, R, sb, pos, row_token,
+                                              qb, qpitch);
+  else
+    permute_kernel<2><<<grid, block, 0, st>>>(xb, T, H, E, k, topk_idx, range_off, seg_start, R, sb, pos, row_token,
+                                              qb, qpitch);
+  return (int)cudaGetLastError();
+}
+
+int launch_dequant_rows(const void* q, int64_t rows, int H, int qpitch, void* out, cudaStream_t st) {
+  if (rows <= 0) return 0;
+  dequant_rows_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, st>>>((const uint8_t*)q, rows, H, qpitch,
+                                                                   (__nv_bfloat16*)out);
   return (int)cudaGetLastError();
 }
 

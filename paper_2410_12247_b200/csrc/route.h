@@ -13,9 +13,14 @@ int launch_gate_topk(const float* logits, int T, int E, int k, int norm_topk, fl
 // per-range offsets, per-expert totals (hist) and expert segment starts (seg_start[E+1])
 int launch_range_scan(const int32_t* range_hist, int T, int E, int32_t* range_off, int32_t* hist,
                       int32_t* seg_start, cudaStream_t st);
+// send == nullptr (and fp8 != 2): index-only (pos, row_token).  fp8: 0 bf16 rows, 1 bf16 rows of the FP8
+// round trip, 2 packed FP8 rows (pitch qpitch = H + H/128 rounded up to 16) into sendq.
 int launch_permute(const void* x, int T, int H, int E, int k, const int32_t* topk_idx, const int32_t* range_off,
-                   const int32_t* seg_start, void* send, int32_t* pos, int32_t* row_token,
-                   cudaStream_t st);  // send == nullptr: index-only (pos, row_token)
+                   const int32_t* seg_start, void* send, int32_t* pos, int32_t* row_token, int fp8, void* sendq,
+                   int qpitch, cudaStream_t st);
+// packed FP8 rows -> bf16 rows (exact), rows [0, rows)
+int launch_dequant_rows(const void* q, int64_t rows, int H, int qpitch, void* out, cudaStream_t st);
+inline int fp8_row_pitch(int H) { return ((H + H / 128) + 15) & ~15; }
 int launch_combine(const void* o, const void* s, int T, int H, int k, const int32_t* pos, const float* topk_w,
                    void* y, cudaStream_t st);
 int launch_pad_rows(const void* src, int rows, int H, void* dst, int rows_pad, cudaStream_t st);

@@ -29,7 +29,7 @@ def test_library_exports_every_header_symbol():
 
 
 def test_struct_sizes_match_header_layout():
-    assert C.sizeof(abi.moe_config_t) == 48
+    assert C.sizeof(abi.moe_config_t) == 56
     assert C.sizeof(abi.moe_weights_t) == 64
     assert C.sizeof(abi.moe_plan_t) == 5 * 4 + 65 * 4 + 256 + 5 * 4 + 4
 

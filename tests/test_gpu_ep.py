@@ -22,7 +22,7 @@ from .gpu_util import assert_close, dev_bf16, to_f32
 pytestmark = pytest.mark.gpu
 
 
-def _ep_forward(inp, k, norm, D, plan=None, skew_bias=None):
+def _ep_forward(inp, k, norm, D, plan=None, skew_bias=None, fp8=False):
     E, H, F, T = inp.E, inp.H, inp.F, inp.T
     E_loc = E // D
     start = oracle.token_shards(T, D)
@@ -38,7 +38,7 @@ def _ep_forward(inp, k, norm, D, plan=None, skew_bias=None):
             w["router_bias"] = torch.from_numpy(skew_bias).cuda()
         T_loc = int(start[r + 1] - start[r])
         layers.append(MoELayer(E, k, H, F, w, S=inp.S, Fs=inp.Fs, ep=D, rank=r, max_tokens=max(T_loc, 1),
-                               norm_topk=norm, local_group=group))
+                               norm_topk=norm, local_group=group, dispatch_fp8=fp8))
         xs.append(dev_bf16(inp.x[start[r]:start[r + 1]]))
     ys, bufs, errs = [None] * D, [None] * D, []
 
@@ -67,14 +67,15 @@ def _ep_forward(inp, k, norm, D, plan=None, skew_bias=None):
     return y, bufs
 
 
-def _ep1_forward(inp, k, norm, plan=None, skew_bias=None):
+def _ep1_forward(inp, k, norm, plan=None, skew_bias=None, fp8=False):
     w = dict(w_router=dev_bf16(inp.w_router), w_gate=dev_bf16(inp.w_gate), w_up=dev_bf16(inp.w_up),
              w_down=dev_bf16(inp.w_down))
     if inp.S:
         w.update(ws_gate=dev_bf16(inp.ws_gate), ws_up=dev_bf16(inp.ws_up), ws_down=dev_bf16(inp.ws_down))
     if skew_bias is not None:
         w["router_bias"] = torch.from_numpy(skew_bias).cuda()
-    L = MoELayer(inp.E, k, inp.H, inp.F, w, S=inp.S, Fs=inp.Fs, max_tokens=inp.T, norm_topk=norm)
+    L = MoELayer(inp.E, k, inp.H, inp.F, w, S=inp.S, Fs=inp.Fs, max_tokens=inp.T, norm_topk=norm,
+                 dispatch_fp8=fp8)
     y = L.forward(dev_bf16(inp.x), plan=plan)
     torch.cuda.synchronize()
     out = y.float().cpu().numpy()
@@ -102,6 +103,25 @@ def test_ep_equals_ep1_and_oracle(D, N, kind, tile_m):
         pu = bufs[r]["plan_used"]
         assert pu.comm_ctas == 8 and pu.sm_gemm == torch.cuda.get_device_properties(0).multi_processor_count - 16
     assert_close(y, ref["y"], f"EP{D} N{N}")
+
+
+@pytest.mark.parametrize("D,N", [(2, 2), (4, 1)])
+def test_fp8_dispatch_ep_equals_ep1_and_oracle(D, N):
+    """NEXT-2: FP8 dispatch payload (packed e4m3 rows + block exponents over the
+    transport, dequantised per chunk) == the ep = 1 FP8 round trip, bit-exact;
+    y vs the oracle's FP8 contract (R15)."""
+    inp = Inputs(E=8, k=2, H=256, F=256, S=1, Fs=128, T=501, seed=61)
+    y, bufs = _ep_forward(inp, 2, 1, D, make_plan(N, MOE_GEMM_GROUPED), fp8=True)
+    y1 = _ep1_forward(inp, 2, 1, make_plan(1, MOE_GEMM_GROUPED), fp8=True)
+    assert np.array_equal(y, y1)
+    ref = oracle.moe_layer(inp.x, inp.w_router, inp.w_gate, inp.w_up, inp.w_down, k=2, norm_topk=1,
+                           ws_gate_bits=inp.ws_gate, ws_up_bits=inp.ws_up, ws_down_bits=inp.ws_down,
+                           dispatch_fp8=True)
+    same = (ref["idx"] == np.concatenate([b["topk_idx"].cpu().numpy() for b in bufs])).all(axis=1)
+    assert same.mean() > 0.99
+    assert_close(y[same], ref["y"][same], f"fp8 EP{D}")
+    y_bf16 = _ep1_forward(inp, 2, 1, make_plan(1, MOE_GEMM_GROUPED), fp8=False)
+    assert not np.array_equal(y1, y_bf16)              # the payload really was FP8
 
 
 def test_ep_planner_auto_and_skew():
