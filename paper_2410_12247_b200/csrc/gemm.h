@@ -28,6 +28,7 @@ struct GemmArgs {
   int N;                   // logical output columns (F for SWIGLU)
   void* out;               // bf16 or fp32
   int64_t ldo;             // output row pitch in elements
+  int64_t out_rows;        // allocated rows of `out` (TMA store bound; 0 = a_rows)
   const float* bias;       // EPI_F32 only, [N] or nullptr
   int G;                   // groups (<= 256)
   const int32_t* row_start;  // device [G] (nullptr -> single group at row 0)

@@ -33,6 +33,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <cstring>
 #include <mutex>
 
 #include "gemm.h"
@@ -66,6 +67,8 @@ struct KParams {
   int raster_gm;  // tile order inside a group: blocks of raster_gm m-tiles, m fastest inside a block
   int dynamic;    // 1: dynamic tile tickets (tile_counter), 0: static round robin
   int row_mode;   // 0 all rows, 1 bulk (multiple of 256), 2 remainder (see GemmArgs)
+  int diag;       // diagnostics only (EPSMOE_GEMM_DIAG): 1 skip output stores, 2 skip TMEM loads + stores
+  int tma_store;  // bf16 outputs: full 32-row warp slices leave through TMA bulk-tensor stores (tmO)
   int64_t ldo;
   void* out;
   const float* bias;
@@ -89,7 +92,7 @@ struct __align__(8) SmemTail {
   int32_t gstart[MAX_G];
   int32_t gcount[MAX_G];
   alignas(16) int32_t tok[BM];  // GATHER: physical A rows of the current tile (read as int4)
-  alignas(16) uint8_t stage_out[4][32 * 64];   // per epilogue warp: 32 rows x 32 bf16, XOR-swizzled
+  alignas(1024) uint8_t stage_out[4][32 * 64];  // per epilogue warp: 32 rows x 32 bf16, 64-B swizzle
 };
 
 template <int CG>
@@ -109,12 +112,29 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
 // swizzled smem tile (conflict-free both ways), then 4 lanes write each row's
 // 64 B as two full 32-B sectors (8 rows per instruction) instead of 32
 // scattered 16-B pieces.  Rows >= vr (past the group's end) are not written.
+// The staging layout is exactly TMA's 64-byte swizzle (16-B chunk c of row r at
+// c ^ ((r >> 1) & 3)), so a fully valid 32-row slice leaves as one async
+// bulk-tensor store (tmo: 32 x 32 box, SWIZZLE_64B) instead of 128 STGs.
 __device__ __forceinline__ void store_chunk(const uint32_t (&pk)[16], uint8_t* stg, __nv_bfloat16* out_row0,
-                                            int64_t ldo, int vr, int lane) {
+                                            int64_t ldo, int vr, int lane, const CUtensorMap* tmo, int col,
+                                            int row0) {
+  if (tmo) {  // the previous bulk store from this buffer must have read it
+    if (lane == 0) ptx::bulk_wait_read0();
+    __syncwarp();
+  }
   uint4* srow = reinterpret_cast<uint4*>(stg + lane * 64);
   const int sw = (lane >> 1) & 3;
 #pragma unroll
   for (int j = 0; j < 4; ++j) srow[j ^ sw] = make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
+  if (tmo && vr == 32) {
+    ptx::fence_proxy_async_smem();
+    __syncwarp();
+    if (lane == 0) {
+      ptx::tma_store_2d(tmo, ptx::smem_u32(stg), col, row0);
+      ptx::bulk_commit();
+    }
+    return;
+  }
   __syncwarp();
   const int j = lane & 3;
 #pragma unroll
@@ -215,7 +235,7 @@ struct Tickets {
 template <int EPI, int CG, bool GATHER>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
 gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB0,
-            const __grid_constant__ CUtensorMap tmB1, const KParams p) {
+            const __grid_constant__ CUtensorMap tmB1, const __grid_constant__ CUtensorMap tmO, const KParams p) {
   using C = Cfg<CG>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -413,7 +433,17 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
       const int64_t grow = (int64_t)st.gstart[g] + local_row;
       const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
       // rows of this warp's 32-row slice that belong to the group
-      const int vr = max(0, min(32, st.gcount[g] - (local_row - lane)));
+      const int vr = (p.diag == 1) ? 0 : max(0, min(32, st.gcount[g] - (local_row - lane)));
+      if (p.diag == 2) {
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if constexpr (CG == 1) ptx::mbar_arrive(ptx::smem_u32(&st.tempty[acc]));
+          else ptx::mbar_arrive_cluster_relaxed(acc ? tempty_leader1 : tempty_leader0);
+        }
+        ++iter;
+        continue;
+      }
       uint8_t* stg = st.stage_out[q];
       if (EPI == EPI_SWIGLU) {
         __nv_bfloat16* out0 = reinterpret_cast<__nv_bfloat16*>(p.out) + (grow - lane) * p.ldo + nt * 128;
@@ -429,7 +459,8 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
             float u0 = __uint_as_float(ur[2 * i]), u1 = __uint_as_float(ur[2 * i + 1]);
             pk[i] = pack_bf16(silu_f32(g0) * u0, silu_f32(g1) * u1);
           }
-          store_chunk(pk, stg, out0 + c * 32, p.ldo, vr, lane);
+          store_chunk(pk, stg, out0 + c * 32, p.ldo, vr, lane, p.tma_store ? &tmO : nullptr, nt * 128 + c * 32,
+                      (int)(grow - lane));
         }
       } else if (EPI == EPI_BF16) {
         __nv_bfloat16* out0 = reinterpret_cast<__nv_bfloat16*>(p.out) + (grow - lane) * p.ldo + nt * BN;
@@ -441,7 +472,8 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
           ptx::tmem_wait_ld();
 #pragma unroll
           for (int i = 0; i < 16; ++i) pk[i] = pack_bf16(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1]));
-          store_chunk(pk, stg, out0 + c * 32, p.ldo, vr, lane);
+          store_chunk(pk, stg, out0 + c * 32, p.ldo, vr, lane, p.tma_store ? &tmO : nullptr, nt * BN + c * 32,
+                      (int)(grow - lane));
         }
       } else {
         float* out = reinterpret_cast<float*>(p.out) + grow * p.ldo;
@@ -481,6 +513,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
   if constexpr (CG == 2) ptx::cluster_sync();  // no CTA leaves while its peer may still signal it
   ptx::tc_fence_after();
   if (warp == 1) ptx::tmem_dealloc<TMEM_COLS, CG>(tmem_base);
+  if (warp >= 2 && lane == 0 && p.tma_store) ptx::bulk_wait0();  // output stores complete
   if (p.dynamic && threadIdx.x == 0) {
     // the last CTA to finish resets the ticket counter for the next launch
     __threadfence();
@@ -548,6 +581,20 @@ bool make_tmap(CUtensorMap* m, const void* base, int64_t rows, int K, int box_ro
   return r == CUDA_SUCCESS;
 }
 
+// bf16 output tensor [rows, ld] for the epilogue's bulk stores: 32 x 32 box
+// (one warp's 32 rows x 32 columns), 64-byte swizzle (the staging layout).
+bool make_tmap_out(CUtensorMap* m, void* base, int64_t rows, int64_t ld) {
+  auto enc = get_encode_fn();
+  if (!enc || rows <= 0) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)ld, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
+  cuuint32_t box[2] = {32, 32};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 template <int EPI, int CG, bool GATHER>
 int launch_epi(const GemmArgs& a, cudaStream_t stream) {
   static bool attr_set = false;
@@ -581,6 +628,13 @@ int launch_epi(const GemmArgs& a, cudaStream_t stream) {
   p.row_count = a.row_count;
   p.a_row_index = a.a_row_index;
   p.row_mode = a.row_mode;
+  p.diag = env_int("EPSMOE_GEMM_DIAG", 0);
+  CUtensorMap tO;
+  std::memset(&tO, 0, sizeof(tO));
+  p.tma_store = 0;
+  if (EPI != EPI_F32 && env_int("EPSMOE_TMA_STORE", 1) &&
+      make_tmap_out(&tO, a.out, a.out_rows > 0 ? a.out_rows : a.a_rows, a.ldo))
+    p.tma_store = 1;
   // Launches that may run concurrently must use different counters (caller's).
   p.tile_counter = a.tile_counter ? a.tile_counter : ticket_counter(0);
   p.dynamic = (dynamic_sched() && p.tile_counter) ? 1 : 0;
@@ -599,7 +653,7 @@ int launch_epi(const GemmArgs& a, cudaStream_t stream) {
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, tA, tB0, tB1, p);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, tA, tB0, tB1, tO, p);
   return (int)e;
 }
 

@@ -249,6 +249,7 @@ int compute_moe(moe_layer* L, const void* A, int64_t a_rows, const int32_t* row_
   g1a.N = c.ffn;
   g1a.out = L->h;
   g1a.ldo = c.ffn;
+  g1a.out_rows = L->gemm_rows_cap;
   GemmArgs g2a = base_args(EPI_BF16, num_ctas);
   g2a.cta_pair = cta_pair;
   g2a.tile_counter = L->tickets;
@@ -261,6 +262,7 @@ int compute_moe(moe_layer* L, const void* A, int64_t a_rows, const int32_t* row_
   g2a.N = c.hidden;
   g2a.out = L->o;
   g2a.ldo = c.hidden;
+  g2a.out_rows = L->gemm_rows_cap;
   // CTA-pair tiles cover each expert's first floor(M/256)*256 rows; with
   // split_rem the remaining < 256 rows go to a second launch on 128-row
   // single-CTA tiles (halves the M padding: ~64 instead of ~128 rows/expert).
