@@ -144,7 +144,9 @@ typedef struct {
   int32_t* pos;             /* out [T_loc, topk]: send row of pair (t, j)     */
   int32_t* hist;            /* out [e]: this rank's pairs per expert          */
   int32_t* seg_start;       /* out [e+1]: send-layout expert offsets (R6)     */
-  void* shared_out;         /* out [T_loc, k] bf16: shared-expert output s    */
+  void* shared_out;         /* out [T_loc, H] bf16: shared-expert output s
+                               (requesting it disables the ep = 1 fused
+                               shared-DownGemm + combine kernel)             */
   int32_t* global_hist_host;/* out HOST [ep, e]                               */
   moe_plan_t* plan_used;    /* out HOST: the plan the forward executed        */
 } moe_debug_t;

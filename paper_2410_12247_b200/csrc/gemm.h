@@ -9,6 +9,8 @@ enum EpiKind : int {
   EPI_SWIGLU = 0,  // acc = [gate(128) | up(128)] -> h = bf16(silu(g) * u)   (GateUpGemm+SiluAct)
   EPI_BF16 = 1,    // acc -> bf16                                             (DownGemm)
   EPI_F32 = 2,     // acc (+ bias[col]) -> fp32                               (Router)
+  EPI_COMBINE = 3, // shared DownGemm fused with K7: s = bf16(acc);
+                   // y = bf16(fmaf chain over slots j of w_j * o[pos[t][j]] on fp32(s))
 };
 
 // One grouped GEMM launch: for each group g (an expert), rows
@@ -42,6 +44,12 @@ struct GemmArgs {
                                // that may run concurrently need distinct counters (nullptr = shared)
   int row_mode;                // 0: all rows of each group; 1: only the first floor(n/256)*256 rows
                                // (bulk); 2: only the rows after them (remainder, < 256)
+  // EPI_COMBINE only (single dense group, row = token t): routed expert outputs
+  // o [*, N] bf16, pos [rows, comb_k] int32 rows of o, w [rows, comb_k] fp32.
+  const void* comb_o;
+  const int32_t* comb_pos;
+  const float* comb_w;
+  int comb_k;                  // 1..8
 };
 
 // Launch on `stream`.  Returns a cudaError_t-compatible code (0 = success).

@@ -16,6 +16,10 @@
 //        boxes; no weight repacking); epilogue h = bf16(silu(g) * u).
 //   DownGemm                  EPI_BF16:  o = bf16(acc).
 //   Router                    EPI_F32:   logits = fp32(acc) + beta.
+//   shared DownGemm + K7 combine      EPI_COMBINE: s = bf16(acc), then the
+//        weighted unpermute y = bf16(fmaf_j(w_j, o[pos[t][j]], fp32(s))) in slot
+//        order (R4) while the tensor core computes the next tile: the combine's
+//        HBM stream hides under a compute-bound GEMM instead of running alone.
 //
 // Tile scheduling: tiles are numbered group-major (expert), then in blocks of
 // RASTER m-tiles (n-major across a block) so that tiles in flight together
@@ -76,7 +80,30 @@ struct KParams {
   const int32_t* row_count;
   const int32_t* a_row_index;
   int32_t* tile_counter;  // [2]: next ticket, CTAs finished (reset by the last CTA)
+  const __nv_bfloat16* comb_o;  // EPI_COMBINE (see GemmArgs)
+  const int32_t* comb_pos;
+  const float* comb_w;
+  int comb_k;
 };
+
+constexpr int COMB_MAX_K = 8;
+
+__device__ __forceinline__ uint64_t evict_first_policy() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+// o rows are read once: L2 evict-first, L1-allocating (a lane's four 16-B
+// pieces share two 32-B sectors)
+__device__ __forceinline__ uint4 ld_once(const void* ptr, uint64_t pol) {
+  uint4 r;
+  asm volatile("ld.global.nc.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(ptr), "l"(pol));
+  return r;
+}
+__device__ __forceinline__ float bf16_lo(uint32_t v) { return __uint_as_float(v << 16); }
+__device__ __forceinline__ float bf16_hi(uint32_t v) { return __uint_as_float(v & 0xffff0000u); }
 
 template <int CG>
 struct __align__(8) SmemTail {
@@ -93,6 +120,8 @@ struct __align__(8) SmemTail {
   int32_t gcount[MAX_G];
   alignas(16) int32_t tok[BM];  // GATHER: physical A rows of the current tile (read as int4)
   alignas(1024) uint8_t stage_out[4][32 * 64];  // per epilogue warp: 32 rows x 32 bf16, 64-B swizzle
+  int32_t comb_pos[4][32 * 8];                   // EPI_COMBINE: per epilogue warp, its rows' pos / w
+  float comb_w[4][32 * 8];
 };
 
 template <int CG>
@@ -115,10 +144,8 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
 // The staging layout is exactly TMA's 64-byte swizzle (16-B chunk c of row r at
 // c ^ ((r >> 1) & 3)), so a fully valid 32-row slice leaves as one async
 // bulk-tensor store (tmo: 32 x 32 box, SWIZZLE_64B) instead of 128 STGs.
-__device__ __forceinline__ void store_chunk(const uint32_t (&pk)[16], uint8_t* stg, __nv_bfloat16* out_row0,
-                                            int64_t ldo, int vr, int lane, const CUtensorMap* tmo, int col,
-                                            int row0) {
-  if (tmo) {  // the previous bulk store from this buffer must have read it
+__device__ __forceinline__ void stage_write(const uint32_t (&pk)[16], uint8_t* stg, int lane, bool tma) {
+  if (tma) {  // the previous bulk store from this buffer must have read it
     if (lane == 0) ptx::bulk_wait_read0();
     __syncwarp();
   }
@@ -126,6 +153,13 @@ __device__ __forceinline__ void store_chunk(const uint32_t (&pk)[16], uint8_t* s
   const int sw = (lane >> 1) & 3;
 #pragma unroll
   for (int j = 0; j < 4; ++j) srow[j ^ sw] = make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
+}
+// 16-B piece jq of staged row r (row-major view: 4 lanes per row, 8 rows per pass)
+__device__ __forceinline__ uint4* stage_piece(uint8_t* stg, int r, int jq) {
+  return reinterpret_cast<uint4*>(stg + r * 64) + (jq ^ ((r >> 1) & 3));
+}
+__device__ __forceinline__ void stage_flush(uint8_t* stg, __nv_bfloat16* out_row0, int64_t ldo, int vr, int lane,
+                                            const CUtensorMap* tmo, int col, int row0) {
   if (tmo && vr == 32) {
     ptx::fence_proxy_async_smem();
     __syncwarp();
@@ -140,10 +174,16 @@ __device__ __forceinline__ void store_chunk(const uint32_t (&pk)[16], uint8_t* s
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const int r = i * 8 + (lane >> 2);
-    const uint4 v = reinterpret_cast<const uint4*>(stg + r * 64)[j ^ ((r >> 1) & 3)];
+    const uint4 v = *stage_piece(stg, r, j);
     if (r < vr) reinterpret_cast<uint4*>(out_row0 + (int64_t)r * ldo)[j] = v;
   }
   __syncwarp();
+}
+__device__ __forceinline__ void store_chunk(const uint32_t (&pk)[16], uint8_t* stg, __nv_bfloat16* out_row0,
+                                            int64_t ldo, int vr, int lane, const CUtensorMap* tmo, int col,
+                                            int row0) {
+  stage_write(pk, stg, lane, tmo != nullptr);
+  stage_flush(stg, out_row0, ldo, vr, lane, tmo, col, row0);
 }
 
 // Linear tile index -> (group, m-tile, n-tile).  Inside a group, tiles are
@@ -475,6 +515,76 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
           store_chunk(pk, stg, out0 + c * 32, p.ldo, vr, lane, p.tma_store ? &tmO : nullptr, nt * BN + c * 32,
                       (int)(grow - lane));
         }
+      } else if (EPI == EPI_COMBINE) {
+        // s = bf16(acc) is staged row-major in smem; the weighted unpermute then
+        // runs with 4 lanes per row so each o row piece is one contiguous 64-B
+        // read (8 rows per instruction) instead of 32 scattered 16-B pieces.
+        __nv_bfloat16* out0 = reinterpret_cast<__nv_bfloat16*>(p.out) + (grow - lane) * p.ldo + nt * BN;
+        const int kk = p.comb_k;
+        const uint64_t pol = evict_first_policy();
+        int32_t* cpos = st.comb_pos[q];
+        float* cw = st.comb_w[q];
+        __syncwarp();  // previous tile's readers are done
+#pragma unroll
+        for (int j = 0; j < COMB_MAX_K; ++j) {
+          if (j < kk) {
+            cpos[lane * COMB_MAX_K + j] = valid ? p.comb_pos[grow * kk + j] : 0;
+            cw[lane * COMB_MAX_K + j] = valid ? p.comb_w[grow * kk + j] : 0.f;
+          }
+        }
+        __syncwarp();
+        const int jq = lane & 3;
+#pragma unroll 1
+        for (int c = 0; c < BN / 32; ++c) {
+          const int col0 = nt * BN + c * 32;
+          if (col0 >= p.N) break;  // N is a multiple of 32 (warp-uniform)
+          // the k expert-output pieces of this lane's 4 rows in flight before the TMEM read
+          uint4 ov[4][COMB_MAX_K];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int r = i * 8 + (lane >> 2);
+#pragma unroll
+            for (int j = 0; j < COMB_MAX_K; ++j)
+              ov[i][j] = (r < vr && j < kk)
+                             ? ld_once(p.comb_o + (int64_t)cpos[r * COMB_MAX_K + j] * p.N + col0 + 8 * jq, pol)
+                             : make_uint4(0, 0, 0, 0);
+          }
+          uint32_t rr[32], pk[16];
+          ptx::tmem_ld32(taddr + c * 32, rr);
+          ptx::tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 16; ++i) pk[i] = pack_bf16(__uint_as_float(rr[2 * i]), __uint_as_float(rr[2 * i + 1]));
+          stage_write(pk, stg, lane, p.tma_store != 0);  // s = bf16(acc)
+          __syncwarp();
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int r = i * 8 + (lane >> 2);
+            uint4* sp = stage_piece(stg, r, jq);
+            const uint4 sv = *sp;
+            const uint32_t s4[4] = {sv.x, sv.y, sv.z, sv.w};
+            float a[8];
+#pragma unroll
+            for (int h = 0; h < 4; ++h) {
+              a[2 * h] = bf16_lo(s4[h]);
+              a[2 * h + 1] = bf16_hi(s4[h]);
+            }
+#pragma unroll
+            for (int j = 0; j < COMB_MAX_K; ++j) {
+              if (j < kk) {
+                const float w = cw[r * COMB_MAX_K + j];
+                const uint32_t o4[4] = {ov[i][j].x, ov[i][j].y, ov[i][j].z, ov[i][j].w};
+#pragma unroll
+                for (int h = 0; h < 4; ++h) {
+                  a[2 * h] = __fmaf_rn(w, bf16_lo(o4[h]), a[2 * h]);
+                  a[2 * h + 1] = __fmaf_rn(w, bf16_hi(o4[h]), a[2 * h + 1]);
+                }
+              }
+            }
+            *sp = make_uint4(pack_bf16(a[0], a[1]), pack_bf16(a[2], a[3]), pack_bf16(a[4], a[5]),
+                             pack_bf16(a[6], a[7]));
+          }
+          stage_flush(stg, out0 + c * 32, p.ldo, vr, lane, p.tma_store ? &tmO : nullptr, col0, (int)(grow - lane));
+        }
       } else {
         float* out = reinterpret_cast<float*>(p.out) + grow * p.ldo;
 #pragma unroll 1
@@ -628,6 +738,10 @@ int launch_epi(const GemmArgs& a, cudaStream_t stream) {
   p.row_count = a.row_count;
   p.a_row_index = a.a_row_index;
   p.row_mode = a.row_mode;
+  p.comb_o = reinterpret_cast<const __nv_bfloat16*>(a.comb_o);
+  p.comb_pos = a.comb_pos;
+  p.comb_w = a.comb_w;
+  p.comb_k = a.comb_k;
   p.diag = env_int("EPSMOE_GEMM_DIAG", 0);
   CUtensorMap tO;
   std::memset(&tO, 0, sizeof(tO));
@@ -664,6 +778,7 @@ int launch_cg(const GemmArgs& a, cudaStream_t stream) {
       return a.a_row_index ? launch_epi<EPI_SWIGLU, CG, true>(a, stream) : launch_epi<EPI_SWIGLU, CG, false>(a, stream);
     case EPI_BF16: return launch_epi<EPI_BF16, CG, false>(a, stream);
     case EPI_F32: return launch_epi<EPI_F32, CG, false>(a, stream);
+    case EPI_COMBINE: return launch_epi<EPI_COMBINE, CG, false>(a, stream);
   }
   return (int)cudaErrorInvalidValue;
 }
@@ -672,6 +787,9 @@ int launch_cg(const GemmArgs& a, cudaStream_t stream) {
 
 int gemm_launch(const GemmArgs& a, cudaStream_t stream) {
   if (a.K % BK != 0 || a.K <= 0 || a.G < 1 || a.G > MAX_G || a.num_ctas < 1) return (int)cudaErrorInvalidValue;
+  if (a.epi == EPI_COMBINE && (!a.comb_o || !a.comb_pos || !a.comb_w || a.comb_k < 1 || a.comb_k > COMB_MAX_K ||
+                               a.G != 1 || a.row_start || a.N % 32))
+    return (int)cudaErrorInvalidValue;
   if (a.row_count == nullptr && a.m_single <= 0) return 0;
   return a.cta_pair ? launch_cg<2>(a, stream) : launch_cg<1>(a, stream);
 }

@@ -50,6 +50,16 @@ struct moe_layer {
   cudaStream_t s_h2d = nullptr, s_d2h = nullptr;  // forward_host copy streams
   cudaEvent_t ev_host_start = nullptr, ev_in[4] = {}, ev_out[4] = {};
   cudaEvent_t ev_router = nullptr, ev_shared = nullptr;
+  // ep == 1 with shared experts, how the shared DownGemm meets the combine
+  // (EPSMOE_FUSE_COMBINE): 0 in order (default); 1 one kernel (EPI_COMBINE
+  // epilogue); 2 token pieces, piece p's combine on s_side concurrent with piece
+  // p+1's DownGemm.  All three are bit-identical.  Measured on dsv2 (B200,
+  // power-capped): 1 is 0.6 ms slower (the epilogue's random 64-B o-row reads
+  // outlast the MMA of the next tile), 2 is a wash (the co-running HBM stream
+  // lowers the GEMM's clock by as much as it hides).
+  int fuse_combine = 0;
+  static constexpr int COMB_PIECES = 4;
+  cudaEvent_t ev_piece[COMB_PIECES] = {};
   bool overlap_shared = true;     // shared experts on s_side, concurrent with routing (EPSMOE_OVERLAP_SHARED=0: in order)
   bool split_rem = false;         // EPSMOE_SPLIT_REM=1: expert GEMMs as bulk on CTA pairs + remainder rows on
                                   // single CTAs; measured 1-3% slower than padding (DSv2, Mixtral), so off
@@ -396,6 +406,7 @@ static moe_status_t create_impl(const moe_config_t* cfg, const moe_weights_t* w,
   }
   default_cost_model(L->cfg, &L->cost);
   if (const char* ov = std::getenv("EPSMOE_OVERLAP_SHARED")) L->overlap_shared = std::atoi(ov) != 0;
+  if (const char* fc = std::getenv("EPSMOE_FUSE_COMBINE")) L->fuse_combine = std::atoi(fc);
   if (const char* gv = std::getenv("EPSMOE_GATHER")) L->gather_a = std::atoi(gv) != 0;
   if (const char* sv = std::getenv("EPSMOE_SPLIT_REM")) L->split_rem = std::atoi(sv) != 0;
   if (cfg->ep > 1) {
@@ -420,6 +431,11 @@ static moe_status_t create_impl(const moe_config_t* cfg, const moe_weights_t* w,
     set_error("side stream creation failed");
     return fail(MOE_ERR_CUDA);
   }
+  for (auto& e : L->ev_piece)
+    if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) {
+      set_error("event creation failed");
+      return fail(MOE_ERR_CUDA);
+    }
   if (cfg->ep > 1) {
     if (cudaStreamCreateWithFlags(&L->s_disp, cudaStreamNonBlocking) != cudaSuccess ||
         cudaStreamCreateWithFlags(&L->s_comb, cudaStreamNonBlocking) != cudaSuccess ||
@@ -504,6 +520,8 @@ moe_status_t moe_layer_destroy(moe_layer_t* L) {
     if (L->ev_out[i]) cudaEventDestroy(L->ev_out[i]);
   }
   for (cudaEvent_t e : {L->ev_router, L->ev_shared})
+    if (e) cudaEventDestroy(e);
+  for (cudaEvent_t e : L->ev_piece)
     if (e) cudaEventDestroy(e);
   if (L->s_comb) cudaStreamDestroy(L->s_comb);
   for (cudaEvent_t e : {L->ev_hist, L->ev_ready, L->ev_comb_done})
@@ -661,6 +679,10 @@ moe_status_t moe_layer_forward(moe_layer_t* L, const void* x, int64_t T, void* y
   // Shared experts depend only on x: they run on s_side, concurrently
   // with topKGating / split (HBM-bound kernels that co-reside with the GEMM's
   // CTAs) and, for ep > 1, with the count exchange, host wait and dispatch(0).
+  // ep == 1: the shared DownGemm is deferred and fused with the combine
+  // (EPI_COMBINE), so only GateUp runs here.
+  // (a debug request for s materialises it: unfused path)
+  const int fuse = ((D == 1) && L->SF && T > 0 && !(dbg && dbg->shared_out)) ? L->fuse_combine : 0;
   auto shared_experts = [&](cudaStream_t ss) -> int {
     if (!L->SF || T == 0) return 0;
     int q0 = prof_rec(L, ss);
@@ -679,6 +701,10 @@ moe_status_t moe_layer_forward(moe_layer_t* L, const void* x, int64_t T, void* y
     int e = gemm_launch(a, ss);
     if (e) return e;
     ++L->last_launches;
+    if (fuse) {
+      prof_mark(L, MOE_STAGE_SHARED, q0, prof_rec(L, ss));
+      return 0;
+    }
     GemmArgs b = base_args(EPI_BF16, num_ctas);
     b.A = L->hs;
     b.a_rows = T;
@@ -746,7 +772,57 @@ moe_status_t moe_layer_forward(moe_layer_t* L, const void* x, int64_t T, void* y
       }
     }
     int c0 = prof_rec(L, st);
-    KERNEL_TRY(launch_combine(L->o, L->SF ? L->s : nullptr, (int)T, H, k, L->pos, topk_w, y, st));
+    if (fuse == 2) {
+      // shared DownGemm in token pieces; piece p's combine (HBM-bound) runs on
+      // s_side next to piece p+1's DownGemm (compute-bound) on the other SMs' slack
+      const int P = (T >= 8192) ? moe_layer::COMB_PIECES : 1;
+      for (int pc = 0; pc < P; ++pc) {
+        const int64_t t0 = T * pc / P, t1 = T * (pc + 1) / P;
+        if (t1 == t0) continue;
+        GemmArgs b = base_args(EPI_BF16, num_ctas);
+        b.A = static_cast<const uint16_t*>(L->hs) + t0 * L->SF;
+        b.a_rows = t1 - t0;
+        b.B0 = L->w.ws_down;
+        b.b_rows = H;
+        b.K = L->SF;
+        b.N = H;
+        b.out = static_cast<uint16_t*>(L->s) + t0 * H;
+        b.ldo = H;
+        b.m_single = (int)(t1 - t0);
+        b.tile_counter = L->tickets;
+        int e = gemm_launch(b, st);
+        if (e) { set_error(std::string("shared DownGemm: ") + cudaGetErrorString((cudaError_t)e)); return MOE_ERR_CUDA; }
+        ++L->last_launches;
+        CUDA_TRY(cudaEventRecord(L->ev_piece[pc], st));
+        CUDA_TRY(cudaStreamWaitEvent(L->s_side, L->ev_piece[pc], 0));
+        KERNEL_TRY(launch_combine(L->o, static_cast<const uint16_t*>(L->s) + t0 * H, (int)(t1 - t0), H, k, L->pos + t0 * k, topk_w + t0 * k,
+                                  reinterpret_cast<uint16_t*>(y) + t0 * H, L->s_side));
+      }
+      CUDA_TRY(cudaEventRecord(L->ev_shared, L->s_side));
+      CUDA_TRY(cudaStreamWaitEvent(st, L->ev_shared, 0));
+    } else if (fuse == 1) {
+      // shared DownGemm + K7 in one kernel: y = bf16(fmaf_j(w_j, o[pos[t][j]], fp32(bf16(hs W_sdown^T))))
+      GemmArgs b = base_args(EPI_COMBINE, num_ctas);
+      b.A = L->hs;
+      b.a_rows = T;
+      b.B0 = L->w.ws_down;
+      b.b_rows = H;
+      b.K = L->SF;
+      b.N = H;
+      b.out = y;
+      b.ldo = H;
+      b.m_single = (int)T;
+      b.tile_counter = L->tickets;
+      b.comb_o = L->o;
+      b.comb_pos = L->pos;
+      b.comb_w = topk_w;
+      b.comb_k = k;
+      int e = gemm_launch(b, st);
+      if (e) { set_error(std::string("shared DownGemm + combine: ") + cudaGetErrorString((cudaError_t)e)); return MOE_ERR_CUDA; }
+      ++L->last_launches;
+    } else {
+      KERNEL_TRY(launch_combine(L->o, L->SF ? L->s : nullptr, (int)T, H, k, L->pos, topk_w, y, st));
+    }
     prof_mark(L, MOE_STAGE_COMBINE, c0, prof_rec(L, st));
   } else {
     // ---- EP > 1: count exchange (C3), plan, chunked dispatch / compute / combine

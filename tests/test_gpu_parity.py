@@ -288,3 +288,28 @@ def test_forward_host_matches_device():
     L.forward_host(xh, yh)
     torch.cuda.synchronize()
     assert torch.equal(yh, y.cpu())
+
+
+@pytest.mark.parametrize("name,T", [("mid_shared", 1000), ("e160_k6", 700), ("e160_k6", 9000)])
+def test_fused_shared_down_combine_equals_unfused(name, T, monkeypatch):
+    """ep == 1 with shared experts: the shared DownGemm with the K7 combine in
+    its epilogue (EPI_COMBINE, mode 1) and the token-piece overlap (mode 2) ==
+    shared DownGemm -> s -> combine kernel (mode 0), bit for bit (same bf16
+    rounding of s, same slot-order fmaf chain, R4); T = 9000 takes the
+    side-stream and 4-piece paths.  y vs the oracle as well."""
+    kw, k, norm = CASES[name]
+    kw = dict(kw, T=T)
+    inp = Inputs(seed=23, grid=True, **kw)
+    x = dev_bf16(inp.x)
+    ys = []
+    for f in ("0", "1", "2"):
+        monkeypatch.setenv("EPSMOE_FUSE_COMBINE", f)
+        L = layer_from_inputs(inp, k, norm)
+        ys.append(L.forward(x).clone())
+        torch.cuda.synchronize()
+        L.close()
+    assert torch.equal(ys[0], ys[1]) and torch.equal(ys[0], ys[2])
+    if T <= 1000:
+        ref = oracle.moe_layer(inp.x, inp.w_router, inp.w_gate, inp.w_up, inp.w_down, k=k, norm_topk=norm,
+                               ws_gate_bits=inp.ws_gate, ws_up_bits=inp.ws_up, ws_down_bits=inp.ws_down)
+        assert_close(to_f32(ys[1]), ref["y"], name + " fused")
