@@ -21,6 +21,7 @@ integer artefacts (histograms, counts, offsets, permutation) are defined too:
     m <- count(input) ; tensor[] <- split(...)   dispatch_layout
     All2All / ComputeMoE / All2All per chunk     expert_ffn on each chunk's rows
     LocalReduce (home-side weighted sum, R7)     combine
+    or expert-side LocalReduce + dedup (R16)     lr_layout, local_reduce_combine
 
 Two numeric modes (R4):
   * "exact":    fp64 everywhere, no intermediate rounding;
@@ -337,6 +338,109 @@ def combine(s, o_slots, w, mode="contract"):
 
 
 # ----------------------------------------------------------------------------
+# NEXT-3 / R16: expert-side LocalReduce with per-(token, destination, chunk)
+# dedup.  ComputeMoE ends with LocalReduce(tensor) on the expert side
+# (P:559); fig:comp_overlap_comm and P:365 place it before the second
+# all2all, which it overlaps.  So each token travels once per (destination
+# rank, chunk) and returns as one partial sum of its experts there.
+# ----------------------------------------------------------------------------
+
+
+def lr_group_ids(idx, E, D, N):
+    """Group of pair (t, j): g = c * D + d, with d = e // E_loc the rank owning
+    e = idx[t, j] (EP) and c the chunk holding e's local id e % E_loc
+    (balanced contiguous groups of local experts, R8)."""
+    E_loc = E // D
+    gb = chunk_groups(E_loc, N)
+    chunk_of = np.searchsorted(gb, np.arange(E_loc), side="right") - 1
+    idx = np.asarray(idx, np.int64)
+    return chunk_of[idx % E_loc] * D + idx // E_loc
+
+
+def lr_layout(idx, E, D, N):
+    """Dedup all2all layout (R16), per rank r of the token shards (R12):
+
+      gid[r]     [T_loc, k]  group of each pair (lr_group_ids)
+      u_hist[r]  [G]         rows r sends for group g = c*D + d: the distinct
+                             tokens of r with a pair in g (to rank d, chunk c)
+      u_start[r] [G+1]       send rows ordered by (g asc, t asc)
+      posg[r]    [T_loc, k]  send row of t's i-th distinct group (groups in
+                             ascending g), -1 past the token's group count
+      recv_u_start[d] [N, D] first row, in d's receive buffer ordered by
+                             (c asc, src asc, t asc), of what src sends d in c
+    G = N * D."""
+    T, k = idx.shape
+    E_loc = E // D
+    G = N * D
+    start = token_shards(T, D)
+    gid_all = lr_group_ids(idx, E, D, N)
+    gid, u_hist, u_start, posg = [], np.zeros((D, G), np.int64), np.zeros((D, G + 1), np.int64), []
+    for r in range(D):
+        gr = gid_all[start[r]:start[r + 1]]
+        T_loc = gr.shape[0]
+        for g in range(G):
+            u_hist[r, g] = int(np.count_nonzero((gr == g).any(axis=1)))
+        u_start[r, 1:] = np.cumsum(u_hist[r])
+        nxt = u_start[r, :G].copy()
+        pg = np.full((T_loc, k), -1, np.int64)
+        for t in range(T_loc):                 # token order => stable within g
+            for i, g in enumerate(sorted(set(int(v) for v in gr[t]))):
+                pg[t, i] = nxt[g]
+                nxt[g] += 1
+        gid.append(gr)
+        posg.append(pg)
+    recv_u_start = np.zeros((D, N, D), np.int64)
+    for d in range(D):
+        row = 0
+        for c in range(N):
+            for src in range(D):
+                recv_u_start[d, c, src] = row
+                row += u_hist[src, c * D + d]
+    return dict(gid=gid, u_hist=u_hist, u_start=u_start, posg=posg, recv_u_start=recv_u_start,
+                token_start=start, E_loc=E_loc)
+
+
+def local_reduce_combine(s, o_slots, w, gid, mode="contract"):
+    """y under R16.  Expert side, per distinct group g of token t:
+        acc = 0; for j ascending with gid[t, j] == g: acc = fmaf(w_j, o_{t,j}, acc);
+        p_{t,g} = bf16(acc)                                (LocalReduce, P:559)
+    home side, after all2all_combine:
+        acc = fp32(s_t); for g ascending: acc = acc + p_{t,g}; y_t = bf16(acc).
+    exact: y = s + sum_g sum_{j in g} w_j o_j in fp64.  o_slots: [T,k,H]."""
+    T, k, H = o_slots.shape
+    gid = np.asarray(gid, np.int64)
+    gs = np.sort(gid, axis=1)
+    distinct = np.ones_like(gs, dtype=bool)
+    distinct[:, 1:] = gs[:, 1:] != gs[:, :-1]
+    if mode == "exact":
+        y = np.array(s, dtype=np.float64, copy=True)
+        for i in range(k):
+            for t in np.nonzero(distinct[:, i])[0]:
+                part = np.zeros(H)
+                for j in range(k):
+                    if gid[t, j] == gs[t, i]:
+                        part = part + float(w[t, j]) * o_slots[t, j]
+                y[t] = y[t] + part
+        return y
+    acc = np.asarray(s, np.float32).copy()
+    for i in range(k):                      # i-th slot of the sorted group list
+        rows = np.nonzero(distinct[:, i])[0]
+        if rows.size == 0:
+            continue
+        g = gs[rows, i]
+        part = np.zeros((rows.size, H), np.float32)
+        for j in range(k):                  # slot order inside the group
+            m = gid[rows, j] == g
+            if m.any():
+                rj = rows[m]
+                part[m] = fmaf(np.broadcast_to(np.asarray(w, np.float32)[rj, j][:, None], (rj.size, H)),
+                               o_slots[rj, j, :], part[m])
+        p = round_bf16(part)                # the combine payload is bf16
+        acc[rows] = (acc[rows] + p).astype(np.float32)
+    return round_bf16(acc)
+
+
+# ----------------------------------------------------------------------------
 # The layer (Algorithm 1, P:561-583), simulated over D ranks and PN chunks.
 # ----------------------------------------------------------------------------
 
@@ -344,12 +448,15 @@ def combine(s, o_slots, w, mode="contract"):
 def moe_layer(x_bits, w_router_bits, w_gate_bits, w_up_bits, w_down_bits, k, norm_topk,
               ws_gate_bits=None, ws_up_bits=None, ws_down_bits=None, router_bias=None,
               routed_scale=1.0, D=1, N=1, token_slices=1, mode="contract",
-              topk_override=None, dispatch_fp8=False):
+              topk_override=None, dispatch_fp8=False, local_reduce=False):
     """Full layer over all T tokens.  Weights are indexed by global expert id.
 
     topk_override = (idx, w) replaces Router + topKGating (explicit routing,
     used by the fig:eps_overview fixture).  dispatch_fp8: every dispatched row
     travels as FP8 (fp8_dispatch_roundtrip, R15); shared experts see x.
+    local_reduce: expert-side LocalReduce with per-(token, destination,
+    chunk) dedup (R16): the rows each expert sees are unchanged, only the sum
+    is regrouped (local_reduce_combine); the result adds the dedup layout.
     """
     T, H = x_bits.shape
     E = w_gate_bits.shape[0]
@@ -414,10 +521,17 @@ def moe_layer(x_bits, w_router_bits, w_gate_bits, w_up_bits, w_down_bits, k, nor
     for r in range(D):
         p = lay["pos"][r]
         o_slots[start[r]:start[r + 1]] = comb[r][p]
-    y = combine(s, o_slots, w, mode)
-    return dict(logits=logits, idx=idx, w=w, y=y, s=s, layout=lay,
-                send_counts=chunk_send_counts(lay["hist"], E, D, N, token_slices, idx),
-                group_begin=gb)
+    out = dict(logits=logits, idx=idx, w=w, s=s, layout=lay,
+               send_counts=chunk_send_counts(lay["hist"], E, D, N, token_slices, idx), group_begin=gb)
+    if local_reduce:
+        if token_slices != 1:
+            raise ValueError("local_reduce: token_slices must be 1")
+        lr = lr_layout(idx, E, D, N)
+        out["lr_layout"] = lr
+        out["y"] = local_reduce_combine(s, o_slots, w, np.concatenate(lr["gid"]), mode)
+    else:
+        out["y"] = combine(s, o_slots, w, mode)
+    return out
 
 
 def moe_tokens(x_bits, w_router_bits, expert_weights, k, norm_topk, shared=None,

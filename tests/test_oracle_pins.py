@@ -392,3 +392,107 @@ def test_pn_grid_within_one_of_closed_form():
     assert oracle.pn_optimum_grid(3.0, 5.0, 0.0, 0.2, 20)[0] == 20
     # small C (few tokens) -> no gain from pipelining -> N = 1
     assert oracle.pn_optimum_grid(0.01, 0.01, 0.05, 0.0, 20)[0] == 1
+
+
+# --------------------------------------------------------------------------
+# 8. Expert-side LocalReduce with per-(token, destination, chunk) dedup
+#    (NEXT-3, R16)
+# --------------------------------------------------------------------------
+
+def test_local_reduce_fixture_counts_by_hand():
+    """fig:eps_overview routing (F-8a completion).  N = 1: rank 0
+    sends rank 0 tokens {0,1,2,4} (t0: e0,e1 and t2: e1,e2 merge) and rank 1
+    tokens {1,3,4} (t3: e3,e4 merge); rank 1 sends rank 0 {5,6,8,9} and rank 1
+    {6,7,8,9}: 15 rows instead of 20 pairs.  N = 3 (chunk = local expert):
+    every (token, rank, chunk) holds one pair, so no row is saved."""
+    fx = json.load(open(os.path.join(GOLDEN, "fig_eps_overview.json")))
+    idx = np.array(fx["routing"])
+    lay1 = oracle.lr_layout(idx, 6, 2, 1)
+    assert lay1["u_hist"].tolist() == [[4, 3], [4, 4]]
+    # rank 0's send rows, (g asc, t asc): g0 = {0,1,2,4}, g1 = {1,3,4}
+    assert lay1["posg"][0].tolist() == [[0, -1], [1, 4], [2, -1], [5, -1], [3, 6]]
+    assert lay1["recv_u_start"][1].tolist() == [[0, 3]]
+    lay3 = oracle.lr_layout(idx, 6, 2, 3)
+    ref = oracle.dispatch_layout(idx, 6, 2)
+    assert lay3["u_hist"].sum() == 20
+    # g = c*D + d with c = local expert id: u_hist[r][c*2+d] = pairs of r to expert d*3+c
+    for r in range(2):
+        for c in range(3):
+            for d in range(2):
+                assert lay3["u_hist"][r, c * 2 + d] == ref["hist"][r, d * 3 + c]
+
+
+def test_local_reduce_exact_mode_equals_plain_sum():
+    """In exact arithmetic regrouping the sum changes nothing: R16's y equals
+    the plain layer's y to fp64 rounding for any (D, N).  A dropped, doubled
+    or mis-weighted pair in the grouping fails this."""
+    inp = _tiny(T=48)
+    args = (inp.x, inp.w_router, inp.w_gate, inp.w_up, inp.w_down)
+    kw = dict(k=2, norm_topk=0, ws_gate_bits=inp.ws_gate, ws_up_bits=inp.ws_up, ws_down_bits=inp.ws_down,
+              mode="exact")
+    base = oracle.moe_layer(*args, **kw)["y"]
+    for D, N in [(1, 1), (1, 4), (2, 1), (2, 3), (4, 2), (8, 1)]:
+        y = oracle.moe_layer(*args, D=D, N=N, local_reduce=True, **kw)["y"]
+        assert np.allclose(y, base, rtol=1e-12, atol=1e-12 * np.abs(base).max()), (D, N)
+
+
+def test_local_reduce_single_group_without_shared_is_plain_contract():
+    """D = 1, N = 1, no shared experts: every token is one group, so
+    y = bf16(0 + bf16(fmaf chain)) = bf16(fmaf chain) = the plain contract."""
+    inp = Inputs(E=8, k=3, H=32, F=64, T=50, seed=8)
+    args = (inp.x, inp.w_router, inp.w_gate, inp.w_up, inp.w_down)
+    a = oracle.moe_layer(*args, k=3, norm_topk=1)["y"]
+    b = oracle.moe_layer(*args, k=3, norm_topk=1, local_reduce=True)["y"]
+    assert np.array_equal(a, b)
+    c = oracle.moe_layer(*args, k=3, norm_topk=1, D=2, N=2, local_reduce=True)["y"]
+    assert not np.array_equal(a, c)     # several groups: one more bf16 rounding per partial
+
+
+def test_local_reduce_layout_invariants():
+    inp = _tiny(T=70)
+    idx = oracle.topk_gating(oracle.router_logits(inp.x, inp.w_router), 2, 1)[0]
+    for D, N in [(1, 3), (2, 1), (2, 4), (4, 2)]:
+        lay = oracle.lr_layout(idx, 8, D, N)
+        for r in range(D):
+            pg, gid = lay["posg"][r], lay["gid"][r]
+            ng = np.array([len(set(row)) for row in gid.tolist()])
+            assert np.array_equal((pg >= 0).sum(axis=1), ng)
+            # every send row is used by exactly one (token, group)
+            assert sorted(pg[pg >= 0].tolist()) == list(range(int(lay["u_hist"][r].sum())))
+            # rows of group g lie in [u_start[g], u_start[g+1])
+            for t in range(pg.shape[0]):
+                for i, g in enumerate(sorted(set(gid[t].tolist()))):
+                    assert lay["u_start"][r][g] <= pg[t, i] < lay["u_start"][r][g + 1]
+        # receive side is the transpose of the send side
+        for d in range(D):
+            tot = sum(int(lay["u_hist"][src, c * D + d]) for c in range(N) for src in range(D))
+            last = lay["recv_u_start"][d][N - 1][D - 1] + lay["u_hist"][D - 1, (N - 1) * D + d]
+            assert last == tot
+
+
+def test_local_reduce_distinct_devices_closed_form():
+    """With N = 1 a token sends one row per distinct destination rank.  For k
+    distinct experts drawn uniformly from E (E_loc per rank), the expected
+    number of distinct ranks is D (1 - C(E-E_loc, k) / C(E, k))
+    (hypergeometric: a rank is missed iff all k experts avoid its E_loc).
+    DSv2 at EP = 8: E = 160, k = 6 -> 4.4586 rows per token instead of 6."""
+    E, k, D, T = 160, 6, 8, 20000
+    rng = np.random.default_rng(3)
+    idx = np.argsort(rng.random((T, E)), axis=1)[:, :k]
+    lay = oracle.lr_layout(idx, E, D, 1)
+    mean = lay["u_hist"].sum() / T
+    expect = D * (1 - math.comb(E - E // D, k) / math.comb(E, k))
+    assert abs(expect - 4.4586) < 1e-4
+    assert abs(mean - expect) < 0.02     # sd of a token's count < 1, so 3 sd/sqrt(T) < 0.02
+
+
+def test_local_reduce_contract_vs_exact_band():
+    inp = Inputs(E=8, k=4, H=256, F=192, S=1, Fs=128, T=64, seed=4)
+    args = (inp.x, inp.w_router, inp.w_gate, inp.w_up, inp.w_down)
+    kw = dict(k=4, norm_topk=1, ws_gate_bits=inp.ws_gate, ws_up_bits=inp.ws_up, ws_down_bits=inp.ws_down,
+              D=2, N=2, local_reduce=True)
+    ex = oracle.moe_layer(*args, mode="exact", **kw)
+    ct = oracle.moe_layer(*args, mode="contract", **kw)
+    rel = np.abs(ct["y"] - ex["y"]).sum() / np.abs(ex["y"]).sum()
+    assert 3e-4 < rel < 6e-3
+    assert np.array_equal(oracle.round_bf16(ct["y"]), ct["y"])
