@@ -73,6 +73,12 @@ typedef struct {
                            two scale per 128 columns (Table II "FP8", P:312,
                            P:331; NEXT-2, R15); experts see the exact dequant;
                            needs hidden % 128 == 0.  0: bf16 payload.        */
+  int32_t local_reduce; /* 1: expert-side LocalReduce (NEXT-3, R16): a
+                           token travels once per (destination rank, chunk)
+                           and returns as that group's partial sum
+                           p = bf16(sum of w_j o_j in slot order); home side
+                           y = bf16(s + p_g ... in (chunk, rank) order).
+                           0: per-pair transfer, home-side weighted sum (R7). */
 } moe_config_t;
 
 /* Caller-owned device weights (bf16, K-major), valid for the layer's life.
@@ -149,6 +155,11 @@ typedef struct {
                                shared-DownGemm + combine kernel)             */
   int32_t* global_hist_host;/* out HOST [ep, e]                               */
   moe_plan_t* plan_used;    /* out HOST: the plan the forward executed        */
+  int32_t* lr_pos;          /* out [T_loc, topk] (local_reduce, ep > 1): send
+                               row of the token's i-th group (ascending
+                               g = chunk*ep + rank), -1 past its group count */
+  int32_t* lr_hist;         /* out [PN*ep] (local_reduce, ep > 1): send rows
+                               per group g                                   */
 } moe_debug_t;
 
 /* ---------------------------------------------------------------- lifecycle */

@@ -28,7 +28,8 @@ class moe_config_t(C.Structure):
     _fields_ = [("num_experts", C.c_int32), ("top_k", C.c_int32), ("hidden", C.c_int32),
                 ("ffn", C.c_int32), ("num_shared", C.c_int32), ("shared_ffn", C.c_int32),
                 ("ep", C.c_int32), ("rank", C.c_int32), ("max_tokens", C.c_int64),
-                ("norm_topk", C.c_int32), ("routed_scale", C.c_float), ("dispatch_fp8", C.c_int32)]
+                ("norm_topk", C.c_int32), ("routed_scale", C.c_float), ("dispatch_fp8", C.c_int32),
+                ("local_reduce", C.c_int32)]
 
 
 class moe_weights_t(C.Structure):
@@ -65,7 +66,8 @@ class moe_debug_t(C.Structure):
     _fields_ = [("override_routing", C.c_int32), ("logits", C.c_void_p), ("topk_idx", C.c_void_p),
                 ("topk_w", C.c_void_p), ("pos", C.c_void_p), ("hist", C.c_void_p),
                 ("seg_start", C.c_void_p), ("shared_out", C.c_void_p),
-                ("global_hist_host", C.c_void_p), ("plan_used", C.POINTER(moe_plan_t))]
+                ("global_hist_host", C.c_void_p), ("plan_used", C.POINTER(moe_plan_t)),
+                ("lr_pos", C.c_void_p), ("lr_hist", C.c_void_p)]
 
 
 _SIGS = {
@@ -128,8 +130,9 @@ def check(status: int, what: str = "") -> None:
 
 
 def make_config(E, k, H, F, S=0, Fs=0, ep=1, rank=0, max_tokens=1, norm_topk=0, routed_scale=1.0,
-                dispatch_fp8=0):
-    return moe_config_t(E, k, H, F, S, Fs, ep, rank, max_tokens, norm_topk, routed_scale, dispatch_fp8)
+                dispatch_fp8=0, local_reduce=0):
+    return moe_config_t(E, k, H, F, S, Fs, ep, rank, max_tokens, norm_topk, routed_scale, dispatch_fp8,
+                        local_reduce)
 
 
 def plan_compute(cfg: moe_config_t, global_tokens: int, global_hist=None, cost: moe_cost_model_t | None = None):

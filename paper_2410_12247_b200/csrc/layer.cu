@@ -20,6 +20,7 @@
 #include "../../include/epsmoe.h"
 #include "gemm.h"
 #include "internal.h"
+#include "lr.h"
 #include "route.h"
 #include "transport.h"
 
@@ -41,10 +42,15 @@ struct moe_layer {
   void *hs = nullptr, *s = nullptr;
   void *sendq = nullptr, *recvq = nullptr;  // ep > 1 && dispatch_fp8: packed FP8 rows (pitch qpitch)
   int qpitch = 0;
+  // local_reduce (NEXT-3, R16): dedup send rows / meta, unique receive rows
+  int32_t *posg = nullptr, *u_hist = nullptr, *u_start = nullptr, *ughist = nullptr;
+  int32_t *meta_send = nullptr, *meta_recv = nullptr, *lr_recv_off_d = nullptr, *lr_usrc_d = nullptr;
+  void* recvu = nullptr;  // bf16 [recv_cap, H]: received unique rows, then their LocalReduce partials
+  int32_t* ughist_host = nullptr;  // pinned [ep*256]
   void *x_dev = nullptr, *y_dev = nullptr;  // staging for forward_host
   // host
   int32_t* ghist_host = nullptr;    // pinned [ep*E]
-  int32_t* tables_host = nullptr;   // pinned [2*E_loc]
+  int32_t* tables_host = nullptr;   // pinned [4*256+8]: GEMM row tables; local_reduce receive tables
   cudaStream_t s_disp = nullptr, s_comb = nullptr;
   cudaStream_t s_side = nullptr;  // shared experts, concurrent with routing / dispatch
   cudaStream_t s_h2d = nullptr, s_d2h = nullptr;  // forward_host copy streams
@@ -150,6 +156,7 @@ int validate(const moe_config_t* c) {
     why = "num_shared * shared_ffn must be a multiple of 128";
   else if (c->dispatch_fp8 && c->hidden % 128) why = "dispatch_fp8 needs hidden % 128 == 0";
   else if (c->max_tokens < 1) why = "max_tokens must be >= 1";
+  else if (c->local_reduce != 0 && c->local_reduce != 1) why = "local_reduce must be 0 or 1";
   if (!why.empty()) { set_error("invalid config: " + why); return MOE_ERR_INVALID; }
   return MOE_OK;
 }
@@ -188,6 +195,19 @@ size_t carve(moe_layer* L, char* base) {
   if (D > 1 && c.dispatch_fp8) {
     L->sendq = cv.take<uint8_t>(L->send_cap * L->qpitch);
     L->recvq = cv.take<uint8_t>(L->recv_cap * L->qpitch);
+  }
+  if (c.local_reduce) {
+    L->posg = cv.take<int32_t>(T * k);
+    L->u_hist = cv.take<int32_t>(MOE_MAX_EXPERTS + 1);
+    L->u_start = cv.take<int32_t>(MOE_MAX_EXPERTS + 1);
+    if (D > 1) {
+      L->ughist = cv.take<int32_t>(D * MOE_MAX_EXPERTS);
+      L->meta_send = cv.take<int32_t>(L->send_cap * 2 * k);
+      L->meta_recv = cv.take<int32_t>(L->recv_cap * 2 * k);
+      L->recvu = cv.take<uint16_t>(L->recv_cap * H);
+      L->lr_recv_off_d = cv.take<int32_t>(MOE_MAX_EXPERTS + 1);
+      L->lr_usrc_d = cv.take<int32_t>(MOE_MAX_EXPERTS + 1);
+    }
   }
   L->hs = SF ? cv.take<uint16_t>(T * SF) : nullptr;
   L->s = SF ? cv.take<uint16_t>(T * H) : nullptr;
@@ -400,7 +420,8 @@ static moe_status_t create_impl(const moe_config_t* cfg, const moe_weights_t* w,
     return fail(MOE_ERR_CUDA);
   }
   if (cudaHostAlloc(&L->ghist_host, sizeof(int32_t) * cfg->ep * cfg->num_experts, cudaHostAllocDefault) != cudaSuccess ||
-      cudaHostAlloc(&L->tables_host, sizeof(int32_t) * 2 * MOE_MAX_EXPERTS, cudaHostAllocDefault) != cudaSuccess) {
+      cudaHostAlloc(&L->tables_host, sizeof(int32_t) * (4 * MOE_MAX_EXPERTS + 8), cudaHostAllocDefault) != cudaSuccess ||
+      cudaHostAlloc(&L->ughist_host, sizeof(int32_t) * cfg->ep * MOE_MAX_EXPERTS, cudaHostAllocDefault) != cudaSuccess) {
     set_error("cudaHostAlloc failed");
     return fail(MOE_ERR_CUDA);
   }
@@ -471,7 +492,8 @@ static moe_status_t create_impl(const moe_config_t* cfg, const moe_weights_t* w,
       }
       // every rank must agree on the shape (MOE_ERR_MISMATCH)
       int32_t sig[8] = {cfg->num_experts, cfg->top_k, cfg->hidden, cfg->ffn, cfg->num_shared, cfg->shared_ffn,
-                        cfg->norm_topk, (int32_t)(cfg->routed_scale * 1e6f)};
+                        cfg->norm_topk | (cfg->dispatch_fp8 << 1) | (cfg->local_reduce << 2),
+                        (int32_t)(cfg->routed_scale * 1e6f)};
       int32_t* d_sig = nullptr;
       if (cudaMalloc(&d_sig, sizeof(sig) * (cfg->ep + 1)) != cudaSuccess) return fail(MOE_ERR_CUDA);
       cudaMemcpy(d_sig, sig, sizeof(sig), cudaMemcpyHostToDevice);
@@ -531,6 +553,7 @@ moe_status_t moe_layer_destroy(moe_layer_t* L) {
   for (auto e : L->pev) if (e) cudaEventDestroy(e);
   if (L->ghist_host) cudaFreeHost(L->ghist_host);
   if (L->tables_host) cudaFreeHost(L->tables_host);
+  if (L->ughist_host) cudaFreeHost(L->ughist_host);
   delete L;
   return MOE_OK;
 }
@@ -682,7 +705,8 @@ moe_status_t moe_layer_forward(moe_layer_t* L, const void* x, int64_t T, void* y
   // ep == 1: the shared DownGemm is deferred and fused with the combine
   // (EPI_COMBINE), so only GateUp runs here.
   // (a debug request for s materialises it: unfused path)
-  const int fuse = ((D == 1) && L->SF && T > 0 && !(dbg && dbg->shared_out)) ? L->fuse_combine : 0;
+  const int fuse =
+      ((D == 1) && L->SF && T > 0 && !c.local_reduce && !(dbg && dbg->shared_out)) ? L->fuse_combine : 0;
   auto shared_experts = [&](cudaStream_t ss) -> int {
     if (!L->SF || T == 0) return 0;
     int q0 = prof_rec(L, ss);
@@ -744,9 +768,12 @@ moe_status_t moe_layer_forward(moe_layer_t* L, const void* x, int64_t T, void* y
   // index-only and the GEMM gathers x's rows with TMA tile::gather4.
   const bool fp8 = c.dispatch_fp8 != 0;
   const bool gather = (D == 1) && L->gather_a && T > 0 && !fp8;
-  KERNEL_TRY(launch_permute(x, (int)T, H, E, k, topk_idx, L->range_off, L->seg_start, gather ? nullptr : L->send,
-                            L->pos, gather ? L->row_token : nullptr, fp8 ? (D == 1 ? 1 : 2) : 0, L->sendq,
-                            L->qpitch, st));
+  // ep > 1 with local_reduce: index-only here (pos feeds the dedup rows' codes);
+  // the dedup permute runs once the plan fixes the chunks
+  const bool lr_ep = (D > 1) && c.local_reduce;
+  KERNEL_TRY(launch_permute(x, (int)T, H, E, k, topk_idx, L->range_off, L->seg_start,
+                            (gather || lr_ep) ? nullptr : L->send, L->pos, gather ? L->row_token : nullptr,
+                            lr_ep ? 0 : (fp8 ? (D == 1 ? 1 : 2) : 0), L->sendq, L->qpitch, st));
   prof_mark(L, MOE_STAGE_ROUTE, p1, prof_rec(L, st));
   if (has_shared && !side) {
     int e = shared_experts(st);
@@ -820,6 +847,13 @@ moe_status_t moe_layer_forward(moe_layer_t* L, const void* x, int64_t T, void* y
       int e = gemm_launch(b, st);
       if (e) { set_error(std::string("shared DownGemm + combine: ") + cudaGetErrorString((cudaError_t)e)); return MOE_ERR_CUDA; }
       ++L->last_launches;
+    } else if (c.local_reduce) {
+      // R16 at ep == 1: groups = chunks; LocalReduce partials + home sum in one pass
+      LrChunks chs;
+      chs.n = plan.num_chunks;
+      for (int i = 0; i <= plan.num_chunks; ++i) chs.begin[i] = plan.group_begin[i];
+      KERNEL_TRY(launch_lr_combine_local(L->o, L->SF ? L->s : nullptr, (int)T, H, k, topk_idx, L->pos, topk_w, E,
+                                         chs, y, st));
     } else {
       KERNEL_TRY(launch_combine(L->o, L->SF ? L->s : nullptr, (int)T, H, k, L->pos, topk_w, y, st));
     }
@@ -849,6 +883,43 @@ moe_status_t moe_layer_forward(moe_layer_t* L, const void* x, int64_t T, void* y
     CUDA_TRY(cudaMemcpyAsync(L->recv_start_d, L->tables_host, sizeof(int32_t) * E_loc, cudaMemcpyHostToDevice, st));
     CUDA_TRY(cudaMemcpyAsync(L->recv_count_d, L->tables_host + MOE_MAX_EXPERTS, sizeof(int32_t) * E_loc,
                              cudaMemcpyHostToDevice, st));
+    // ---- local_reduce (R16): the dedup layout needs the plan's chunks, and the
+    // unique-row counts per (chunk, peer) need a second (G-int) exchange
+    const int G = plan.num_chunks * D;
+    std::vector<int64_t> usend_off(G + 1, 0);                     // my send rows of group g = c*D + peer
+    std::vector<int64_t> urecv((size_t)plan.num_chunks * D + 1, 0);  // first unique recv row of (c, src)
+    const int32_t* ug = L->ughist_host;                           // [D][G]
+    if (lr_ep) {
+      int q0 = prof_rec(L, st);
+      LrChunks chs;
+      chs.n = plan.num_chunks;
+      for (int i = 0; i <= plan.num_chunks; ++i) chs.begin[i] = plan.group_begin[i];
+      KERNEL_TRY(launch_lr_count(topk_idx, (int)T, k, E_loc, D, chs, L->range_hist, st));
+      KERNEL_TRY(launch_range_scan(L->range_hist, (int)T, G, L->range_off, L->u_hist, L->u_start, st));
+      KERNEL_TRY(launch_lr_permute(x, (int)T, H, k, topk_idx, topk_w, L->pos, L->seg_start, E_loc, D, chs,
+                                   L->range_off, L->u_start, fp8 ? nullptr : L->send, fp8 ? L->sendq : nullptr,
+                                   L->qpitch, L->posg, L->meta_send, st));
+      prof_mark(L, MOE_STAGE_ROUTE, q0, prof_rec(L, st));
+      TR_TRY(L->tr->allgather_i32(L->u_hist, L->ughist, G, st));
+      CUDA_TRY(cudaMemcpyAsync(L->ughist_host, L->ughist, sizeof(int32_t) * D * G, cudaMemcpyDeviceToHost, st));
+      CUDA_TRY(cudaEventRecord(L->ev_hist, st));
+      CUDA_TRY(cudaEventSynchronize(L->ev_hist));
+      for (int g = 0; g < G; ++g) usend_off[g + 1] = usend_off[g] + ug[(size_t)me * G + g];
+      int64_t row = 0;
+      for (int ch = 0; ch < plan.num_chunks; ++ch)
+        for (int src = 0; src < D; ++src) {
+          urecv[(size_t)ch * D + src] = row;
+          row += ug[(size_t)src * G + ch * D + me];
+        }
+      urecv[G] = row;
+      if (row > L->recv_cap) { set_error("unique recv rows exceed capacity"); return MOE_ERR_CAPACITY; }
+      int32_t* tb = L->tables_host + 2 * MOE_MAX_EXPERTS;  // [E_loc*D+1] recv_off, then [G+1] urecv
+      for (int i = 0; i <= E_loc * D; ++i) tb[i] = (int32_t)recv_off[i];
+      for (int i = 0; i <= G; ++i) tb[MOE_MAX_EXPERTS + 4 + i] = (int32_t)urecv[i];
+      CUDA_TRY(cudaMemcpyAsync(L->lr_recv_off_d, tb, sizeof(int32_t) * (E_loc * D + 1), cudaMemcpyHostToDevice, st));
+      CUDA_TRY(cudaMemcpyAsync(L->lr_usrc_d, tb + MOE_MAX_EXPERTS + 4, sizeof(int32_t) * (G + 1),
+                               cudaMemcpyHostToDevice, st));
+    }
     CUDA_TRY(cudaEventRecord(L->ev_ready, st));
     CUDA_TRY(cudaStreamWaitEvent(L->s_disp, L->ev_ready, 0));
     CUDA_TRY(cudaStreamWaitEvent(L->s_comb, L->ev_ready, 0));
@@ -857,11 +928,27 @@ moe_status_t moe_layer_forward(moe_layer_t* L, const void* x, int64_t T, void* y
     char* dsend = fp8 ? (char*)L->sendq : (char*)L->send;
     char* drecv = fp8 ? (char*)L->recvq : (char*)L->recv;
     const size_t drow = fp8 ? (size_t)L->qpitch : row_bytes;
+    const size_t meta_bytes = (size_t)2 * k * sizeof(int32_t);
     auto dispatch = [&](int ch) -> moe_status_t {
       int g0 = plan.group_begin[ch], g1 = plan.group_begin[ch + 1];
       int d0 = prof_rec(L, L->s_disp);
       TR_TRY(L->tr->group_start(0));
-      for (int peer = 0; peer < D; ++peer)
+      if (lr_ep) {  // one unique-row message + its meta per peer (R16)
+        char* urows = fp8 ? (char*)L->recvq : (char*)L->recvu;
+        for (int peer = 0; peer < D; ++peer) {
+          const int64_t s0 = usend_off[ch * D + peer], ns = ug[(size_t)me * G + ch * D + peer];
+          if (ns) {
+            TR_TRY(L->tr->send(dsend + s0 * drow, ns * drow, peer, 0, L->s_disp));
+            TR_TRY(L->tr->send((char*)L->meta_send + s0 * meta_bytes, ns * meta_bytes, peer, 0, L->s_disp));
+          }
+          const int64_t r0 = urecv[(size_t)ch * D + peer], nr = ug[(size_t)peer * G + ch * D + me];
+          if (nr) {
+            TR_TRY(L->tr->recv(urows + r0 * drow, nr * drow, peer, 0, L->s_disp));
+            TR_TRY(L->tr->recv((char*)L->meta_recv + r0 * meta_bytes, nr * meta_bytes, peer, 0, L->s_disp));
+          }
+        }
+      }
+      for (int peer = 0; peer < D && !lr_ep; ++peer)
         for (int el = g0; el < g1; ++el) {
           int ex = peer * E_loc + el;
           int64_t n_send = gh[(int64_t)me * E + ex];
@@ -880,7 +967,15 @@ moe_status_t moe_layer_forward(moe_layer_t* L, const void* x, int64_t T, void* y
       CUDA_TRY(cudaStreamWaitEvent(L->s_comb, L->ev_gemm[ch], 0));
       int b0 = prof_rec(L, L->s_comb);
       TR_TRY(L->tr->group_start(1));
-      for (int peer = 0; peer < D; ++peer)
+      if (lr_ep) {  // each unique row returns as its LocalReduce partial (R16)
+        for (int peer = 0; peer < D; ++peer) {
+          const int64_t r0 = urecv[(size_t)ch * D + peer], nb = ug[(size_t)peer * G + ch * D + me];
+          if (nb) TR_TRY(L->tr->send((char*)L->recvu + r0 * row_bytes, nb * row_bytes, peer, 1, L->s_comb));
+          const int64_t s0 = usend_off[ch * D + peer], nh = ug[(size_t)me * G + ch * D + peer];
+          if (nh) TR_TRY(L->tr->recv((char*)L->comb + s0 * row_bytes, nh * row_bytes, peer, 1, L->s_comb));
+        }
+      }
+      for (int peer = 0; peer < D && !lr_ep; ++peer)
         for (int el = g0; el < g1; ++el) {
           int64_t n_back = gh[(int64_t)peer * E + me * E_loc + el];
           if (n_back)
@@ -898,7 +993,11 @@ moe_status_t moe_layer_forward(moe_layer_t* L, const void* x, int64_t T, void* y
     auto compute = [&](int ch) -> moe_status_t {
       int g0 = plan.group_begin[ch], g1 = plan.group_begin[ch + 1];
       CUDA_TRY(cudaStreamWaitEvent(st, L->ev_disp[ch], 0));
-      if (fp8) {  // the chunk's received rows are contiguous in the recv layout (R6)
+      const int64_t u0 = urecv[(size_t)ch * D], u1 = urecv[(size_t)(ch + 1) * D];
+      if (lr_ep) {  // unique rows -> expert-major GEMM rows (R6 order, so the GEMMs are unchanged)
+        KERNEL_TRY(launch_lr_expand(L->recvu, fp8 ? L->recvq : nullptr, L->qpitch, u0, u1, H, k, D, ch, L->lr_usrc_d,
+                                    L->lr_recv_off_d, L->meta_recv, L->recv, st));
+      } else if (fp8) {  // the chunk's received rows are contiguous in the recv layout (R6)
         const int64_t r0 = recv_off[(size_t)g0 * D], r1 = recv_off[(size_t)g1 * D];
         KERNEL_TRY(launch_dequant_rows(drecv + r0 * drow, r1 - r0, H, L->qpitch, (char*)L->recv + r0 * row_bytes, st));
       }
@@ -913,6 +1012,8 @@ moe_status_t moe_layer_forward(moe_layer_t* L, const void* x, int64_t T, void* y
         if (err) { set_error(std::string("ComputeMoE: ") + cudaGetErrorString((cudaError_t)err)); return MOE_ERR_CUDA; }
         a = b;
       }
+      // LocalReduce: the chunk's partial per unique row, in place of its x row
+      if (lr_ep) KERNEL_TRY(launch_lr_reduce(L->o, L->meta_recv, u0, u1, H, k, L->recvu, st));
       CUDA_TRY(cudaEventRecord(L->ev_gemm[ch], st));
       return MOE_OK;
     };
@@ -930,8 +1031,15 @@ moe_status_t moe_layer_forward(moe_layer_t* L, const void* x, int64_t T, void* y
     CUDA_TRY(cudaStreamWaitEvent(st, L->ev_comb_done, 0));
     if (side) CUDA_TRY(cudaStreamWaitEvent(st, L->ev_shared, 0));
     int c0 = prof_rec(L, st);
-    KERNEL_TRY(launch_combine(L->comb, L->SF ? L->s : nullptr, (int)T, H, k, L->pos, topk_w, y, st));
+    if (lr_ep)
+      KERNEL_TRY(launch_lr_combine(L->comb, L->SF ? L->s : nullptr, (int)T, H, k, L->posg, y, st));
+    else
+      KERNEL_TRY(launch_combine(L->comb, L->SF ? L->s : nullptr, (int)T, H, k, L->pos, topk_w, y, st));
     prof_mark(L, MOE_STAGE_COMBINE, c0, prof_rec(L, st));
+    if (dbg && lr_ep) {
+      if (dbg->lr_pos) CUDA_TRY(cudaMemcpyAsync(dbg->lr_pos, L->posg, sizeof(int32_t) * T * k, cudaMemcpyDeviceToDevice, st));
+      if (dbg->lr_hist) CUDA_TRY(cudaMemcpyAsync(dbg->lr_hist, L->u_hist, sizeof(int32_t) * G, cudaMemcpyDeviceToDevice, st));
+    }
   }
   prof_mark(L, MOE_STAGE_TOTAL, p_total, prof_rec(L, st));
 

@@ -40,12 +40,12 @@ class MoELayer:
     ws_down [H,S*Fs], router_bias fp32 [E]."""
 
     def __init__(self, E, k, H, F, weights, S=0, Fs=0, ep=1, rank=0, max_tokens=1, norm_topk=0,
-                 routed_scale=1.0, dispatch_fp8: bool = False,
+                 routed_scale=1.0, dispatch_fp8: bool = False, local_reduce: bool = False,
                  uid_dispatch: bytes | None = None, uid_combine: bytes | None = None,
                  device=None, local_group: "LocalGroup | None" = None):
         self.lib = abi.lib()
         self.cfg = abi.make_config(E, k, H, F, S, Fs, ep, rank, max_tokens, norm_topk, routed_scale,
-                                   1 if dispatch_fp8 else 0)
+                                   1 if dispatch_fp8 else 0, 1 if local_reduce else 0)
         self.E, self.k, self.H, self.F, self.S, self.Fs, self.ep, self.rank = E, k, H, F, S, Fs, ep, rank
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         nbytes = self.lib.moe_layer_workspace_bytes(C.byref(self.cfg))
@@ -148,6 +148,8 @@ class MoELayer:
             hist=torch.empty(self.E, dtype=torch.int32, device=dev),
             seg_start=torch.empty(self.E + 1, dtype=torch.int32, device=dev),
             shared_out=torch.empty(T, self.H, dtype=torch.bfloat16, device=dev) if self.S else None,
+            lr_pos=torch.full((T, self.k), -7, dtype=torch.int32, device=dev) if self.cfg.local_reduce else None,
+            lr_hist=torch.full((256,), -7, dtype=torch.int32, device=dev) if self.cfg.local_reduce else None,
         )
         if override is not None:
             bufs["topk_idx"] = override[0].to(dev, torch.int32).contiguous()
@@ -158,7 +160,8 @@ class MoELayer:
         d = abi.moe_debug_t(1 if override is not None else 0,
                             *[_ptr(bufs[n]) for n in ("logits", "topk_idx", "topk_w", "pos", "hist",
                                                        "seg_start", "shared_out")],
-                            ghist.ctypes.data_as(C.c_void_p), C.pointer(plan_used))
+                            ghist.ctypes.data_as(C.c_void_p), C.pointer(plan_used),
+                            _ptr(bufs["lr_pos"]), _ptr(bufs["lr_hist"]))
         bufs["global_hist"] = ghist
         bufs["plan_used"] = plan_used
         bufs["_struct"] = d

@@ -22,7 +22,7 @@ from .gpu_util import assert_close, dev_bf16, to_f32
 pytestmark = pytest.mark.gpu
 
 
-def _ep_forward(inp, k, norm, D, plan=None, skew_bias=None, fp8=False):
+def _ep_forward(inp, k, norm, D, plan=None, skew_bias=None, fp8=False, lr=False):
     E, H, F, T = inp.E, inp.H, inp.F, inp.T
     E_loc = E // D
     start = oracle.token_shards(T, D)
@@ -38,7 +38,7 @@ def _ep_forward(inp, k, norm, D, plan=None, skew_bias=None, fp8=False):
             w["router_bias"] = torch.from_numpy(skew_bias).cuda()
         T_loc = int(start[r + 1] - start[r])
         layers.append(MoELayer(E, k, H, F, w, S=inp.S, Fs=inp.Fs, ep=D, rank=r, max_tokens=max(T_loc, 1),
-                               norm_topk=norm, local_group=group, dispatch_fp8=fp8))
+                               norm_topk=norm, local_group=group, dispatch_fp8=fp8, local_reduce=lr))
         xs.append(dev_bf16(inp.x[start[r]:start[r + 1]]))
     ys, bufs, errs = [None] * D, [None] * D, []
 
@@ -67,7 +67,7 @@ def _ep_forward(inp, k, norm, D, plan=None, skew_bias=None, fp8=False):
     return y, bufs
 
 
-def _ep1_forward(inp, k, norm, plan=None, skew_bias=None, fp8=False):
+def _ep1_forward(inp, k, norm, plan=None, skew_bias=None, fp8=False, lr=False):
     w = dict(w_router=dev_bf16(inp.w_router), w_gate=dev_bf16(inp.w_gate), w_up=dev_bf16(inp.w_up),
              w_down=dev_bf16(inp.w_down))
     if inp.S:
@@ -75,7 +75,7 @@ def _ep1_forward(inp, k, norm, plan=None, skew_bias=None, fp8=False):
     if skew_bias is not None:
         w["router_bias"] = torch.from_numpy(skew_bias).cuda()
     L = MoELayer(inp.E, k, inp.H, inp.F, w, S=inp.S, Fs=inp.Fs, max_tokens=inp.T, norm_topk=norm,
-                 dispatch_fp8=fp8)
+                 dispatch_fp8=fp8, local_reduce=lr)
     y = L.forward(dev_bf16(inp.x), plan=plan)
     torch.cuda.synchronize()
     out = y.float().cpu().numpy()
@@ -143,3 +143,59 @@ def test_ep_planner_auto_and_skew():
     assert idx_ok.mean() > 0.99
     assert_close(y[idx_ok], ref["y"][idx_ok], "EP4 skew")
     assert_close(y1[idx_ok], ref["y"][idx_ok], "EP1 skew")
+
+
+# ---------------------------------------------------------------- NEXT-3: expert-side LocalReduce (R16)
+
+@pytest.mark.parametrize("D,N,kind,tile_m", [(2, 1, MOE_GEMM_GROUPED, 256), (2, 3, MOE_GEMM_GROUPED, 128),
+                                             (4, 2, MOE_GEMM_DENSE, 256), (4, 4, MOE_GEMM_GROUPED, 128),
+                                             (8, 2, MOE_GEMM_GROUPED, 256)])
+def test_local_reduce_ep_vs_oracle(D, N, kind, tile_m):
+    """Dedup dispatch (one row per (token, rank, chunk)), expert-side
+    LocalReduce partials, home sum: the dedup layout (per-group row counts,
+    each token's group rows) bit-exact vs the oracle's lr_layout; y vs the
+    oracle's R16 contract."""
+    inp = Inputs(E=16, k=4, H=256, F=256, S=1, Fs=128, T=997, seed=70 + D, grid=True)
+    y, bufs = _ep_forward(inp, 4, 0, D, make_plan(N, kind, tile_m=tile_m), lr=True)
+    ref = oracle.moe_layer(inp.x, inp.w_router, inp.w_gate, inp.w_up, inp.w_down, k=4, norm_topk=0,
+                           ws_gate_bits=inp.ws_gate, ws_up_bits=inp.ws_up, ws_down_bits=inp.ws_down, D=D, N=N,
+                           local_reduce=True)
+    lay = ref["lr_layout"]
+    for r in range(D):
+        assert np.array_equal(bufs[r]["lr_hist"].cpu().numpy()[:N * D], lay["u_hist"][r])
+        assert np.array_equal(bufs[r]["lr_pos"].cpu().numpy(), lay["posg"][r])
+    if N < 16 // D:                                 # groups of >1 expert: the dedup saved rows
+        assert lay["u_hist"].sum() < 997 * 4
+    else:                                           # one expert per group: one row per pair
+        assert lay["u_hist"].sum() == 997 * 4
+    assert_close(y, ref["y"], f"LR EP{D} N{N}")
+    # the rows each expert sees are unchanged: the plain path's o feeds both,
+    # so y differs from the per-pair path only by the regrouped rounding
+    y_pp, _ = _ep_forward(inp, 4, 0, D, make_plan(N, kind, tile_m=tile_m))
+    assert not np.array_equal(y, y_pp)
+    assert_close(y, y_pp, "LR vs per-pair")
+
+
+def test_local_reduce_fp8_ep_vs_oracle():
+    inp = Inputs(E=8, k=2, H=256, F=256, S=1, Fs=128, T=501, seed=62)
+    y, bufs = _ep_forward(inp, 2, 1, 2, make_plan(2, MOE_GEMM_GROUPED), fp8=True, lr=True)
+    ref = oracle.moe_layer(inp.x, inp.w_router, inp.w_gate, inp.w_up, inp.w_down, k=2, norm_topk=1,
+                           ws_gate_bits=inp.ws_gate, ws_up_bits=inp.ws_up, ws_down_bits=inp.ws_down,
+                           dispatch_fp8=True, D=2, N=2, local_reduce=True)
+    same = (ref["idx"] == np.concatenate([b["topk_idx"].cpu().numpy() for b in bufs])).all(axis=1)
+    assert same.mean() > 0.99
+    assert_close(y[same], ref["y"][same], "LR fp8 EP2")
+
+
+@pytest.mark.parametrize("N,S", [(1, 0), (1, 1), (3, 1)])
+def test_local_reduce_ep1(N, S):
+    """ep == 1: groups are chunks; one kernel forms the partials and the home
+    sum.  S = 0, N = 1: one group per token, so y == the plain path bit for bit."""
+    inp = Inputs(E=16, k=4, H=256, F=256, S=S, Fs=128, T=600, seed=71, grid=True)
+    kw = dict(ws_gate_bits=inp.ws_gate, ws_up_bits=inp.ws_up, ws_down_bits=inp.ws_down) if S else {}
+    y = _ep1_forward(inp, 4, 0, make_plan(N, MOE_GEMM_GROUPED), lr=True)
+    ref = oracle.moe_layer(inp.x, inp.w_router, inp.w_gate, inp.w_up, inp.w_down, k=4, norm_topk=0, N=N,
+                           local_reduce=True, **kw)
+    assert_close(y, ref["y"], f"LR EP1 N{N}")
+    if S == 0 and N == 1:
+        assert np.array_equal(y, _ep1_forward(inp, 4, 0, make_plan(1, MOE_GEMM_GROUPED)))
