@@ -159,22 +159,37 @@ def router_logits(x_bits, w_router_bits, router_bias=None, mode="contract"):
 # ----------------------------------------------------------------------------
 
 
-def topk_gating(logits, k, norm_topk, routed_scale=1.0, mode="contract"):
+def topk_gating(logits, k, norm_topk, routed_scale=1.0, mode="contract", route_groups=0, route_topk_groups=0):
     """Returns (idx [T,k] int32, w [T,k] float32; float64 in exact mode).
 
     idx_t = the k experts ordered by (logit desc, expert id asc).
     p = softmax over all E (computed in fp64 from the fp32 logits, rounded to
     fp32); w_j = p_{idx_j}; if norm_topk: w_j = p_{idx_j} / sum_j p_{idx_j};
     then w_j *= routed_scale.
+
+    Device-limited routing (DeepSeek-V2's mechanism; NEXT-4, R17) when
+    1 < route_groups and route_topk_groups < route_groups: the E experts form
+    route_groups contiguous groups of E/route_groups; a group's score is its
+    largest logit; only the experts of the route_topk_groups best groups
+    (score desc, group id asc) are eligible for the top-k above.  The softmax
+    still runs over all E.
     """
     logits = np.asarray(logits)
     T, E = logits.shape
     idx = np.empty((T, k), dtype=np.int32)
     w = np.empty((T, k), dtype=np.float64 if mode == "exact" else np.float32)
     experts = np.arange(E)
+    limited = route_groups > 1 and route_topk_groups < route_groups
+    if limited:
+        gsz = E // route_groups
+        groups = np.arange(route_groups)
     for t in range(T):
         row = logits[t].astype(np.float64)
         order = np.lexsort((experts, -row))          # primary: -logit, secondary: e
+        if limited:
+            score = row.reshape(route_groups, gsz).max(axis=1)
+            keep = np.lexsort((groups, -score))[:route_topk_groups]
+            order = order[np.isin(order // gsz, keep)]
         sel = order[:k]
         ex = np.exp(row - row.max())
         p = ex / ex.sum()
@@ -448,7 +463,8 @@ def local_reduce_combine(s, o_slots, w, gid, mode="contract"):
 def moe_layer(x_bits, w_router_bits, w_gate_bits, w_up_bits, w_down_bits, k, norm_topk,
               ws_gate_bits=None, ws_up_bits=None, ws_down_bits=None, router_bias=None,
               routed_scale=1.0, D=1, N=1, token_slices=1, mode="contract",
-              topk_override=None, dispatch_fp8=False, local_reduce=False):
+              topk_override=None, dispatch_fp8=False, local_reduce=False, route_groups=0,
+              route_topk_groups=0):
     """Full layer over all T tokens.  Weights are indexed by global expert id.
 
     topk_override = (idx, w) replaces Router + topKGating (explicit routing,
@@ -465,7 +481,7 @@ def moe_layer(x_bits, w_router_bits, w_gate_bits, w_up_bits, w_down_bits, k, nor
     E_loc = E // D
     if topk_override is None:
         logits = router_logits(x_bits, w_router_bits, router_bias, mode)
-        idx, w = topk_gating(logits, k, norm_topk, routed_scale, mode)
+        idx, w = topk_gating(logits, k, norm_topk, routed_scale, mode, route_groups, route_topk_groups)
     else:
         logits = None
         idx, w = (np.asarray(a) for a in topk_override)
@@ -535,12 +551,13 @@ def moe_layer(x_bits, w_router_bits, w_gate_bits, w_up_bits, w_down_bits, k, nor
 
 
 def moe_tokens(x_bits, w_router_bits, expert_weights, k, norm_topk, shared=None,
-               router_bias=None, routed_scale=1.0, mode="contract", dispatch_fp8=False):
+               router_bias=None, routed_scale=1.0, mode="contract", dispatch_fp8=False, route_groups=0,
+               route_topk_groups=0):
     """y for an arbitrary subset of tokens (y_t depends only on x_t and the
     weights).  expert_weights: callable e -> (Wg, Wu, Wd) bits.
     Used for sampled parity at the full BASELINE sizes."""
     logits = router_logits(x_bits, w_router_bits, router_bias, mode)
-    idx, w = topk_gating(logits, k, norm_topk, routed_scale, mode)
+    idx, w = topk_gating(logits, k, norm_topk, routed_scale, mode, route_groups, route_topk_groups)
     T, H = x_bits.shape
     x_disp = fp8_dispatch_roundtrip(x_bits) if dispatch_fp8 else x_bits
     o_slots = np.zeros((T, k, H), dtype=np.float64 if mode == "exact" else np.float32)

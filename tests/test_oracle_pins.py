@@ -496,3 +496,39 @@ def test_local_reduce_contract_vs_exact_band():
     rel = np.abs(ct["y"] - ex["y"]).sum() / np.abs(ex["y"]).sum()
     assert 3e-4 < rel < 6e-3
     assert np.array_equal(oracle.round_bf16(ct["y"]), ct["y"])
+
+
+# --------------------------------------------------------------------------
+# 9. Device-limited routing (NEXT-4, R17)
+# --------------------------------------------------------------------------
+
+def test_device_limited_routing_hand_fixture():
+    fx = json.load(open(os.path.join(GOLDEN, "device_limited_routing.json")))
+    lg = np.array([c["logits"] for c in fx["cases"]], dtype=np.float32)
+    idx, _ = oracle.topk_gating(lg, fx["k"], 0, route_groups=fx["route_groups"],
+                                route_topk_groups=fx["route_topk_groups"])
+    assert idx.tolist() == [c["idx"] for c in fx["cases"]]
+    plain, _ = oracle.topk_gating(lg, fx["k"], 0)
+    assert plain.tolist() == [c["plain_idx"] for c in fx["cases"]]
+
+
+def test_device_limited_routing_special_cases_and_bound():
+    """M = number of groups: plain routing.  Any M: a token's experts span at
+    most M groups (g <= min(k, D)), so with groups = EP ranks, N = 1 and
+    the dedup of R16 a token sends at most M rows (M = 1: exactly one)."""
+    inp = Inputs(E=16, k=4, H=64, F=128, T=300, seed=33)
+    lg = oracle.router_logits(inp.x, inp.w_router)
+    plain = oracle.topk_gating(lg, 4, 1)
+    same = oracle.topk_gating(lg, 4, 1, route_groups=4, route_topk_groups=4)
+    assert np.array_equal(plain[0], same[0]) and np.array_equal(plain[1], same[1])
+    for M in (1, 2, 3):
+        idx, w = oracle.topk_gating(lg, 4, 1, route_groups=4, route_topk_groups=M)
+        assert max(len(set((row // 4).tolist())) for row in idx) <= M
+        assert np.allclose(w.sum(axis=1), 1.0, atol=1e-6)          # norm_topk over the kept experts
+        lay = oracle.lr_layout(idx, 16, 4, 1)
+        assert lay["u_hist"].sum() <= M * 300
+        if M == 1:
+            assert lay["u_hist"].sum() == 300
+    # the restriction can only lower the selected logits
+    idx2, _ = oracle.topk_gating(lg, 4, 1, route_groups=4, route_topk_groups=2)
+    assert (np.take_along_axis(lg, idx2, 1).sum(1) <= np.take_along_axis(lg, plain[0], 1).sum(1)).all()
