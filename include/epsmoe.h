@@ -79,6 +79,12 @@ typedef struct {
                            p = bf16(sum of w_j o_j in slot order); home side
                            y = bf16(s + p_g ... in (chunk, rank) order).
                            0: per-pair transfer, home-side weighted sum (R7). */
+  int32_t route_groups; /* device-limited routing (DeepSeek-V2; NEXT-4,
+                           R17): experts form route_groups contiguous groups
+                           (<= 32, dividing e); only experts of the
+                           route_topk_groups groups with the largest best
+                           logit may be selected.  0 or 1: off.             */
+  int32_t route_topk_groups; /* M, 1 <= M <= route_groups, topk <= M*e/groups */
 } moe_config_t;
 
 /* Caller-owned device weights (bf16, K-major), valid for the layer's life.

@@ -157,6 +157,11 @@ int validate(const moe_config_t* c) {
   else if (c->dispatch_fp8 && c->hidden % 128) why = "dispatch_fp8 needs hidden % 128 == 0";
   else if (c->max_tokens < 1) why = "max_tokens must be >= 1";
   else if (c->local_reduce != 0 && c->local_reduce != 1) why = "local_reduce must be 0 or 1";
+  else if (c->route_groups > 1 &&
+           (c->route_groups > 32 || c->num_experts % c->route_groups || c->route_topk_groups < 1 ||
+            c->route_topk_groups > c->route_groups ||
+            c->top_k > c->route_topk_groups * (c->num_experts / c->route_groups)))
+    why = "route_groups must divide e (<= 32) with 1 <= route_topk_groups <= route_groups and topk <= M*e/groups";
   if (!why.empty()) { set_error("invalid config: " + why); return MOE_ERR_INVALID; }
   return MOE_OK;
 }
@@ -492,7 +497,8 @@ static moe_status_t create_impl(const moe_config_t* cfg, const moe_weights_t* w,
       }
       // every rank must agree on the shape (MOE_ERR_MISMATCH)
       int32_t sig[8] = {cfg->num_experts, cfg->top_k, cfg->hidden, cfg->ffn, cfg->num_shared, cfg->shared_ffn,
-                        cfg->norm_topk | (cfg->dispatch_fp8 << 1) | (cfg->local_reduce << 2),
+                        cfg->norm_topk | (cfg->dispatch_fp8 << 1) | (cfg->local_reduce << 2) |
+                            (cfg->route_groups << 3) | (cfg->route_topk_groups << 9),
                         (int32_t)(cfg->routed_scale * 1e6f)};
       int32_t* d_sig = nullptr;
       if (cudaMalloc(&d_sig, sizeof(sig) * (cfg->ep + 1)) != cudaSuccess) return fail(MOE_ERR_CUDA);
@@ -760,7 +766,8 @@ moe_status_t moe_layer_forward(moe_layer_t* L, const void* x, int64_t T, void* y
   }
 
   KERNEL_TRY(launch_gate_topk(L->logits, (int)T, E, k, c.norm_topk, c.routed_scale, override_routing ? 1 : 0,
-                              topk_idx, topk_w, L->range_hist, st));
+                              c.route_groups > 1 ? c.route_groups : 0, c.route_topk_groups, topk_idx, topk_w,
+                              L->range_hist, st));
   KERNEL_TRY(launch_range_scan(L->range_hist, (int)T, E, L->range_off, L->hist, L->seg_start, st));
   ++L->last_launches;  // range scan + expert scan
   // ---- split (K3): x -> send rows, expert-major (R6).  At ep == 1 the send

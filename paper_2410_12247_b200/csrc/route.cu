@@ -34,8 +34,8 @@ __device__ __forceinline__ bool better(float av, int ae, float bv, int be) {
 // Also writes the range's expert histogram range_hist[e * R + r].
 __global__ void __launch_bounds__(WARPS_R * 32)
 gate_topk_kernel(const float* __restrict__ logits, int T, int E, int k, int norm_topk, float scale,
-                 int override_routing, int32_t* __restrict__ topk_idx, float* __restrict__ topk_w,
-                 int32_t* __restrict__ range_hist, int R) {
+                 int override_routing, int route_groups, int route_topk_groups, int32_t* __restrict__ topk_idx,
+                 float* __restrict__ topk_w, int32_t* __restrict__ range_hist, int R) {
   __shared__ int32_t hist_s[WARPS_R][256];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int r = blockIdx.x * WARPS_R + warp;
@@ -59,6 +59,43 @@ gate_topk_kernel(const float* __restrict__ logits, int T, int E, int k, int norm
         v[i] = (e < E) ? row[e] : -INFINITY;
       }
       uint32_t taken = 0;
+      if (route_groups) {
+        // device-limited routing (R17): lane q < route_groups holds group q's
+        // best logit; the route_topk_groups best groups (score desc, id asc)
+        // stay eligible, the other groups' experts are marked taken
+        const int gsz = E / route_groups;
+        float gscore = -INFINITY;
+        for (int q = 0; q < route_groups; ++q) {
+          float m = -INFINITY;
+#pragma unroll
+          for (int i = 0; i < MAX_EPL; ++i) {
+            const int e = lane + 32 * i;
+            if (e < E && e / gsz == q) m = fmaxf(m, v[i]);
+          }
+#pragma unroll
+          for (int off = 16; off > 0; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
+          if (lane == q) gscore = m;
+        }
+        uint32_t keep = 0;
+        bool used = lane >= route_groups;
+        for (int j = 0; j < route_topk_groups; ++j) {
+          float bv = used ? -INFINITY : gscore;
+          int bg = used ? 0x7fffffff : lane;
+#pragma unroll
+          for (int off = 16; off > 0; off >>= 1) {
+            const float ov = __shfl_xor_sync(0xffffffffu, bv, off);
+            const int og = __shfl_xor_sync(0xffffffffu, bg, off);
+            if (better(ov, og, bv, bg)) { bv = ov; bg = og; }
+          }
+          keep |= 1u << bg;
+          if (lane == bg) used = true;
+        }
+#pragma unroll
+        for (int i = 0; i < MAX_EPL; ++i) {
+          const int e = lane + 32 * i;
+          if (e < E && !((keep >> (e / gsz)) & 1u)) taken |= 1u << i;
+        }
+      }
       float top_v[8];
       int top_e[8];
       for (int j = 0; j < k; ++j) {
@@ -363,11 +400,14 @@ __global__ void pad_rows_kernel(const __nv_bfloat16* __restrict__ src, int rows,
 int num_ranges(int64_t T) { return (int)((T + RANGE_T - 1) / RANGE_T); }
 
 int launch_gate_topk(const float* logits, int T, int E, int k, int norm_topk, float scale, int override_routing,
-                     int32_t* topk_idx, float* topk_w, int32_t* range_hist, cudaStream_t st) {
+                     int route_groups, int route_topk_groups, int32_t* topk_idx, float* topk_w,
+                     int32_t* range_hist, cudaStream_t st) {
   int R = num_ranges(T);
   if (R == 0) return 0;
+  if (route_groups <= 1 || route_topk_groups >= route_groups) route_groups = 0;  // unrestricted
   gate_topk_kernel<<<(R + WARPS_R - 1) / WARPS_R, WARPS_R * 32, 0, st>>>(logits, T, E, k, norm_topk, scale,
-                                                                         override_routing, topk_idx, topk_w,
+                                                                         override_routing, route_groups,
+                                                                         route_topk_groups, topk_idx, topk_w,
                                                                          range_hist, R);
   return (int)cudaGetLastError();
 }

@@ -8,8 +8,10 @@ namespace epsmoe {
 constexpr int RANGE_T = 32;  // tokens per deterministic counting range (one warp)
 
 int num_ranges(int64_t T);
+// route_groups > 1 (and route_topk_groups < route_groups): device-limited routing (R17).
 int launch_gate_topk(const float* logits, int T, int E, int k, int norm_topk, float scale, int override_routing,
-                     int32_t* topk_idx, float* topk_w, int32_t* range_hist, cudaStream_t st);
+                     int route_groups, int route_topk_groups, int32_t* topk_idx, float* topk_w,
+                     int32_t* range_hist, cudaStream_t st);
 // per-range offsets, per-expert totals (hist) and expert segment starts (seg_start[E+1])
 int launch_range_scan(const int32_t* range_hist, int T, int E, int32_t* range_off, int32_t* hist,
                       int32_t* seg_start, cudaStream_t st);

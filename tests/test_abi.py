@@ -5,6 +5,7 @@ import ctypes as C
 import math
 import os
 import re
+import subprocess
 
 import numpy as np
 import pytest
@@ -28,10 +29,28 @@ def test_library_exports_every_header_symbol():
     assert declared <= set(abi._SIGS), declared - set(abi._SIGS)
 
 
-def test_struct_sizes_match_header_layout():
-    assert C.sizeof(abi.moe_config_t) == 56
-    assert C.sizeof(abi.moe_weights_t) == 64
-    assert C.sizeof(abi.moe_plan_t) == 5 * 4 + 65 * 4 + 256 + 5 * 4 + 4
+def test_struct_sizes_match_header_layout(tmp_path):
+    """The ctypes mirrors have the C header's sizes and field offsets (compiled
+    with gcc against include/epsmoe.h)."""
+    structs = {"moe_config_t": abi.moe_config_t, "moe_weights_t": abi.moe_weights_t,
+               "moe_plan_t": abi.moe_plan_t, "moe_cost_model_t": abi.moe_cost_model_t,
+               "moe_debug_t": abi.moe_debug_t}
+    lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "epsmoe.h"', 'int main(void) {']
+    for name, cls in structs.items():
+        lines.append(f'  printf("{name} %zu\\n", sizeof({name}));')
+        for f, _ in cls._fields_:
+            lines.append(f'  printf("{name}.{f} %zu\\n", offsetof({name}, {f}));')
+    lines += ['  return 0;', '}']
+    src = tmp_path / "sizes.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "sizes"
+    subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)], check=True)
+    out = dict(l.rsplit(" ", 1) for l in subprocess.run([str(exe)], capture_output=True, text=True,
+                                                         check=True).stdout.splitlines())
+    for name, cls in structs.items():
+        assert int(out[name]) == C.sizeof(cls), name
+        for f, _ in cls._fields_:
+            assert int(out[f"{name}.{f}"]) == getattr(cls, f).offset, (name, f)
 
 
 @pytest.mark.parametrize("bad", [

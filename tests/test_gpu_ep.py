@@ -199,3 +199,48 @@ def test_local_reduce_ep1(N, S):
     assert_close(y, ref["y"], f"LR EP1 N{N}")
     if S == 0 and N == 1:
         assert np.array_equal(y, _ep1_forward(inp, 4, 0, make_plan(1, MOE_GEMM_GROUPED)))
+
+
+def test_device_limited_routing_with_local_reduce_one_row_per_token():
+    """Groups = EP ranks, M = 1, N = 1: every token's experts sit on one rank,
+    so the dedup dispatch sends exactly one row per token (g = 1)."""
+    D = 4
+    inp = Inputs(E=16, k=3, H=256, F=256, S=0, T=640, seed=81, grid=True)
+    E_loc, start = 4, oracle.token_shards(640, D)
+    group = LocalGroup(D)
+    layers, xs = [], []
+    for r in range(D):
+        w = dict(w_router=dev_bf16(inp.w_router), w_gate=dev_bf16(inp.w_gate[r * E_loc:(r + 1) * E_loc]),
+                 w_up=dev_bf16(inp.w_up[r * E_loc:(r + 1) * E_loc]),
+                 w_down=dev_bf16(inp.w_down[r * E_loc:(r + 1) * E_loc]))
+        layers.append(MoELayer(16, 3, 256, 256, w, ep=D, rank=r, max_tokens=160, norm_topk=1, local_group=group,
+                               local_reduce=True, route_groups=D, route_topk_groups=1))
+        xs.append(dev_bf16(inp.x[start[r]:start[r + 1]]))
+    ys, bufs, errs = [None] * D, [None] * D, []
+
+    def worker(r):
+        try:
+            torch.cuda.set_device(0)
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                d, b = layers[r].debug_buffers(160)
+                ys[r] = layers[r].forward(xs[r], plan=make_plan(1, MOE_GEMM_GROUPED), stream=s, debug=d)
+                s.synchronize()
+                bufs[r] = b
+        except Exception as e:  # pragma: no cover
+            errs.append(repr(e))
+
+    th = [threading.Thread(target=worker, args=(r,), daemon=True) for r in range(D)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=120)
+    assert not errs, errs
+    for r in range(D):
+        assert bufs[r]["lr_hist"].cpu().numpy()[:D].sum() == 160
+    y = torch.cat(ys).float().cpu().numpy()
+    ref = oracle.moe_layer(inp.x, inp.w_router, inp.w_gate, inp.w_up, inp.w_down, k=3, norm_topk=1, D=D, N=1,
+                           local_reduce=True, route_groups=D, route_topk_groups=1)
+    assert_close(y, ref["y"], "device-limited M=1 + LR")
+    for L in layers:
+        L.close()

@@ -313,3 +313,23 @@ def test_fused_shared_down_combine_equals_unfused(name, T, monkeypatch):
         ref = oracle.moe_layer(inp.x, inp.w_router, inp.w_gate, inp.w_up, inp.w_down, k=k, norm_topk=norm,
                                ws_gate_bits=inp.ws_gate, ws_up_bits=inp.ws_up, ws_down_bits=inp.ws_down)
         assert_close(to_f32(ys[1]), ref["y"], name + " fused")
+
+
+@pytest.mark.parametrize("E,k,G,M,H", [(16, 4, 4, 2, 256), (160, 6, 8, 3, 256), (64, 6, 8, 1, 128)])
+def test_device_limited_routing_exact(E, k, G, M, H):
+    """NEXT-4 (R17): group-limited top-k on the exact-logit grid:
+    indices bit-exact vs the oracle, every token within M groups, y vs oracle."""
+    inp = Inputs(E=E, k=k, H=H, F=128, S=1, Fs=128, T=700, seed=44, grid=True)
+    L = layer_from_inputs(inp, k, 1, route_groups=G, route_topk_groups=M)
+    d, b = L.debug_buffers(inp.T)
+    y = L.forward(dev_bf16(inp.x), debug=d)
+    torch.cuda.synchronize()
+    ref = oracle.moe_layer(inp.x, inp.w_router, inp.w_gate, inp.w_up, inp.w_down, k=k, norm_topk=1,
+                           ws_gate_bits=inp.ws_gate, ws_up_bits=inp.ws_up, ws_down_bits=inp.ws_down,
+                           route_groups=G, route_topk_groups=M)
+    idx = b["topk_idx"].cpu().numpy()
+    assert np.array_equal(idx, ref["idx"])
+    assert max(len(set((row // (E // G)).tolist())) for row in idx) <= M
+    assert not np.array_equal(idx, oracle.topk_gating(ref["logits"], k, 1)[0])   # the limit bites
+    assert_close(to_f32(y), ref["y"], f"device-limited E{E} G{G} M{M}")
+    L.close()
