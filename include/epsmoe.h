@@ -112,12 +112,18 @@ typedef enum {
 
 /* Output of the expert pipeline scheduler (Algorithm 1's PN). */
 typedef struct {
-  int32_t num_chunks;   /* PN, 1 <= PN <= E_loc * token_slices */
-  int32_t token_slices; /* 1 = paper (chunks are expert groups, R8)               */
+  int32_t num_chunks;   /* PN = groups * token_slices <= 64 */
+  int32_t token_slices; /* S: 1 = paper (chunks are expert groups, R8); S > 1 (ep
+                           > 1, not with local_reduce): every expert group is
+                           split into S source-token slices (balanced ranges
+                           of each rank's tokens), chunk c = (group c / S,
+                           slice c % S); the forward then exchanges the
+                           (expert, slice) counts once more                    */
   int32_t gemm_kind;    /* moe_gemm_kind_t applied to all experts (AUTO: see below) */
   int32_t sm_gemm;      /* persistent GEMM grid (0 = all SMs)           P:492, A15 */
   int32_t comm_ctas;    /* NCCL maxCTAs per communicator (0 = default) */
-  int32_t group_begin[MOE_MAX_CHUNKS + 1]; /* local-expert group bounds (R8)     */
+  int32_t group_begin[MOE_MAX_CHUNKS + 1]; /* local-expert group bounds (R8),
+                                              [0 .. PN / token_slices]        */
   uint8_t expert_kind[MOE_MAX_EXPERTS];    /* resolved kind per local expert      */
   float pred_comm_ms;   /* T_comm before splitting    */
   float pred_comp_ms;   /* T_comp before splitting    */

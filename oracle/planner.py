@@ -19,10 +19,13 @@ def pn_objective(N, t_comm, t_comp, k, b):
     return min(t_comm / N, t_comp / N) * (N - 1) - (k * N + b)
 
 
-def pn_optimum_grid(t_comm, t_comp, k, b, e_loc):
-    """Exhaustive argmax over 1 <= N <= E, ties -> smaller N."""
+def pn_optimum_grid(t_comm, t_comp, k, b, e_loc, slice_max=1):
+    """Exhaustive argmax over 1 <= N <= E, ties -> smaller N.
+    slice_max > 1 adds the token-sliced candidates N = E * S, S = 2..slice_max
+    (R8 extension: chunks beyond one expert per chunk split the tokens)."""
+    cands = list(range(1, e_loc + 1)) + [e_loc * s for s in range(2, slice_max + 1)]
     best_n, best_v = 1, pn_objective(1, t_comm, t_comp, k, b)
-    for n in range(2, e_loc + 1):
+    for n in cands[1:]:
         v = pn_objective(n, t_comm, t_comp, k, b)
         if v > best_v:
             best_n, best_v = n, v

@@ -50,7 +50,7 @@ class moe_plan_t(C.Structure):
         n = self.num_chunks
         return dict(num_chunks=n, token_slices=self.token_slices, gemm_kind=self.gemm_kind,
                     sm_gemm=self.sm_gemm, comm_ctas=self.comm_ctas,
-                    group_begin=list(self.group_begin[:n + 1]),
+                    group_begin=list(self.group_begin[:n // max(1, self.token_slices) + 1]),
                     pred_comm_ms=self.pred_comm_ms, pred_comp_ms=self.pred_comp_ms,
                     pred_k_ms=self.pred_k_ms, pred_b_ms=self.pred_b_ms, pred_gain_ms=self.pred_gain_ms,
                     tile_m=self.tile_m)
@@ -163,11 +163,12 @@ def exchange_layout(cfg: moe_config_t, plan: moe_plan_t, global_hist):
     return send_off, recv_off, cs, cr
 
 
-def make_plan(num_chunks=1,gemm_kind=MOE_GEMM_GROUPED, sm_gemm=0, comm_ctas=0, tile_m=0):
+def make_plan(num_chunks=1, gemm_kind=MOE_GEMM_GROUPED, sm_gemm=0, comm_ctas=0, tile_m=0, token_slices=1):
+    """num_chunks = PN = expert groups x token_slices (chunk c = group c // S, slice c % S)."""
     p = moe_plan_t()
     p.tile_m = tile_m
     p.num_chunks = num_chunks
-    p.token_slices = 1
+    p.token_slices = token_slices
     p.gemm_kind = gemm_kind
     p.sm_gemm = sm_gemm
     p.comm_ctas = comm_ctas

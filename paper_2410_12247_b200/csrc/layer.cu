@@ -50,7 +50,13 @@ struct moe_layer {
   void *x_dev = nullptr, *y_dev = nullptr;  // staging for forward_host
   // host
   int32_t* ghist_host = nullptr;    // pinned [ep*E]
-  int32_t* tables_host = nullptr;   // pinned [4*256+8]: GEMM row tables; local_reduce receive tables
+  // pinned: per-chunk GEMM row tables [2][TBL] (start, count; chunk c at c*E_loc), then the
+  // local_reduce receive tables [2][256+4]
+  static constexpr int TBL = MOE_MAX_CHUNKS * MOE_MAX_EXPERTS;
+  int32_t* tables_host = nullptr;
+  // token-sliced chunks (R8 extension): per-(expert, slice) counts, local and all ranks
+  int32_t *slice_hist = nullptr, *gslice = nullptr;
+  int32_t* gslice_host = nullptr;  // pinned [ep * E * 64]
   cudaStream_t s_disp = nullptr, s_comb = nullptr;
   cudaStream_t s_side = nullptr;  // shared experts, concurrent with routing / dispatch
   cudaStream_t s_h2d = nullptr, s_d2h = nullptr;  // forward_host copy streams
@@ -189,8 +195,12 @@ size_t carve(moe_layer* L, char* base) {
   L->hist = cv.take<int32_t>(MOE_MAX_EXPERTS + 1);
   L->seg_start = cv.take<int32_t>(MOE_MAX_EXPERTS + 1);
   L->ghist = cv.take<int32_t>(D * E);
-  L->recv_start_d = cv.take<int32_t>(MOE_MAX_EXPERTS);
-  L->recv_count_d = cv.take<int32_t>(MOE_MAX_EXPERTS);
+  L->recv_start_d = cv.take<int32_t>(moe_layer::TBL);
+  L->recv_count_d = cv.take<int32_t>(moe_layer::TBL);
+  if (D > 1) {
+    L->slice_hist = cv.take<int32_t>(E * MOE_MAX_CHUNKS);
+    L->gslice = cv.take<int32_t>(D * E * MOE_MAX_CHUNKS);
+  }
   L->send = cv.take<uint16_t>(L->send_cap * H);
   L->recv = (D == 1) ? nullptr : cv.take<uint16_t>(L->recv_cap * H);
   L->h = cv.take<uint16_t>(L->gemm_rows_cap * F);
@@ -425,7 +435,10 @@ static moe_status_t create_impl(const moe_config_t* cfg, const moe_weights_t* w,
     return fail(MOE_ERR_CUDA);
   }
   if (cudaHostAlloc(&L->ghist_host, sizeof(int32_t) * cfg->ep * cfg->num_experts, cudaHostAllocDefault) != cudaSuccess ||
-      cudaHostAlloc(&L->tables_host, sizeof(int32_t) * (4 * MOE_MAX_EXPERTS + 8), cudaHostAllocDefault) != cudaSuccess ||
+      cudaHostAlloc(&L->tables_host, sizeof(int32_t) * (2 * moe_layer::TBL + 2 * (MOE_MAX_EXPERTS + 4)),
+                    cudaHostAllocDefault) != cudaSuccess ||
+      (cfg->ep > 1 && cudaHostAlloc(&L->gslice_host, sizeof(int32_t) * cfg->ep * cfg->num_experts * MOE_MAX_CHUNKS,
+                                    cudaHostAllocDefault) != cudaSuccess) ||
       cudaHostAlloc(&L->ughist_host, sizeof(int32_t) * cfg->ep * MOE_MAX_EXPERTS, cudaHostAllocDefault) != cudaSuccess) {
     set_error("cudaHostAlloc failed");
     return fail(MOE_ERR_CUDA);
@@ -560,6 +573,7 @@ moe_status_t moe_layer_destroy(moe_layer_t* L) {
   if (L->ghist_host) cudaFreeHost(L->ghist_host);
   if (L->tables_host) cudaFreeHost(L->tables_host);
   if (L->ughist_host) cudaFreeHost(L->ughist_host);
+  if (L->gslice_host) cudaFreeHost(L->gslice_host);
   delete L;
   return MOE_OK;
 }
@@ -572,6 +586,10 @@ moe_status_t moe_exchange_layout(const moe_config_t* cfg, const moe_plan_t* plan
   moe_plan_t plan = *plan_in;
   int pv = plan_normalise(*cfg, &plan);
   if (pv) { set_error("invalid plan"); return (moe_status_t)pv; }
+  if (plan.token_slices > 1) {  // per-slice counts are not derivable from ghist
+    set_error("moe_exchange_layout: token_slices > 1 needs the per-slice histogram (see moe_layer_forward)");
+    return MOE_ERR_UNSUPPORTED;
+  }
   exchange_layout(*cfg, ghist, send_off, recv_off);
   const int E = cfg->num_experts, D = cfg->ep, E_loc = E / D, me = cfg->rank;
   for (int ch = 0; ch < plan.num_chunks; ++ch)
@@ -883,13 +901,51 @@ moe_status_t moe_layer_forward(moe_layer_t* L, const void* x, int64_t T, void* y
     std::vector<int64_t> recv_off((size_t)E_loc * D + 1, 0);
     exchange_layout(c, gh, send_off.data(), recv_off.data());
     if (recv_off.back() > L->recv_cap) { set_error("recv rows exceed capacity"); return MOE_ERR_CAPACITY; }
-    for (int el = 0; el < E_loc; ++el) {
-      L->tables_host[el] = (int32_t)recv_off[(size_t)el * D];
-      L->tables_host[MOE_MAX_EXPERTS + el] = (int32_t)(recv_off[(size_t)(el + 1) * D] - recv_off[(size_t)el * D]);
+    // Token-sliced chunks (R8 extension, S > 1): chunk c = (expert group c / S,
+    // source-token slice c % S); the (expert, slice) counts of every rank take
+    // one more exchange.  Send rows stay (e, t), so (e, s) is contiguous; recv
+    // rows become (e_l, s, src, t), so each expert's rows of a chunk are.  Every
+    // row still meets the same weights and returns to the same send row, so
+    // slicing changes no bit of y.
+    const int S = plan.token_slices;
+    const int NG = plan.num_chunks / S;
+    const int32_t* hsl = gh;  // [D][E * S]
+    if (S > 1) {
+      KERNEL_TRY(launch_slice_hist(topk_idx, (int)T, k, E, S, L->slice_hist, st));
+      TR_TRY(L->tr->allgather_i32(L->slice_hist, L->gslice, E * S, st));
+      CUDA_TRY(cudaMemcpyAsync(L->gslice_host, L->gslice, sizeof(int32_t) * D * E * S, cudaMemcpyDeviceToHost, st));
+      CUDA_TRY(cudaEventRecord(L->ev_hist, st));
+      CUDA_TRY(cudaEventSynchronize(L->ev_hist));
+      hsl = L->gslice_host;
     }
-    CUDA_TRY(cudaMemcpyAsync(L->recv_start_d, L->tables_host, sizeof(int32_t) * E_loc, cudaMemcpyHostToDevice, st));
-    CUDA_TRY(cudaMemcpyAsync(L->recv_count_d, L->tables_host + MOE_MAX_EXPERTS, sizeof(int32_t) * E_loc,
-                             cudaMemcpyHostToDevice, st));
+    auto cnt = [&](int src, int ex, int sl) -> int64_t { return hsl[((int64_t)src * E + ex) * S + sl]; };
+    std::vector<int64_t> send_pos((size_t)E * S);
+    for (int ex = 0; ex < E; ++ex) {
+      int64_t p0 = send_off[ex];
+      for (int sl = 0; sl < S; ++sl) {
+        send_pos[(size_t)ex * S + sl] = p0;
+        p0 += cnt(me, ex, sl);
+      }
+    }
+    std::vector<int64_t> recv_pos((size_t)E_loc * S * D + 1, 0);  // (e_l, s, src)
+    for (int el = 0, i = 0; el < E_loc; ++el)
+      for (int sl = 0; sl < S; ++sl)
+        for (int src = 0; src < D; ++src, ++i) recv_pos[i + 1] = recv_pos[i] + cnt(src, me * E_loc + el, sl);
+    auto rpos = [&](int el, int sl, int src) -> int64_t { return recv_pos[((size_t)el * S + sl) * D + src]; };
+    // per-chunk GEMM row tables: chunk c's experts at [c * E_loc + e_l]
+    int32_t* tstart = L->tables_host;
+    int32_t* tcount = L->tables_host + moe_layer::TBL;
+    for (int ch = 0; ch < plan.num_chunks; ++ch) {
+      const int grp = ch / S, sl = ch % S;
+      for (int el = plan.group_begin[grp]; el < plan.group_begin[grp + 1]; ++el) {
+        tstart[ch * E_loc + el] = (int32_t)rpos(el, sl, 0);
+        tcount[ch * E_loc + el] = (int32_t)(rpos(el, sl, D - 1) + cnt(D - 1, me * E_loc + el, sl) - rpos(el, sl, 0));
+      }
+    }
+    const size_t tbytes = sizeof(int32_t) * (size_t)plan.num_chunks * E_loc;
+    CUDA_TRY(cudaMemcpyAsync(L->recv_start_d, tstart, tbytes, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemcpyAsync(L->recv_count_d, tcount, tbytes, cudaMemcpyHostToDevice, st));
+    (void)NG;
     // ---- local_reduce (R16): the dedup layout needs the plan's chunks, and the
     // unique-row counts per (chunk, peer) need a second (G-int) exchange
     const int G = plan.num_chunks * D;
@@ -920,7 +976,7 @@ moe_status_t moe_layer_forward(moe_layer_t* L, const void* x, int64_t T, void* y
         }
       urecv[G] = row;
       if (row > L->recv_cap) { set_error("unique recv rows exceed capacity"); return MOE_ERR_CAPACITY; }
-      int32_t* tb = L->tables_host + 2 * MOE_MAX_EXPERTS;  // [E_loc*D+1] recv_off, then [G+1] urecv
+      int32_t* tb = L->tables_host + 2 * moe_layer::TBL;  // [E_loc*D+1] recv_off, then [G+1] urecv
       for (int i = 0; i <= E_loc * D; ++i) tb[i] = (int32_t)recv_off[i];
       for (int i = 0; i <= G; ++i) tb[MOE_MAX_EXPERTS + 4 + i] = (int32_t)urecv[i];
       CUDA_TRY(cudaMemcpyAsync(L->lr_recv_off_d, tb, sizeof(int32_t) * (E_loc * D + 1), cudaMemcpyHostToDevice, st));
@@ -937,7 +993,7 @@ moe_status_t moe_layer_forward(moe_layer_t* L, const void* x, int64_t T, void* y
     const size_t drow = fp8 ? (size_t)L->qpitch : row_bytes;
     const size_t meta_bytes = (size_t)2 * k * sizeof(int32_t);
     auto dispatch = [&](int ch) -> moe_status_t {
-      int g0 = plan.group_begin[ch], g1 = plan.group_begin[ch + 1];
+      const int sl = ch % S, g0 = plan.group_begin[ch / S], g1 = plan.group_begin[ch / S + 1];
       int d0 = prof_rec(L, L->s_disp);
       TR_TRY(L->tr->group_start(0));
       if (lr_ep) {  // one unique-row message + its meta per peer (R16)
@@ -957,12 +1013,12 @@ moe_status_t moe_layer_forward(moe_layer_t* L, const void* x, int64_t T, void* y
       }
       for (int peer = 0; peer < D && !lr_ep; ++peer)
         for (int el = g0; el < g1; ++el) {
-          int ex = peer * E_loc + el;
-          int64_t n_send = gh[(int64_t)me * E + ex];
-          if (n_send) TR_TRY(L->tr->send(dsend + send_off[ex] * drow, n_send * drow, peer, 0, L->s_disp));
-          int64_t n_recv = gh[(int64_t)peer * E + me * E_loc + el];
-          if (n_recv)
-            TR_TRY(L->tr->recv(drecv + recv_off[(size_t)el * D + peer] * drow, n_recv * drow, peer, 0, L->s_disp));
+          const int ex = peer * E_loc + el;
+          const int64_t n_send = cnt(me, ex, sl);
+          if (n_send)
+            TR_TRY(L->tr->send(dsend + send_pos[(size_t)ex * S + sl] * drow, n_send * drow, peer, 0, L->s_disp));
+          const int64_t n_recv = cnt(peer, me * E_loc + el, sl);
+          if (n_recv) TR_TRY(L->tr->recv(drecv + rpos(el, sl, peer) * drow, n_recv * drow, peer, 0, L->s_disp));
         }
       TR_TRY(L->tr->group_end(0, L->s_disp));
       prof_mark(L, MOE_STAGE_DISPATCH, d0, prof_rec(L, L->s_disp));
@@ -970,7 +1026,7 @@ moe_status_t moe_layer_forward(moe_layer_t* L, const void* x, int64_t T, void* y
       return MOE_OK;
     };
     auto combine_send = [&](int ch) -> moe_status_t {
-      int g0 = plan.group_begin[ch], g1 = plan.group_begin[ch + 1];
+      const int sl = ch % S, g0 = plan.group_begin[ch / S], g1 = plan.group_begin[ch / S + 1];
       CUDA_TRY(cudaStreamWaitEvent(L->s_comb, L->ev_gemm[ch], 0));
       int b0 = prof_rec(L, L->s_comb);
       TR_TRY(L->tr->group_start(1));
@@ -984,38 +1040,44 @@ moe_status_t moe_layer_forward(moe_layer_t* L, const void* x, int64_t T, void* y
       }
       for (int peer = 0; peer < D && !lr_ep; ++peer)
         for (int el = g0; el < g1; ++el) {
-          int64_t n_back = gh[(int64_t)peer * E + me * E_loc + el];
+          const int64_t n_back = cnt(peer, me * E_loc + el, sl);
           if (n_back)
-            TR_TRY(L->tr->send((char*)L->o + recv_off[(size_t)el * D + peer] * row_bytes, n_back * row_bytes, peer, 1,
-                               L->s_comb));
-          int ex = peer * E_loc + el;
-          int64_t n_home = gh[(int64_t)me * E + ex];
+            TR_TRY(L->tr->send((char*)L->o + rpos(el, sl, peer) * row_bytes, n_back * row_bytes, peer, 1, L->s_comb));
+          const int ex = peer * E_loc + el;
+          const int64_t n_home = cnt(me, ex, sl);
           if (n_home)
-            TR_TRY(L->tr->recv((char*)L->comb + send_off[ex] * row_bytes, n_home * row_bytes, peer, 1, L->s_comb));
+            TR_TRY(L->tr->recv((char*)L->comb + send_pos[(size_t)ex * S + sl] * row_bytes, n_home * row_bytes, peer, 1,
+                               L->s_comb));
         }
       TR_TRY(L->tr->group_end(1, L->s_comb));
       prof_mark(L, MOE_STAGE_COMB_A2A, b0, prof_rec(L, L->s_comb));
       return MOE_OK;
     };
     auto compute = [&](int ch) -> moe_status_t {
-      int g0 = plan.group_begin[ch], g1 = plan.group_begin[ch + 1];
+      const int sl = ch % S, g0 = plan.group_begin[ch / S], g1 = plan.group_begin[ch / S + 1];
       CUDA_TRY(cudaStreamWaitEvent(st, L->ev_disp[ch], 0));
       const int64_t u0 = urecv[(size_t)ch * D], u1 = urecv[(size_t)(ch + 1) * D];
       if (lr_ep) {  // unique rows -> expert-major GEMM rows (R6 order, so the GEMMs are unchanged)
         KERNEL_TRY(launch_lr_expand(L->recvu, fp8 ? L->recvq : nullptr, L->qpitch, u0, u1, H, k, D, ch, L->lr_usrc_d,
                                     L->lr_recv_off_d, L->meta_recv, L->recv, st));
-      } else if (fp8) {  // the chunk's received rows are contiguous in the recv layout (R6)
-        const int64_t r0 = recv_off[(size_t)g0 * D], r1 = recv_off[(size_t)g1 * D];
-        KERNEL_TRY(launch_dequant_rows(drecv + r0 * drow, r1 - r0, H, L->qpitch, (char*)L->recv + r0 * row_bytes, st));
+      } else if (fp8) {  // the chunk's rows: one range per expert, merged where contiguous (all, if S == 1)
+        int el = g0;
+        while (el < g1) {
+          const int64_t r0 = rpos(el, sl, 0);
+          int64_t r1 = rpos(el, sl, D - 1) + cnt(D - 1, me * E_loc + el, sl);
+          while (++el < g1 && rpos(el, sl, 0) == r1) r1 = rpos(el, sl, D - 1) + cnt(D - 1, me * E_loc + el, sl);
+          KERNEL_TRY(launch_dequant_rows(drecv + r0 * drow, r1 - r0, H, L->qpitch, (char*)L->recv + r0 * row_bytes,
+                                         st));
+        }
       }
       int a = g0;
       while (a < g1) {
         int b = a + 1;
         while (b < g1 && plan.expert_kind[b] == plan.expert_kind[a]) ++b;
         double rows = 0;
-        for (int el = a; el < b; ++el) rows += L->tables_host[MOE_MAX_EXPERTS + el];
-        int err = compute_moe(L, L->recv, L->recv_cap, L->recv_start_d, L->recv_count_d, a, b, plan.expert_kind[a],
-                              num_ctas, pick_cta_pair(plan, rows / (b - a)), st);
+        for (int el = a; el < b; ++el) rows += tcount[ch * E_loc + el];
+        int err = compute_moe(L, L->recv, L->recv_cap, L->recv_start_d + ch * E_loc, L->recv_count_d + ch * E_loc,
+                              a, b, plan.expert_kind[a], num_ctas, pick_cta_pair(plan, rows / (b - a)), st);
         if (err) { set_error(std::string("ComputeMoE: ") + cudaGetErrorString((cudaError_t)err)); return MOE_ERR_CUDA; }
         a = b;
       }

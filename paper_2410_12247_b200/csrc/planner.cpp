@@ -4,7 +4,9 @@
 //       L(theta;N) = min{T_comm/N, T_comp/N} (N-1),  R(N) = kN + b
 //   kernel choice:   GroupGemm vs DenseGemm by per-expert load        (A8)
 //   chunks:          horizontal split, weights split by expert, each chunk a
-//                    balanced contiguous group of local experts       (R8)
+//                    balanced contiguous group of local experts       (R8);
+//                    beyond N = E_loc, every expert group is split further
+//                    into S token slices (N = E_loc * S, R8 extension)
 #include <algorithm>
 #include <cmath>
 #include <cstring>
@@ -67,6 +69,14 @@ static void balanced_groups(int e_loc, int n, int32_t* begin) {
   }
 }
 
+// Largest token-slice count the planner considers: chunks stay <= 64, slices
+// <= 8 and >= 256 source tokens each (smaller slices re-read the group's
+// weights for too few rows).
+int plan_slice_max(int e_loc, int64_t t_loc) {
+  int s = std::min<int64_t>(8, std::min<int64_t>(MOE_MAX_CHUNKS / e_loc, t_loc / 256));
+  return std::max(1, s);
+}
+
 int plan_compute(const moe_config_t& cfg, const moe_cost_model_t& cost, int64_t global_tokens,
                  const int32_t* ghist, moe_plan_t* out) {
   const int E = cfg.num_experts, D = cfg.ep, k = cfg.top_k;
@@ -116,17 +126,22 @@ int plan_compute(const moe_config_t& cfg, const moe_cost_model_t& cost, int64_t 
     t_comm = 2.0 * one;                                   // dispatch + combine
   }
 
-  // pipeline number; ties -> smaller N
+  // pipeline number over N = 1..E_loc, then N = E_loc * S token-
+  // sliced chunks (S = 2..slice_max, R8 extension); ties -> smaller N
   const double C = std::min(t_comm, t_comp);
   const int n_max = std::min(E_loc, MOE_MAX_CHUNKS);
   int best_n = 1;
   double best_v = -(cost.k_ms * 1 + cost.b_ms);
-  for (int n = 2; n <= n_max; ++n) {
+  auto consider = [&](int n) {
     double v = C / n * (n - 1) - (cost.k_ms * n + cost.b_ms);
     if (v > best_v) { best_v = v; best_n = n; }
-  }
+  };
+  for (int n = 2; n <= n_max; ++n) consider(n);
+  const int s_max = (D > 1 && !cfg.local_reduce) ? plan_slice_max(E_loc, global_tokens / D) : 1;
+  for (int s = 2; s <= s_max; ++s) consider(E_loc * s);
   out->num_chunks = best_n;
-  balanced_groups(E_loc, best_n, out->group_begin);
+  out->token_slices = best_n > E_loc ? best_n / E_loc : 1;
+  balanced_groups(E_loc, best_n / out->token_slices, out->group_begin);
   out->gemm_kind = MOE_GEMM_AUTO;
   out->sm_gemm = 0;
   out->comm_ctas = 0;
@@ -143,11 +158,19 @@ int plan_compute(const moe_config_t& cfg, const moe_cost_model_t& cost, int64_t 
 int plan_normalise(const moe_config_t& cfg, moe_plan_t* p) {
   const int E_loc = cfg.num_experts / cfg.ep;
   if (p->token_slices < 1) p->token_slices = 1;
-  if (p->token_slices != 1) return MOE_ERR_UNSUPPORTED;
-  if (p->num_chunks < 1 || p->num_chunks > std::min(E_loc, MOE_MAX_CHUNKS)) return MOE_ERR_INVALID;
-  bool ok = p->group_begin[0] == 0 && p->group_begin[p->num_chunks] == E_loc;
-  for (int c = 0; ok && c < p->num_chunks; ++c) ok = p->group_begin[c + 1] > p->group_begin[c];
-  if (!ok) balanced_groups(E_loc, p->num_chunks, p->group_begin);
+  const int S = p->token_slices;
+  if (p->num_chunks < 1 || p->num_chunks > MOE_MAX_CHUNKS || p->num_chunks % S) return MOE_ERR_INVALID;
+  const int NG = p->num_chunks / S;  // expert groups; chunk c = group c / S, slice c % S (R8)
+  if (NG > E_loc) return MOE_ERR_INVALID;
+  if (S > 1 && (cfg.ep == 1 || cfg.local_reduce)) {
+    // ep == 1 has no all2all to pipeline; R16's groups assume expert-only chunks
+    if (cfg.local_reduce && cfg.ep > 1) return MOE_ERR_UNSUPPORTED;
+    p->token_slices = 1;
+    p->num_chunks = NG;
+  }
+  bool ok = p->group_begin[0] == 0 && p->group_begin[NG] == E_loc;
+  for (int c = 0; ok && c < NG; ++c) ok = p->group_begin[c + 1] > p->group_begin[c];
+  if (!ok) balanced_groups(E_loc, NG, p->group_begin);
   if (p->gemm_kind != MOE_GEMM_AUTO)
     for (int e = 0; e < E_loc; ++e) p->expert_kind[e] = (uint8_t)p->gemm_kind;
   else

@@ -385,6 +385,19 @@ combine_kernel(const __nv_bfloat16* __restrict__ o, const __nv_bfloat16* __restr
   }
 }
 
+// Pairs per (expert, token slice) for token-sliced chunks (R8 extension):
+// slice s of T tokens = balanced contiguous ranges, the first T mod S one
+// token longer.  Order-free counts (atomics on a zeroed array).
+__global__ void __launch_bounds__(256) slice_hist_kernel(const int32_t* __restrict__ topk_idx, int T, int k, int S,
+                                                         int32_t* __restrict__ hs) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (int64_t)T * k) return;
+  const int t = (int)(i / k);
+  const int base = T / S, rem = T % S;
+  const int s = (t < rem * (base + 1)) ? t / (base + 1) : rem + (t - rem * (base + 1)) / base;
+  atomicAdd(&hs[topk_idx[i] * S + s], 1);
+}
+
 // Zero-pad copy of the router weight into a [256, H] buffer (create time).
 __global__ void pad_rows_kernel(const __nv_bfloat16* __restrict__ src, int rows, int H,
                                 __nv_bfloat16* __restrict__ dst, int rows_pad) {
@@ -459,6 +472,15 @@ int launch_combine(const void* o, const void* s, int T, int H, int k, const int3
   combine_kernel<<<(T + WARPS - 1) / WARPS, WARPS * 32, 0, st>>>((const __nv_bfloat16*)o,
                                                                  (const __nv_bfloat16*)s, T, H, k, pos, topk_w,
                                                                  (__nv_bfloat16*)y);
+  return (int)cudaGetLastError();
+}
+
+int launch_slice_hist(const int32_t* topk_idx, int T, int k, int E, int S, int32_t* hs, cudaStream_t st) {
+  cudaError_t e = cudaMemsetAsync(hs, 0, sizeof(int32_t) * E * S, st);
+  if (e != cudaSuccess) return (int)e;
+  if (T == 0) return 0;
+  const int64_t n = (int64_t)T * k;
+  slice_hist_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(topk_idx, T, k, S, hs);
   return (int)cudaGetLastError();
 }
 

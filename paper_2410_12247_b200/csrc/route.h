@@ -25,6 +25,8 @@ int launch_dequant_rows(const void* q, int64_t rows, int H, int qpitch, void* ou
 inline int fp8_row_pitch(int H) { return ((H + H / 128) + 15) & ~15; }
 int launch_combine(const void* o, const void* s, int T, int H, int k, const int32_t* pos, const float* topk_w,
                    void* y, cudaStream_t st);
+// hs[e * S + s] = pairs of expert e among the tokens of slice s (token-sliced chunks, R8)
+int launch_slice_hist(const int32_t* topk_idx, int T, int k, int E, int S, int32_t* hs, cudaStream_t st);
 int launch_pad_rows(const void* src, int rows, int H, void* dst, int rows_pad, cudaStream_t st);
 
 }  // namespace epsmoe

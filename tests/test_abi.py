@@ -99,10 +99,15 @@ def test_planner_matches_oracle_pn_rule():
         T = int(rng.integers(1000, 100000))
         hist = rng.multinomial(T * k // D, np.ones(E) / E, size=D).astype(np.int32)
         plan = abi.plan_compute(cfg, T, hist, c)
-        n_ref, _ = oracle.pn_optimum_grid(plan.pred_comm_ms, plan.pred_comp_ms, c.k_ms, c.b_ms, E // D)
+        E_loc = E // D
+        # token slices (R8 extension): <= 8, <= 64 chunks, >= 256 tokens per slice
+        s_max = max(1, min(8, 64 // E_loc, (T // D) // 256)) if D > 1 else 1
+        n_ref, _ = oracle.pn_optimum_grid(plan.pred_comm_ms, plan.pred_comp_ms, c.k_ms, c.b_ms, E_loc, s_max)
         assert plan.num_chunks == n_ref
-        g = plan.group_begin[:plan.num_chunks + 1]
-        assert list(g) == oracle.chunk_groups(E // D, plan.num_chunks).tolist()
+        S = plan.token_slices
+        assert S == (n_ref // E_loc if n_ref > E_loc else 1)
+        g = plan.group_begin[:plan.num_chunks // S + 1]
+        assert list(g) == oracle.chunk_groups(E_loc, plan.num_chunks // S).tolist()
         if D == 1:
             assert plan.num_chunks == 1 and plan.pred_comm_ms == 0.0   # no all2all -> nothing to hide
 
@@ -156,3 +161,20 @@ def test_exchange_layout_matches_oracle_single_process():
             assert recv_off[-1] == lay["recv_total"][r]
             assert np.array_equal(cs, res["send_counts"][:, r, :])
             assert np.array_equal(cr, res["send_counts"][:, :, r])
+
+
+def test_planner_token_slices_when_one_expert_per_rank():
+    """Mixtral at EP = 8 has E_loc = 1: without token slices no chunking is
+    possible; with a communication-heavy cost model the planner splits tokens."""
+    cfg = abi.make_config(8, 2, 4096, 14336, ep=8, max_tokens=1 << 16)
+    c = _cost(k_ms=0.02, b_ms=0.0)
+    for kind in (0, 1):
+        c.gemm_ms[kind][0], c.gemm_ms[kind][1] = 1.0, 100.0
+    c.a2a_gbps = 50.0
+    hist = np.full((8, 8), 16384 * 2 // 8 // 8, np.int32)
+    plan = abi.plan_compute(cfg, 16384, hist, c)
+    assert plan.token_slices > 1 and plan.num_chunks == plan.token_slices
+    assert plan.group_begin[0] == 0 and plan.group_begin[1] == 1
+    # local_reduce keeps expert-only chunks (R16)
+    cfg_lr = abi.make_config(8, 2, 4096, 14336, ep=8, max_tokens=1 << 16, local_reduce=1)
+    assert abi.plan_compute(cfg_lr, 16384, hist, c).num_chunks == 1

@@ -244,3 +244,24 @@ def test_device_limited_routing_with_local_reduce_one_row_per_token():
     assert_close(y, ref["y"], "device-limited M=1 + LR")
     for L in layers:
         L.close()
+
+
+# ---------------------------------------------------------------- token-sliced chunks (R8 extension)
+
+@pytest.mark.parametrize("E,k,D,N,S,fp8", [(4, 2, 4, 1, 3, False), (16, 4, 2, 8, 2, False),
+                                           (8, 2, 8, 1, 4, True), (16, 4, 4, 2, 3, False)])
+def test_token_sliced_chunks_equal_unchunked(E, k, D, N, S, fp8):
+    """Expert groups x source-token slices (Mixtral at EP = 8 has one expert
+    per rank, so only slices can pipeline it): the extra (expert, slice) count
+    exchange, the (e_l, slice, src, t) receive layout and per-chunk GEMM tables
+    leave y bit-identical to EP = 1, and the oracle's sliced simulation agrees."""
+    inp = Inputs(E=E, k=k, H=256, F=256, S=1, Fs=128, T=811, seed=90 + S, grid=True)
+    y, bufs = _ep_forward(inp, k, 1, D, make_plan(N * S, MOE_GEMM_GROUPED, token_slices=S), fp8=fp8)
+    for b in bufs:
+        assert b["plan_used"].token_slices == S and b["plan_used"].num_chunks == N * S
+    y1 = _ep1_forward(inp, k, 1, make_plan(1, MOE_GEMM_GROUPED), fp8=fp8)
+    assert np.array_equal(y, y1)
+    ref = oracle.moe_layer(inp.x, inp.w_router, inp.w_gate, inp.w_up, inp.w_down, k=k, norm_topk=1,
+                           ws_gate_bits=inp.ws_gate, ws_up_bits=inp.ws_up, ws_down_bits=inp.ws_down, D=D, N=N,
+                           token_slices=S, dispatch_fp8=fp8)
+    assert_close(y, ref["y"], f"sliced EP{D} N{N} S{S}")
