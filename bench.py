@@ -52,6 +52,11 @@ def parse():
     p.add_argument("--cpu-sample", type=int, default=0, help="oracle sample tokens (0 = auto)")
     p.add_argument("--e2e-steps", type=int, default=5)
     p.add_argument("--seed", type=int, default=20241016)
+    p.add_argument("--dispatch-fp8", action="store_true", help="FP8 e4m3 dispatch payload (NEXT-2, R15)")
+    p.add_argument("--local-reduce", action="store_true", help="expert-side LocalReduce + dedup (NEXT-3, R16)")
+    p.add_argument("--route-groups", type=int, default=0, help="device-limited routing groups (NEXT-4, R17)")
+    p.add_argument("--route-topk-groups", type=int, default=0, help="M: groups a token may use (R17)")
+    p.add_argument("--token-slices", type=int, default=1, help="with --chunks: chunks = groups x slices (R8)")
     return p.parse_args()
 
 
@@ -169,17 +174,19 @@ def oracle_sample(cfg, seed, n_tokens, token0=0, skew=0.0, device_gen=False):
     return inp, expert_weights, cache
 
 
-def run_oracle_timed(cfg, inp, expert_weights, cache):
+def run_oracle_timed(cfg, inp, expert_weights, cache, opts=None):
     import oracle
+    o = opts or {}
+    rg = dict(route_groups=o.get("route_groups", 0), route_topk_groups=o.get("route_topk_groups", 0))
     # pre-generate the experts these tokens route to (generation is not timed)
     idx, _ = oracle.topk_gating(oracle.router_logits(inp.x, inp.w_router, inp.router_bias), cfg["k"],
-                                cfg["norm_topk"])
+                                cfg["norm_topk"], **rg)
     for e in np.unique(idx):
         expert_weights(int(e))
     shared = (inp.ws_gate, inp.ws_up, inp.ws_down) if cfg["S"] else None
     t0 = time.perf_counter()
     oracle.moe_tokens(inp.x, inp.w_router, expert_weights, cfg["k"], cfg["norm_topk"], shared=shared,
-                      router_bias=inp.router_bias)
+                      router_bias=inp.router_bias, dispatch_fp8=o.get("dispatch_fp8", False), **rg)
     return time.perf_counter() - t0
 
 
@@ -190,12 +197,18 @@ def host_cores():
         return os.cpu_count()
 
 
-def cpu_baseline(cfg, seed, skew, sample=0):
+def feature_opts(args):
+    """The layer options a run uses (both arms see the same workload)."""
+    return dict(dispatch_fp8=bool(args.dispatch_fp8), local_reduce=bool(args.local_reduce),
+                route_groups=int(args.route_groups), route_topk_groups=int(args.route_topk_groups))
+
+
+def cpu_baseline(cfg, seed, skew, sample=0, opts=None):
     # sized for ~10-20 s of oracle work on a 16-core host (the contract's bounded sample)
     n = sample or {"tiny": 256, "dsv2_lite": 256, "mixtral": 24, "dsv2": 48, "dsv2_decode": 48,
                    "mixtral_decode": 24}.get(cfg["name"], 32)
     inp, ew, cache = oracle_sample(cfg, seed, n, 0, skew, device_gen=True)
-    dt = run_oracle_timed(cfg, inp, ew, cache)
+    dt = run_oracle_timed(cfg, inp, ew, cache, opts)
     return {"value": n / dt, "unit": UNIT, "cores": host_cores(), "kind": "oracle",
             "sample": f"first {n} tokens of the {cfg['name']} workload (all their experts + shared), "
                       f"contract mode fp64 numpy, {dt:.1f} s"}
@@ -210,7 +223,7 @@ def reference_arm(args, cfg):
     inp, ew, cache = oracle_sample(cfg, args.seed, n, 0, args.skew)
     times = []
     for i in range(args.warmup + args.steps):
-        dt = run_oracle_timed(cfg, inp, ew, cache)
+        dt = run_oracle_timed(cfg, inp, ew, cache, feature_opts(args))
         if i >= args.warmup:
             times.append(dt)
     ms = 1e3 * sum(times) / len(times)
@@ -220,7 +233,7 @@ def reference_arm(args, cfg):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": cfg["name"], "tokens_per_step": n, "E": cfg["E"], "k": cfg["k"], "H": cfg["H"],
-                       "F": cfg["F"], "shared": cfg["S"], "skew": args.skew},
+                       "F": cfg["F"], "shared": cfg["S"], "skew": args.skew, **feature_opts(args)},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
                              "sample": f"{n} tokens per step of the {cfg['name']} workload"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -286,12 +299,14 @@ def ours(args, cfg):
         ids = [MoELayer.unique_id(), MoELayer.unique_id()] if rank == 0 else [None, None]
         dist.broadcast_object_list(ids, src=0)
         uid_d, uid_c = ids
+    opts = feature_opts(args)
     layer = MoELayer(E, k, H, F, w, S=S, Fs=Fs, ep=D, rank=rank, max_tokens=T_loc, norm_topk=cfg["norm_topk"],
-                     uid_dispatch=uid_d, uid_combine=uid_c, device=dev)
+                     uid_dispatch=uid_d, uid_combine=uid_c, device=dev, **opts)
     plan = None
     if args.chunks or args.kind != "auto" or args.sm_gemm or args.tile_m:
         kind = {"auto": MOE_GEMM_AUTO, "grouped": MOE_GEMM_GROUPED, "dense": MOE_GEMM_DENSE}[args.kind]
-        plan = make_plan(max(1, args.chunks), kind, args.sm_gemm, tile_m=args.tile_m)
+        plan = make_plan(max(1, args.chunks), kind, args.sm_gemm, tile_m=args.tile_m,
+                         token_slices=args.token_slices if args.chunks else 1)
         if not args.chunks:
             plan.num_chunks = layer.plan(T).num_chunks
     stream = torch.cuda.current_stream(dev)
@@ -371,11 +386,22 @@ def ours(args, cfg):
     # ---- layer roofline: max(expert+shared+router FLOPs / peak, all2all bytes / NVLink), max over ranks
     flops_rank = [6.0 * H * F * rl + 6.0 * H * SF * (starts[r + 1] - starts[r]) + 2.0 * H * E * (starts[r + 1] - starts[r])
                   for r, rl in enumerate(rows_local)]
+    # rows each rank sends each peer: per (token, expert) pair, or per (token, rank, chunk) under R16
+    rows_to = np.zeros((D, D), np.int64)                      # [src, dst]
+    for r in range(D):
+        rows_to[r] = ghist[r].reshape(D, E_loc).sum(axis=1)
+    if opts["local_reduce"] and D > 1:
+        mine = torch.from_numpy(bufs["lr_hist"].cpu().numpy()[:plan_used["num_chunks"] * D].reshape(-1, D)
+                                .sum(axis=0).astype(np.int64)).to(dev)
+        allr = [torch.empty_like(mine) for _ in range(D)]
+        dist.all_gather(allr, mine)
+        rows_to = torch.stack(allr).cpu().numpy()
+    row_disp = ((H + H // 128 + 15) & ~15) if opts["dispatch_fp8"] else 2 * H   # wire bytes per dispatched row
     a2a_bytes = []
     for r in range(D):
-        sent = int(ghist[r].sum() - ghist[r, r * E_loc:(r + 1) * E_loc].sum())
-        recv = int(ghist[:, r * E_loc:(r + 1) * E_loc].sum() - ghist[r, r * E_loc:(r + 1) * E_loc].sum())
-        a2a_bytes.append(2.0 * H * 2 * max(sent, recv))
+        sent = int(rows_to[r].sum() - rows_to[r, r])
+        recv = int(rows_to[:, r].sum() - rows_to[r, r])
+        a2a_bytes.append((row_disp + 2 * H) * max(sent, recv))
     nvl = float(peaks.get("nvlink_gbs", FALLBACK_PEAKS["nvlink_gbs"]))
     hbm = float(peaks.get("hbm_gbs", FALLBACK_PEAKS["hbm_gbs"]))
     # HBM floor (decode-regime batches are weight-streaming): every activated expert's weights, the
@@ -417,7 +443,7 @@ def ours(args, cfg):
     stages = {n: round(v / args.steps, 4) for n, v in stage_sum.items()}
     cpu = None
     if rank == 0 and D == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(cfg, seed, args.skew, args.cpu_sample)
+        cpu = cpu_baseline(cfg, seed, args.skew, args.cpu_sample, opts)
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": D, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
@@ -426,7 +452,7 @@ def ours(args, cfg):
                 "config": {"workload": cfg["name"], "E": E, "k": k, "H": H, "F": F, "shared": S, "shared_ffn": Fs,
                            "global_tokens": T, "ep": D, "parallelism": f"ep{D}" + (f"+dp{D}" if D > 1 else ""),
                            "skew": args.skew, "l2": "inputs > L2 (x alone %.0f MB), no flush" % (T_loc * H * 2 / 1e6),
-                           "plan": plan_used},
+                           **opts, "plan": plan_used},
                 "roofline": roofline, "layer_roofline": layer_roofline,
                 "exposed_a2a_ms": stages.get("exposed_a2a", 0.0), "stages_ms": stages,
                 "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk}
