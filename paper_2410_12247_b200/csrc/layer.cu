@@ -60,7 +60,8 @@ struct moe_layer {
   cudaStream_t s_disp = nullptr, s_comb = nullptr;
   cudaStream_t s_side = nullptr;  // shared experts, concurrent with routing / dispatch
   cudaStream_t s_h2d = nullptr, s_d2h = nullptr;  // forward_host copy streams
-  cudaEvent_t ev_host_start = nullptr, ev_in[4] = {}, ev_out[4] = {};
+  static constexpr int MAX_HOST_SLICES = 8;
+  cudaEvent_t ev_host_start = nullptr, ev_in[MAX_HOST_SLICES] = {}, ev_out[MAX_HOST_SLICES] = {};
   cudaEvent_t ev_router = nullptr, ev_shared = nullptr;
   // ep == 1 with shared experts, how the shared DownGemm meets the combine
   // (EPSMOE_FUSE_COMBINE): 0 in order (default); 1 one kernel (EPI_COMBINE
@@ -458,7 +459,7 @@ static moe_status_t create_impl(const moe_config_t* cfg, const moe_weights_t* w,
     set_error("copy stream creation failed");
     return fail(MOE_ERR_CUDA);
   }
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < moe_layer::MAX_HOST_SLICES; ++i)
     if (cudaEventCreateWithFlags(&L->ev_in[i], cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&L->ev_out[i], cudaEventDisableTiming) != cudaSuccess) {
       set_error("event creation failed");
@@ -556,7 +557,7 @@ moe_status_t moe_layer_destroy(moe_layer_t* L) {
   if (L->s_h2d) cudaStreamDestroy(L->s_h2d);
   if (L->s_d2h) cudaStreamDestroy(L->s_d2h);
   if (L->ev_host_start) cudaEventDestroy(L->ev_host_start);
-  for (int i = 0; i < 4; ++i) {
+  for (int i = 0; i < moe_layer::MAX_HOST_SLICES; ++i) {
     if (L->ev_in[i]) cudaEventDestroy(L->ev_in[i]);
     if (L->ev_out[i]) cudaEventDestroy(L->ev_out[i]);
   }
@@ -1142,6 +1143,43 @@ moe_status_t moe_layer_forward(moe_layer_t* L, const void* x, int64_t T, void* y
   return MOE_OK;
 }
 
+// Token-slice schedule of moe_layer_forward_host: relative slice sizes chosen
+// from a small family by simulating the three-stream pipeline (H2D copy ->
+// layer -> D2H copy, each stream in order) with a model of this config:
+// PCIe ~50 GB/s each way; layer time per token from its FLOPs at ~1.25 PF/s,
+// inflated by the 256-row tile padding of a slice's rows per expert, plus a
+// fixed ~0.3 ms per forward.  A function of the config only, so every rank
+// (each slice is a collective when ep > 1) derives the same schedule.
+std::vector<double> host_slice_schedule(const moe_config_t& c) {
+  const double T = (double)c.max_tokens, H = c.hidden, F = c.ffn, k = c.top_k, E = c.num_experts;
+  const double SF = (double)c.num_shared * c.shared_ffn;
+  const double copy_tok = 2.0 * H / 50e9;
+  const double flop_tok = 6.0 * H * F * k + 6.0 * H * SF + 2.0 * H * E;
+  auto layer_time = [&](double n) {
+    const double rows = n * k * c.ep / E;  // rows per local expert (uniform routing)
+    const double eff = rows > 0 ? rows / (std::ceil(rows / 256.0) * 256.0) : 1.0;
+    return n * flop_tok / 1.25e15 / eff + 3e-4;
+  };
+  static const std::vector<std::vector<double>> family = {
+      {1}, {1, 1}, {1, 1, 1, 1}, {1, 2, 2, 1}, {1, 2, 3, 2}, {1, 3, 3, 1}, {1, 2, 3, 2, 1}, {1, 2, 4, 4, 2, 1},
+      {1, 2, 3, 3, 3, 2, 1}, {1, 1, 1, 1, 1, 1, 1, 1}};
+  std::vector<double> best = family[0];
+  double best_t = 1e30;
+  for (const auto& w : family) {
+    double wsum = 0;
+    for (double v : w) wsum += v;
+    double h_end = 0, c_end = 0, d_end = 0;
+    for (double v : w) {
+      const double n = T * v / wsum;
+      h_end += n * copy_tok;
+      c_end = std::max(c_end, h_end) + layer_time(n);
+      d_end = std::max(d_end, c_end) + n * copy_tok;
+    }
+    if (d_end < best_t * 0.99) { best_t = d_end; best = w; }  // a larger family member must win by > 1%
+  }
+  return best;
+}
+
 moe_status_t moe_layer_forward_host(moe_layer_t* L, const void* x_host, int64_t T, void* y_host,
                                     const moe_plan_t* plan, void* stream_v) {
   if (!L || T < 0 || T > L->cfg.max_tokens) { set_error("bad argument"); return MOE_ERR_INVALID; }
@@ -1152,12 +1190,30 @@ moe_status_t moe_layer_forward_host(moe_layer_t* L, const void* x_host, int64_t 
   // their own streams while the layer computes slice s.  The slice count is a
   // function of max_tokens (identical on every rank: each slice's forward is
   // a collective when ep > 1), chosen so slices keep >= 16K tokens.
-  const int S = (int)std::max<int64_t>(1, std::min<int64_t>(4, L->cfg.max_tokens / 16384));
-  const int64_t per = (T + S - 1) / S;
+  // EPSMOE_HOST_SLICES="w0,w1,..." (<= 8 relative weights) overrides the schedule.
+  std::vector<double> wts;
+  if (const char* hs = std::getenv("EPSMOE_HOST_SLICES")) {
+    for (const char* p = hs; *p && (int)wts.size() < moe_layer::MAX_HOST_SLICES;) {
+      char* end = nullptr;
+      double v = std::strtod(p, &end);
+      if (end == p) break;
+      if (v > 0) wts.push_back(v);
+      p = (*end == ',') ? end + 1 : end;
+    }
+  }
+  if (wts.empty()) wts = host_slice_schedule(L->cfg);
+  const int S = (int)wts.size();
+  std::vector<int64_t> bound(S + 1, 0);
+  double wsum = 0, acc = 0;
+  for (double v : wts) wsum += v;
+  for (int s = 0; s < S; ++s) {
+    acc += wts[s];
+    bound[s + 1] = (s + 1 == S) ? T : std::min<int64_t>(T, (int64_t)std::llround(T * acc / wsum));
+  }
   CUDA_TRY(cudaEventRecord(L->ev_host_start, st));  // x_dev / y_dev free once prior work on st is done
   CUDA_TRY(cudaStreamWaitEvent(L->s_h2d, L->ev_host_start, 0));
   for (int s = 0; s < S; ++s) {
-    const int64_t t0 = std::min(T, s * per), n = std::min(T, t0 + per) - t0;
+    const int64_t t0 = bound[s], n = bound[s + 1] - t0;
     char* xd = (char*)L->x_dev + t0 * row;
     char* yd = (char*)L->y_dev + t0 * row;
     if (n) CUDA_TRY(cudaMemcpyAsync(xd, (const char*)x_host + t0 * row, n * row, cudaMemcpyHostToDevice, L->s_h2d));
