@@ -50,6 +50,7 @@ struct GemmArgs {
   const int32_t* comb_pos;
   const float* comb_w;
   int comb_k;                  // 1..8
+  double rows_hint;            // expected rows per group (0 = unknown): picks the tile raster
 };
 
 // Launch on `stream`.  Returns a cudaError_t-compatible code (0 = success).

@@ -79,6 +79,7 @@ struct KParams {
   const int32_t* row_start;
   const int32_t* row_count;
   const int32_t* a_row_index;
+  const uint8_t* a_ptr;   // GATHER: A base (row pitch K * 2 bytes)
   int32_t* tile_counter;  // [2]: next ticket, CTAs finished (reset by the last CTA)
   const __nv_bfloat16* comb_o;  // EPI_COMBINE (see GemmArgs)
   const int32_t* comb_pos;
@@ -111,6 +112,7 @@ struct __align__(8) SmemTail {
   uint64_t empty[Cfg<CG>::STAGES];
   uint64_t tfull[2];
   uint64_t tempty[2];
+  uint64_t gfull[Cfg<CG>::STAGES];  // GATHER, peer CTA: its A copies landed (forwarded to the leader)
   uint64_t qfull[TQ];
   uint64_t qempty[TQ];
   int32_t tq[TQ];
@@ -118,7 +120,6 @@ struct __align__(8) SmemTail {
   int32_t tile_prefix[MAX_G + 1];
   int32_t gstart[MAX_G];
   int32_t gcount[MAX_G];
-  alignas(16) int32_t tok[BM];  // GATHER: physical A rows of the current tile (read as int4)
   alignas(1024) uint8_t stage_out[4][32 * 64];  // per epilogue warp: 32 rows x 32 bf16, 64-B swizzle
   int32_t comb_pos[4][32 * 8];                   // EPI_COMBINE: per epilogue warp, its rows' pos / w
   float comb_w[4][32 * 8];
@@ -305,7 +306,9 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
   }
   if (threadIdx.x == 0) {
     for (int i = 0; i < C::STAGES; ++i) {
-      ptx::mbar_init(ptx::smem_u32(&st.full[i]), 1);
+      // GATHER: + the 32 producer lanes' cp.async completions (+ the peer's forwarder)
+      ptx::mbar_init(ptx::smem_u32(&st.full[i]), GATHER ? 1 + 32 + (CG - 1) : 1);
+      ptx::mbar_init(ptx::smem_u32(&st.gfull[i]), 32);
       ptx::mbar_init(ptx::smem_u32(&st.empty[i]), 1);
     }
     for (int i = 0; i < 2; ++i) {
@@ -314,7 +317,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
     }
     for (int i = 0; i < TQ; ++i) {
       ptx::mbar_init(ptx::smem_u32(&st.qfull[i]), 1);
-      ptx::mbar_init(ptx::smem_u32(&st.qempty[i]), C::TQ_CONSUMERS);
+      ptx::mbar_init(ptx::smem_u32(&st.qempty[i]), C::TQ_CONSUMERS + ((GATHER && CG == 2) ? 1 : 0));
     }
     ptx::fence_barrier_init();
   }
@@ -361,9 +364,13 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
   if (warp == 0) {
     // ===================== TMA producer (each CTA loads its own halves) =====================
     // The leader's lane 0 fetches tickets; the peer's lane 0 consumes them.
-    // GATHER: the whole warp stages the tile's 128 physical A row indices in
-    // smem; lane 0 then issues 32 tile::gather4 loads per stage.
+    // GATHER (A rows picked by a_row_index, i.e. GateUp reading x directly):
+    // the whole warp copies A with 16-B cp.async into the swizzled stage; lane 0
+    // still TMA-loads B.
     uint32_t stage = 0, phase = 0;
+    // GATHER: this lane's A row indices of the tile, A row pitch
+    int32_t gidx[GATHER ? BM / 4 : 1];
+    const size_t a_pitch = (size_t)p.K * 2;
     while (true) {
       int t = 0;
       if (lane == 0) t = (rank == 0) ? tk.fetch() : tk.consume(true);
@@ -374,28 +381,41 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
       const int a_row = st.gstart[g] + mt * C::TILE_M + (int)rank * BM;
       const int b_row0 = (p.b_base + g) * p.b_group_rows + nt * n_out_tile;
       if constexpr (GATHER) {
-        __syncwarp();
+        // this lane's rows of the tile: chunk (lane & 7) of rows (lane >> 3) + 4 i;
+        // rows past the group's end read the group's first row (not stored)
         const int local0 = mt * C::TILE_M + (int)rank * BM;
 #pragma unroll
-        for (int i = 0; i < BM / 32; ++i) {
-          const int r = lane * (BM / 32) + i;
-          // rows past the group's end load any valid row (their results are not stored)
+        for (int i = 0; i < BM / 4; ++i) {
+          const int r = (lane >> 3) + 4 * i;
           const int src = (local0 + r < st.gcount[g]) ? a_row + r : st.gstart[g];
-          st.tok[r] = p.a_row_index[src];
+          gidx[i] = p.a_row_index[src];
         }
-        __syncwarp();
       }
-      if (lane == 0) {
+      if (GATHER || lane == 0) {
         for (int kb = 0; kb < num_kb; ++kb) {
           ptx::mbar_wait(ptx::smem_u32(&st.empty[stage]), phase ^ 1);
           const uint32_t fb = ptx::smem_u32(&st.full[stage]);
           const uint32_t a_dst = ptx::smem_u32(sA + stage * C::A_BYTES);
           const uint32_t b_dst = ptx::smem_u32(sB + stage * C::B_BYTES);
-          if (CG == 1 || rank == 0) ptx::mbar_arrive_expect_tx(fb, CG * (C::A_BYTES + C::B_BYTES));
+          if ((CG == 1 || rank == 0) && lane == 0)
+            ptx::mbar_arrive_expect_tx(fb, CG * ((GATHER ? 0 : C::A_BYTES) + C::B_BYTES));
           if constexpr (GATHER) {
-            const int4* tkr = reinterpret_cast<const int4*>(st.tok);
-#pragma unroll 8
-            for (int i = 0; i < BM / 4; ++i) ptx::tma_gather4<CG>(a_dst + i * 512, &tmA, fb, kb * BK, tkr[i]);
+            // A by 16-B cp.async straight into the 128-B swizzle (chunk c of row r at
+            // c ^ (r & 7)): 4 rows x 128 B per warp instruction, no TMA descriptor per row
+            const int c = lane & 7;
+            const uint8_t* src0 = p.a_ptr + (size_t)kb * (BK * 2) + c * 16;
+#pragma unroll
+            for (int i = 0; i < BM / 4; ++i) {
+              const int r = (lane >> 3) + 4 * i;
+              ptx::cp_async16(a_dst + r * 128 + ((c ^ (r & 7)) << 4), src0 + (size_t)gidx[i] * a_pitch);
+            }
+            // each lane's completion arrives asynchronously (no wait, no fence in this
+            // warp): on the full barrier, or in the peer on gfull for its forwarder
+            ptx::cp_async_mbar_arrive_noinc((CG == 1 || rank == 0) ? fb : ptx::smem_u32(&st.gfull[stage]));
+            if (lane != 0) {
+              if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+              continue;
+            }
           } else if constexpr (CG == 1) {
             ptx::tma_load_2d(a_dst, &tmA, fb, kb * BK, a_row);
           } else {
@@ -431,7 +451,11 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
         ptx::tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
         for (int kb = 0; kb < num_kb; ++kb) {
-          ptx::mbar_wait(ptx::smem_u32(&st.full[stage]), phase);
+          // GATHER pair: the peer's A arrives by a cluster-scope release (not a TMA
+          // complete_tx), so the wait needs cluster-scope acquire
+          if constexpr (GATHER && CG == 2) ptx::mbar_wait_cluster(ptx::smem_u32(&st.full[stage]), phase);
+          else ptx::mbar_wait(ptx::smem_u32(&st.full[stage]), phase);
+          if constexpr (GATHER) ptx::fence_proxy_async_smem();  // cp.async (generic) writes -> MMA reads
           ptx::tc_fence_after();
           const uint64_t adesc = ptx::sdesc_k_sw128(ptx::smem_u32(sA + stage * C::A_BYTES));
           const uint64_t bdesc = ptx::sdesc_k_sw128(ptx::smem_u32(sB + stage * C::B_BYTES));
@@ -450,6 +474,21 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
         if constexpr (CG == 1) ptx::mma_commit(ptx::smem_u32(&st.tfull[acc]));
         else ptx::mma_commit_pair(ptx::smem_u32(&st.tfull[acc]), 0x3);
         ++iter;
+      }
+    }
+    if constexpr (GATHER && CG == 2) {
+      // the peer's forwarder: its A copies of a stage landed (gfull) -> proxy fence ->
+      // cluster-release arrive on the leader's full barrier
+      if (lane == 0 && rank == 1) {
+        uint32_t stage = 0, phase = 0;
+        while (tk.consume(true) >= 0) {
+          for (int kb = 0; kb < num_kb; ++kb) {
+            ptx::mbar_wait(ptx::smem_u32(&st.gfull[stage]), phase);
+            ptx::fence_proxy_async_smem();
+            ptx::mbar_arrive_cluster(ptx::mapa(ptx::smem_u32(&st.full[stage]), 0));
+            if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+          }
+        }
       }
     }
   } else {
@@ -655,11 +694,22 @@ int env_int(const char* name, int dflt) {
   return e ? std::atoi(e) : dflt;
 }
 
-// Tile rasterisation block (m-tiles); 4 measured best on DSv2 and Mixtral
-// shapes (tools/gemm_bench.py); EPSMOE_RASTER_GM overrides.
-int raster_gm() {
-  static int v = std::max(1, env_int("EPSMOE_RASTER_GM", 4));
-  return v;
+// Tile rasterisation block (m-tiles).  Blocks of 4 m-tiles (n-major across
+// the block) keep a group's A and B tiles in flight together; when a group's
+// weights dwarf its rows (B > 4 A, A <= 48 MB: Mixtral's GateUp) all m-tiles
+// of an n-tile go first instead, so A stays L2-resident and B streams once
+// (measured: Mixtral GateUp DRAM reads ~4x lower, layer -4.5%; DSv2 shapes and
+// the dense shared GEMMs are faster with blocks of 4).  EPSMOE_RASTER_GM
+// overrides.
+int raster_gm(int epi, int N, int K, double rows_hint) {
+  static int v = env_int("EPSMOE_RASTER_GM", 0);
+  if (v > 0) return v;
+  if (rows_hint > 0) {
+    const double a_bytes = rows_hint * K * 2.0;
+    const double b_bytes = (epi == EPI_SWIGLU ? 2.0 : 1.0) * N * K * 2.0;
+    if (b_bytes > 4.0 * a_bytes && a_bytes <= 48e6) return 1 << 20;
+  }
+  return 4;
 }
 int dynamic_sched() {
   static int v = env_int("EPSMOE_DYN_SCHED", 1);
@@ -730,13 +780,14 @@ int launch_epi(const GemmArgs& a, cudaStream_t stream) {
   p.m_single = a.m_single;
   p.b_group_rows = a.b_group_rows;
   p.b_base = a.b_base;
-  p.raster_gm = raster_gm();
+  p.raster_gm = raster_gm(EPI, a.N, a.K, a.rows_hint);
   p.ldo = a.ldo;
   p.out = a.out;
   p.bias = a.bias;
   p.row_start = a.row_start;
   p.row_count = a.row_count;
   p.a_row_index = a.a_row_index;
+  p.a_ptr = reinterpret_cast<const uint8_t*>(a.A);
   p.row_mode = a.row_mode;
   p.comb_o = reinterpret_cast<const __nv_bfloat16*>(a.comb_o);
   p.comb_pos = a.comb_pos;

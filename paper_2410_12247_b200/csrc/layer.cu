@@ -278,10 +278,11 @@ int pick_cta_pair(const moe_plan_t& plan, double mean_rows) {
 // ComputeMoE for local experts [g0, g1): GateUpGemm+SiluAct fused,
 // then DownGemm.  Rows of expert g are [row_start[g], +row_count[g]) of A.
 int compute_moe(moe_layer* L, const void* A, int64_t a_rows, const int32_t* row_start, const int32_t* row_count,
-                int g0, int g1, int kind, int num_ctas, int cta_pair, cudaStream_t st,
+                int g0, int g1, int kind, int num_ctas, int cta_pair, double rows_per_group, cudaStream_t st,
                 const int32_t* a_row_index = nullptr) {
   const moe_config_t& c = L->cfg;
   GemmArgs g1a = base_args(EPI_SWIGLU, num_ctas);
+  g1a.rows_hint = rows_per_group;
   g1a.cta_pair = cta_pair;
   g1a.A = A;
   g1a.a_row_index = a_row_index;
@@ -297,6 +298,7 @@ int compute_moe(moe_layer* L, const void* A, int64_t a_rows, const int32_t* row_
   g1a.ldo = c.ffn;
   g1a.out_rows = L->gemm_rows_cap;
   GemmArgs g2a = base_args(EPI_BF16, num_ctas);
+  g2a.rows_hint = rows_per_group;
   g2a.cta_pair = cta_pair;
   g2a.tile_counter = L->tickets;
   g2a.A = L->h;
@@ -818,8 +820,8 @@ moe_status_t moe_layer_forward(moe_layer_t* L, const void* x, int64_t T, void* y
         int b = a + 1;
         while (b < g1 && plan.expert_kind[b] == plan.expert_kind[a]) ++b;
         int err = compute_moe(L, gather ? x : L->send, gather ? T : L->send_cap, L->seg_start, L->hist, a, b,
-                              plan.expert_kind[a], num_ctas, pick_cta_pair(plan, (double)T * k / E), st,
-                              gather ? L->row_token : nullptr);
+                              plan.expert_kind[a], num_ctas, pick_cta_pair(plan, (double)T * k / E),
+                              (double)T * k / E, st, gather ? L->row_token : nullptr);
         if (err) { set_error(std::string("ComputeMoE: ") + cudaGetErrorString((cudaError_t)err)); return MOE_ERR_CUDA; }
         a = b;
       }
@@ -1078,7 +1080,8 @@ moe_status_t moe_layer_forward(moe_layer_t* L, const void* x, int64_t T, void* y
         double rows = 0;
         for (int el = a; el < b; ++el) rows += tcount[ch * E_loc + el];
         int err = compute_moe(L, L->recv, L->recv_cap, L->recv_start_d + ch * E_loc, L->recv_count_d + ch * E_loc,
-                              a, b, plan.expert_kind[a], num_ctas, pick_cta_pair(plan, rows / (b - a)), st);
+                              a, b, plan.expert_kind[a], num_ctas, pick_cta_pair(plan, rows / (b - a)), rows / (b - a),
+                              st);
         if (err) { set_error(std::string("ComputeMoE: ") + cudaGetErrorString((cudaError_t)err)); return MOE_ERR_CUDA; }
         a = b;
       }
@@ -1286,7 +1289,7 @@ moe_status_t moe_layer_calibrate(moe_layer_t* L, void* stream, moe_cost_model_t*
       for (int rep = 0; rep < 3; ++rep) {
         CUDA_TRY(cudaEventRecord(e0, st));
         int err = compute_moe(L, A, arows, L->recv_start_d, L->recv_count_d, 0, G, kind, L->num_sms,
-                              rows >= 512 ? 1 : 0, st);
+                              rows >= 512 ? 1 : 0, rows, st);
         if (err) { set_error("calibrate gemm failed"); return MOE_ERR_CUDA; }
         CUDA_TRY(cudaEventRecord(e1, st));
         CUDA_TRY(cudaEventSynchronize(e1));
