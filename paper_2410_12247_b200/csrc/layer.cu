@@ -178,7 +178,7 @@ size_t carve(moe_layer* L, char* base) {
   const moe_config_t& c = L->cfg;
   const int64_t T = c.max_tokens, E = c.num_experts, k = c.top_k, H = c.hidden, F = c.ffn;
   const int64_t D = c.ep, E_loc = E / D, SF = (int64_t)c.num_shared * c.shared_ffn;
-  const int64_t R = num_ranges(T);
+  const int64_t R = max_ranges(T);
   L->send_cap = T * k;
   L->recv_cap = (D == 1) ? 0 : D * T * std::min<int64_t>(k, E_loc);
   L->gemm_rows_cap = (D == 1) ? L->send_cap : L->recv_cap;

@@ -19,8 +19,8 @@
 // Home (rank r):     lr_combine: y = bf16(fp32(s) + p_g ... in g order).
 // ep == 1:           lr_combine_local does both sides in one pass.
 //
-// Every row index is a deterministic prefix sum (ranges of RANGE_T tokens, one
-// warp each), as in route.cu: no atomics decide a row.
+// Every row index is a deterministic prefix sum (ranges of range_len(T)
+// tokens, one warp each), as in route.cu: no atomics decide a row.
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -77,7 +77,7 @@ __device__ __forceinline__ void load_chunks(const LrChunks& ch, int E_loc, int32
 
 __global__ void __launch_bounds__(WARPS_R * 32)
 lr_count_kernel(const int32_t* __restrict__ topk_idx, int T, int k, int E_loc, int D, LrChunks ch, int G,
-                int32_t* __restrict__ range_hist, int R) {
+                int32_t* __restrict__ range_hist, int R, int rt) {
   __shared__ int32_t hist_s[WARPS_R][256];
   __shared__ int32_t chunk_s[256];
   load_chunks(ch, E_loc, chunk_s);
@@ -86,8 +86,8 @@ lr_count_kernel(const int32_t* __restrict__ topk_idx, int T, int k, int E_loc, i
   for (int g = lane; g < G; g += 32) hist_s[warp][g] = 0;
   __syncwarp();
   if (r < R) {
-    const int t_end = min(T, (r + 1) * RANGE_T);
-    for (int t = r * RANGE_T; t < t_end; ++t) {
+    const int t_end = min(T, (r + 1) * rt);
+    for (int t = r * rt; t < t_end; ++t) {
       const TokGroups tg = token_groups(topk_idx, t, k, lane, chunk_s, E_loc, D);
       if (tg.lead) atomicAdd(&hist_s[warp][tg.g], 1);  // order-free count
       __syncwarp();
@@ -104,7 +104,7 @@ __global__ void __launch_bounds__(WARPS_R * 32, 4)
 lr_permute_kernel(const __nv_bfloat16* __restrict__ x, int T, int H, int k, const int32_t* __restrict__ topk_idx,
                   const float* __restrict__ topk_w, const int32_t* __restrict__ pos,
                   const int32_t* __restrict__ seg_start, int E_loc, int D, LrChunks ch, int G,
-                  const int32_t* __restrict__ range_off, const int32_t* __restrict__ u_start, int R,
+                  const int32_t* __restrict__ range_off, const int32_t* __restrict__ u_start, int R, int rt,
                   __nv_bfloat16* __restrict__ send, uint8_t* __restrict__ sendq, int qpitch,
                   int32_t* __restrict__ posg, int32_t* __restrict__ meta) {
   __shared__ int32_t off_s[WARPS_R][256];
@@ -116,9 +116,9 @@ lr_permute_kernel(const __nv_bfloat16* __restrict__ x, int T, int H, int k, cons
   for (int g = lane; g < G; g += 32) off_s[warp][g] = u_start[g] + range_off[(int64_t)g * R + r];
   __syncwarp();
   const int nvec = H >> 3;
-  const int t_end = min(T, (r + 1) * RANGE_T);
+  const int t_end = min(T, (r + 1) * rt);
   const uint64_t pol = evict_first_policy();
-  for (int t = r * RANGE_T; t < t_end; ++t) {
+  for (int t = r * rt; t < t_end; ++t) {
     const TokGroups tg = token_groups(topk_idx, t, k, lane, chunk_s, E_loc, D);
     int code = -1;
     float w = 0.f;
@@ -419,7 +419,7 @@ int launch_lr_count(const int32_t* topk_idx, int T, int k, int E_loc, int D, con
   const int R = num_ranges(T);
   if (R == 0) return 0;
   lr_count_kernel<<<(R + WARPS_R - 1) / WARPS_R, WARPS_R * 32, 0, st>>>(topk_idx, T, k, E_loc, D, ch, ch.n * D,
-                                                                         range_hist, R);
+                                                                         range_hist, R, range_len(T));
   return (int)cudaGetLastError();
 }
 
@@ -434,11 +434,12 @@ int launch_lr_permute(const void* x, int T, int H, int k, const int32_t* topk_id
   auto xb = (const __nv_bfloat16*)x;
   if (sendq)
     lr_permute_kernel<2><<<grid, block, 0, st>>>(xb, T, H, k, topk_idx, topk_w, pos, seg_start, E_loc, D, ch, G,
-                                                 range_off, u_start, R, nullptr, (uint8_t*)sendq, qpitch, posg, meta);
+                                                 range_off, u_start, R, range_len(T), nullptr, (uint8_t*)sendq, qpitch,
+                                                 posg, meta);
   else
     lr_permute_kernel<0><<<grid, block, 0, st>>>(xb, T, H, k, topk_idx, topk_w, pos, seg_start, E_loc, D, ch, G,
-                                                 range_off, u_start, R, (__nv_bfloat16*)send, nullptr, qpitch, posg,
-                                                 meta);
+                                                 range_off, u_start, R, range_len(T), (__nv_bfloat16*)send, nullptr, qpitch,
+                                                 posg, meta);
   return (int)cudaGetLastError();
 }
 

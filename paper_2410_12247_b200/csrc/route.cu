@@ -2,7 +2,7 @@
 // (`split`, K3) and the gate-weighted unpermute fused into combine (K7).
 //
 // Layout readings: send buffer rows are ordered by (expert asc,
-// token asc) (R6); tokens are processed in ranges of RANGE_T consecutive
+// token asc) (R6); tokens are processed in ranges of range_len(T) consecutive
 // tokens, one warp per range, so every per-expert offset is a deterministic
 // prefix sum: no atomics decide any row index.
 #include <cuda_bf16.h>
@@ -10,6 +10,7 @@
 #include <cuda_fp8.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 
 #include "route.h"
@@ -28,22 +29,22 @@ __device__ __forceinline__ bool better(float av, int ae, float bv, int be) {
   return av > bv || (av == bv && ae < be);
 }
 
-// K2 topKGating.  One warp per range of RANGE_T tokens, tokens
+// K2 topKGating.  One warp per range of range_len(T) tokens, tokens
 // in order.  idx = k largest logits (ties -> lower expert id, R2); p = softmax
 // over all E in fp32; w_j = p_{idx_j} (/ sum_j p_{idx_j} if norm_topk) * scale.
 // Also writes the range's expert histogram range_hist[e * R + r].
 __global__ void __launch_bounds__(WARPS_R * 32)
 gate_topk_kernel(const float* __restrict__ logits, int T, int E, int k, int norm_topk, float scale,
                  int override_routing, int route_groups, int route_topk_groups, int32_t* __restrict__ topk_idx,
-                 float* __restrict__ topk_w, int32_t* __restrict__ range_hist, int R) {
+                 float* __restrict__ topk_w, int32_t* __restrict__ range_hist, int R, int rt) {
   __shared__ int32_t hist_s[WARPS_R][256];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int r = blockIdx.x * WARPS_R + warp;
   for (int e = lane; e < E; e += 32) hist_s[warp][e] = 0;
   __syncwarp();
   if (r < R) {
-    const int t_end = min(T, (r + 1) * RANGE_T);
-    for (int t = r * RANGE_T; t < t_end; ++t) {
+    const int t_end = min(T, (r + 1) * rt);
+    for (int t = r * rt; t < t_end; ++t) {
       if (override_routing) {
         if (lane < k) {
           int e = topk_idx[(int64_t)t * k + lane];
@@ -225,7 +226,7 @@ template <int fp8>
 __global__ void __launch_bounds__(WARPS_R * 32, 4)
 permute_kernel(const __nv_bfloat16* __restrict__ x, int T, int H, int E, int k,
                const int32_t* __restrict__ topk_idx, const int32_t* __restrict__ range_off,
-               const int32_t* __restrict__ seg_start, int R, __nv_bfloat16* __restrict__ send,
+               const int32_t* __restrict__ seg_start, int R, int rt, __nv_bfloat16* __restrict__ send,
                int32_t* __restrict__ pos, int32_t* __restrict__ row_token, uint8_t* __restrict__ sendq,
                int qpitch) {
   __shared__ int32_t off_s[WARPS_R][256];
@@ -235,9 +236,9 @@ permute_kernel(const __nv_bfloat16* __restrict__ x, int T, int H, int E, int k,
   for (int e = lane; e < E; e += 32) off_s[warp][e] = seg_start[e] + range_off[(int64_t)e * R + r];
   __syncwarp();
   const int nvec = H >> 3;  // uint4 = 8 bf16
-  const int t_end = min(T, (r + 1) * RANGE_T);
+  const int t_end = min(T, (r + 1) * rt);
   const uint64_t pol = evict_first_policy();
-  for (int t = r * RANGE_T; t < t_end; ++t) {
+  for (int t = r * rt; t < t_end; ++t) {
     int dest = 0;
     if (lane < k) {
       int e = topk_idx[(int64_t)t * k + lane];
@@ -410,7 +411,16 @@ __global__ void pad_rows_kernel(const __nv_bfloat16* __restrict__ src, int rows,
 
 }  // namespace
 
-int num_ranges(int64_t T) { return (int)((T + RANGE_T - 1) / RANGE_T); }
+int range_len(int64_t T) {
+  int p = 1;
+  while (p < 32 && (T + p - 1) / p > 2048) p <<= 1;
+  return p;
+}
+int num_ranges(int64_t T) {
+  const int p = range_len(T);
+  return (int)((T + p - 1) / p);
+}
+int max_ranges(int64_t T_max) { return (int)std::max<int64_t>(std::min<int64_t>(T_max, 2048), num_ranges(T_max)); }
 
 int launch_gate_topk(const float* logits, int T, int E, int k, int norm_topk, float scale, int override_routing,
                      int route_groups, int route_topk_groups, int32_t* topk_idx, float* topk_w,
@@ -421,7 +431,7 @@ int launch_gate_topk(const float* logits, int T, int E, int k, int norm_topk, fl
   gate_topk_kernel<<<(R + WARPS_R - 1) / WARPS_R, WARPS_R * 32, 0, st>>>(logits, T, E, k, norm_topk, scale,
                                                                          override_routing, route_groups,
                                                                          route_topk_groups, topk_idx, topk_w,
-                                                                         range_hist, R);
+                                                                         range_hist, R, range_len(T));
   return (int)cudaGetLastError();
 }
 
@@ -442,19 +452,20 @@ int launch_permute(const void* x, int T, int H, int E, int k, const int32_t* top
                    const int32_t* seg_start, void* send, int32_t* pos, int32_t* row_token, int fp8, void* sendq,
                    int qpitch, cudaStream_t st) {
   int R = num_ranges(T);
+  const int rt = range_len(T);
   if (R == 0) return 0;
   const dim3 grid((R + WARPS_R - 1) / WARPS_R), block(WARPS_R * 32);
   auto xb = (const __nv_bfloat16*)x;
   auto sb = (__nv_bfloat16*)send;
   auto qb = (uint8_t*)sendq;
   if (fp8 == 0)
-    permute_kernel<0><<<grid, block, 0, st>>>(xb, T, H, E, k, topk_idx, range_off, seg_start, R, sb, pos, row_token,
+    permute_kernel<0><<<grid, block, 0, st>>>(xb, T, H, E, k, topk_idx, range_off, seg_start, R, rt, sb, pos, row_token,
                                               qb, qpitch);
   else if (fp8 == 1)
-    permute_kernel<1><<<grid, block, 0, st>>>(xb, T, H, E, k, topk_idx, range_off, seg_start, R, sb, pos, row_token,
+    permute_kernel<1><<<grid, block, 0, st>>>(xb, T, H, E, k, topk_idx, range_off, seg_start, R, rt, sb, pos, row_token,
                                               qb, qpitch);
   else
-    permute_kernel<2><<<grid, block, 0, st>>>(xb, T, H, E, k, topk_idx, range_off, seg_start, R, sb, pos, row_token,
+    permute_kernel<2><<<grid, block, 0, st>>>(xb, T, H, E, k, topk_idx, range_off, seg_start, R, rt, sb, pos, row_token,
                                               qb, qpitch);
   return (int)cudaGetLastError();
 }

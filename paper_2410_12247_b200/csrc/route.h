@@ -5,9 +5,13 @@
 
 namespace epsmoe {
 
-constexpr int RANGE_T = 32;  // tokens per deterministic counting range (one warp)
-
+// Tokens are counted in ranges of range_len(T) consecutive tokens, one warp
+// per range, so every row offset is a deterministic prefix sum.  Long batches
+// use 32-token ranges; short ones (decode) shorter ranges, so that up to ~2048
+// warps share the work instead of T/32.
+int range_len(int64_t T);
 int num_ranges(int64_t T);
+int max_ranges(int64_t T_max);  // over every T <= T_max (workspace sizing)
 // route_groups > 1 (and route_topk_groups < route_groups): device-limited routing (R17).
 int launch_gate_topk(const float* logits, int T, int E, int k, int norm_topk, float scale, int override_routing,
                      int route_groups, int route_topk_groups, int32_t* topk_idx, float* topk_w,
