@@ -265,3 +265,50 @@ def test_token_sliced_chunks_equal_unchunked(E, k, D, N, S, fp8):
                            ws_gate_bits=inp.ws_gate, ws_up_bits=inp.ws_up, ws_down_bits=inp.ws_down, D=D, N=N,
                            token_slices=S, dispatch_fp8=fp8)
     assert_close(y, ref["y"], f"sliced EP{D} N{N} S{S}")
+
+
+def test_ep_stage_profiling_and_exposed_a2a():
+    """The per-stage device timing the bench reports at ep > 1: every chunk's
+    dispatch and combine all2all is timed on its own stream, the exposed
+    (non-overlapped) all2all time is within [0, total], and stage counts
+    follow the chunk count."""
+    D, N = 2, 3
+    inp = Inputs(E=12, k=2, H=256, F=256, S=1, Fs=128, T=1200, seed=5)
+    E_loc = 6
+    start = oracle.token_shards(1200, D)
+    group = LocalGroup(D)
+    layers, xs = [], []
+    for r in range(D):
+        w = dict(w_router=dev_bf16(inp.w_router), w_gate=dev_bf16(inp.w_gate[r * E_loc:(r + 1) * E_loc]),
+                 w_up=dev_bf16(inp.w_up[r * E_loc:(r + 1) * E_loc]),
+                 w_down=dev_bf16(inp.w_down[r * E_loc:(r + 1) * E_loc]),
+                 ws_gate=dev_bf16(inp.ws_gate), ws_up=dev_bf16(inp.ws_up), ws_down=dev_bf16(inp.ws_down))
+        L = MoELayer(12, 2, 256, 256, w, S=1, Fs=128, ep=D, rank=r, max_tokens=600, norm_topk=1, local_group=group)
+        L.set_profiling(True)
+        layers.append(L)
+        xs.append(dev_bf16(inp.x[start[r]:start[r + 1]]))
+    stages, errs = [None] * D, []
+
+    def worker(r):
+        try:
+            torch.cuda.set_device(0)
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                layers[r].forward(xs[r], plan=make_plan(N, MOE_GEMM_GROUPED), stream=s)
+                s.synchronize()
+                stages[r] = layers[r].stage_ms()
+        except Exception as e:  # pragma: no cover
+            errs.append(repr(e))
+
+    th = [threading.Thread(target=worker, args=(r,), daemon=True) for r in range(D)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=120)
+    assert not errs, errs
+    for st in stages:
+        assert st["dispatch_a2a"][1] == N and st["combine_a2a"][1] == N
+        assert st["total"][0] > 0 and st["gateup"][0] > 0 and st["shared"][0] > 0
+        assert 0.0 <= st["exposed_a2a"][0] <= st["total"][0]
+    for L in layers:
+        L.close()
