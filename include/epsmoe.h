@@ -85,6 +85,14 @@ typedef struct {
                            route_topk_groups groups with the largest best
                            logit may be selected.  0 or 1: off.             */
   int32_t route_topk_groups; /* M, 1 <= M <= route_groups, topk <= M*e/groups */
+  int32_t a2a_p2p;      /* ep > 1 all2all data plane.  0: NCCL grouped send/recv
+                           (two communicators).  1: the layer's own put
+                           kernels store rows straight into the peers'
+                           workspaces (cudaIpc-mapped over NVLink; the
+                           workspace must be a cudaMalloc allocation) and
+                           raise per-(chunk, source) flags there; NCCL only
+                           allgathers counts (and, once, the buffer offsets
+                           of every rank's workspace).                       */
 } moe_config_t;
 
 /* Caller-owned device weights (bf16, K-major), valid for the layer's life.

@@ -29,7 +29,8 @@ class moe_config_t(C.Structure):
                 ("ffn", C.c_int32), ("num_shared", C.c_int32), ("shared_ffn", C.c_int32),
                 ("ep", C.c_int32), ("rank", C.c_int32), ("max_tokens", C.c_int64),
                 ("norm_topk", C.c_int32), ("routed_scale", C.c_float), ("dispatch_fp8", C.c_int32),
-                ("local_reduce", C.c_int32), ("route_groups", C.c_int32), ("route_topk_groups", C.c_int32)]
+                ("local_reduce", C.c_int32), ("route_groups", C.c_int32), ("route_topk_groups", C.c_int32),
+                ("a2a_p2p", C.c_int32)]
 
 
 class moe_weights_t(C.Structure):
@@ -130,9 +131,9 @@ def check(status: int, what: str = "") -> None:
 
 
 def make_config(E, k, H, F, S=0, Fs=0, ep=1, rank=0, max_tokens=1, norm_topk=0, routed_scale=1.0,
-                dispatch_fp8=0, local_reduce=0, route_groups=0, route_topk_groups=0):
+                dispatch_fp8=0, local_reduce=0, route_groups=0, route_topk_groups=0, a2a_p2p=0):
     return moe_config_t(E, k, H, F, S, Fs, ep, rank, max_tokens, norm_topk, routed_scale, dispatch_fp8,
-                        local_reduce, route_groups, route_topk_groups)
+                        local_reduce, route_groups, route_topk_groups, a2a_p2p)
 
 
 def plan_compute(cfg: moe_config_t, global_tokens: int, global_hist=None, cost: moe_cost_model_t | None = None):

@@ -21,6 +21,7 @@
 #include "gemm.h"
 #include "internal.h"
 #include "lr.h"
+#include "p2p.h"
 #include "route.h"
 #include "transport.h"
 
@@ -46,6 +47,22 @@ struct moe_layer {
   int32_t *posg = nullptr, *u_hist = nullptr, *u_start = nullptr, *ughist = nullptr;
   int32_t *meta_send = nullptr, *meta_recv = nullptr, *lr_recv_off_d = nullptr, *lr_usrc_d = nullptr;
   void* recvu = nullptr;  // bf16 [recv_cap, H]: received unique rows, then their LocalReduce partials
+  // a2a_p2p: own put kernels over peer-mapped workspaces.  flags [2][64][ep]:
+  // per (direction, chunk, source) completion epochs written by the sources;
+  // done [2][64]: put-kernel CTA counters; segment tables per launch.
+  static constexpr int P2P_MAXS = 2 * MOE_MAX_EXPERTS;  // segments per put launch
+  char* ws_base = nullptr;
+  std::vector<char*> peer_ws;  // [ep] every rank's workspace base, mapped here
+  // [ep][P2P_NBUF] byte offsets of the buffers peers write into, per rank (a
+  // rank's max_tokens, hence its workspace layout, may differ from its peers')
+  enum { P2P_RECV, P2P_RECVQ, P2P_RECVU, P2P_META, P2P_COMB, P2P_FLAGS, P2P_NBUF };
+  std::vector<int64_t> peer_off;
+  uint32_t p2p_epoch = 0;
+  uint32_t *p2p_flags = nullptr, *p2p_done = nullptr;
+  epsmoe::P2PSeg* p2p_segs = nullptr;  // device [2][64][P2P_MAXS]
+  int64_t* p2p_pre = nullptr;          // device [2][64][P2P_MAXS + 1]
+  uint32_t** p2p_fptr = nullptr;       // device [2][64][ep]: consumer flag addresses
+  char* p2p_host = nullptr;            // pinned mirror of segs | pre | fptr
   int32_t* ughist_host = nullptr;  // pinned [ep*256]
   void *x_dev = nullptr, *y_dev = nullptr;  // staging for forward_host
   // host
@@ -150,6 +167,11 @@ struct Carve {
   }
 };
 
+// a2a_p2p segment tables (host mirror == device layout): segs | pre | flag pointers
+constexpr size_t P2P_SEGS_BYTES = sizeof(epsmoe::P2PSeg) * 2 * MOE_MAX_CHUNKS * moe_layer::P2P_MAXS;
+constexpr size_t P2P_PRE_BYTES = sizeof(int64_t) * 2 * MOE_MAX_CHUNKS * (moe_layer::P2P_MAXS + 1);
+size_t p2p_table_bytes(int ep) { return P2P_SEGS_BYTES + P2P_PRE_BYTES + sizeof(uint32_t*) * 2 * MOE_MAX_CHUNKS * ep; }
+
 int validate(const moe_config_t* c) {
   if (!c) return MOE_ERR_INVALID;
   std::string why;
@@ -164,6 +186,7 @@ int validate(const moe_config_t* c) {
   else if (c->dispatch_fp8 && c->hidden % 128) why = "dispatch_fp8 needs hidden % 128 == 0";
   else if (c->max_tokens < 1) why = "max_tokens must be >= 1";
   else if (c->local_reduce != 0 && c->local_reduce != 1) why = "local_reduce must be 0 or 1";
+  else if (c->a2a_p2p != 0 && c->a2a_p2p != 1) why = "a2a_p2p must be 0 or 1";
   else if (c->route_groups > 1 &&
            (c->route_groups > 32 || c->num_experts % c->route_groups || c->route_topk_groups < 1 ||
             c->route_topk_groups > c->route_groups ||
@@ -218,12 +241,19 @@ size_t carve(moe_layer* L, char* base) {
     L->u_start = cv.take<int32_t>(MOE_MAX_EXPERTS + 1);
     if (D > 1) {
       L->ughist = cv.take<int32_t>(D * MOE_MAX_EXPERTS);
-      L->meta_send = cv.take<int32_t>(L->send_cap * 2 * k);
-      L->meta_recv = cv.take<int32_t>(L->recv_cap * 2 * k);
+      L->meta_send = cv.take<int32_t>(L->send_cap * lr_meta_pitch((int)k));
+      L->meta_recv = cv.take<int32_t>(L->recv_cap * lr_meta_pitch((int)k));
       L->recvu = cv.take<uint16_t>(L->recv_cap * H);
       L->lr_recv_off_d = cv.take<int32_t>(MOE_MAX_EXPERTS + 1);
       L->lr_usrc_d = cv.take<int32_t>(MOE_MAX_EXPERTS + 1);
     }
+  }
+  if (D > 1 && c.a2a_p2p) {
+    L->p2p_flags = cv.take<uint32_t>(2 * MOE_MAX_CHUNKS * D);
+    L->p2p_done = cv.take<uint32_t>(2 * MOE_MAX_CHUNKS);
+    L->p2p_segs = cv.take<epsmoe::P2PSeg>((size_t)2 * MOE_MAX_CHUNKS * moe_layer::P2P_MAXS);
+    L->p2p_pre = cv.take<int64_t>((size_t)2 * MOE_MAX_CHUNKS * (moe_layer::P2P_MAXS + 1));
+    L->p2p_fptr = cv.take<uint32_t*>((size_t)2 * MOE_MAX_CHUNKS * D);
   }
   L->hs = SF ? cv.take<uint16_t>(T * SF) : nullptr;
   L->s = SF ? cv.take<uint16_t>(T * H) : nullptr;
@@ -418,7 +448,10 @@ static moe_status_t create_impl(const moe_config_t* cfg, const moe_weights_t* w,
   }
   char* base = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(workspace) + ALIGN - 1) & ~(uintptr_t)(ALIGN - 1));
   carve(L, base);
-  if (cudaMemset(L->tickets, 0, 4 * sizeof(int32_t)) != cudaSuccess) {
+  L->ws_base = base;
+  if (cudaMemset(L->tickets, 0, 4 * sizeof(int32_t)) != cudaSuccess ||
+      (L->p2p_flags && (cudaMemset(L->p2p_flags, 0, sizeof(uint32_t) * 2 * MOE_MAX_CHUNKS * cfg->ep) != cudaSuccess ||
+                        cudaMemset(L->p2p_done, 0, sizeof(uint32_t) * 2 * MOE_MAX_CHUNKS) != cudaSuccess))) {
     set_error("workspace memset failed");
     delete L;
     return MOE_ERR_CUDA;
@@ -442,6 +475,7 @@ static moe_status_t create_impl(const moe_config_t* cfg, const moe_weights_t* w,
                     cudaHostAllocDefault) != cudaSuccess ||
       (cfg->ep > 1 && cudaHostAlloc(&L->gslice_host, sizeof(int32_t) * cfg->ep * cfg->num_experts * MOE_MAX_CHUNKS,
                                     cudaHostAllocDefault) != cudaSuccess) ||
+      (L->p2p_segs && cudaHostAlloc(&L->p2p_host, p2p_table_bytes(cfg->ep), cudaHostAllocDefault) != cudaSuccess) ||
       cudaHostAlloc(&L->ughist_host, sizeof(int32_t) * cfg->ep * MOE_MAX_EXPERTS, cudaHostAllocDefault) != cudaSuccess) {
     set_error("cudaHostAlloc failed");
     return fail(MOE_ERR_CUDA);
@@ -514,7 +548,7 @@ static moe_status_t create_impl(const moe_config_t* cfg, const moe_weights_t* w,
       // every rank must agree on the shape (MOE_ERR_MISMATCH)
       int32_t sig[8] = {cfg->num_experts, cfg->top_k, cfg->hidden, cfg->ffn, cfg->num_shared, cfg->shared_ffn,
                         cfg->norm_topk | (cfg->dispatch_fp8 << 1) | (cfg->local_reduce << 2) |
-                            (cfg->route_groups << 3) | (cfg->route_topk_groups << 9),
+                            (cfg->route_groups << 3) | (cfg->route_topk_groups << 9) | (cfg->a2a_p2p << 15),
                         (int32_t)(cfg->routed_scale * 1e6f)};
       int32_t* d_sig = nullptr;
       if (cudaMalloc(&d_sig, sizeof(sig) * (cfg->ep + 1)) != cudaSuccess) return fail(MOE_ERR_CUDA);
@@ -577,6 +611,7 @@ moe_status_t moe_layer_destroy(moe_layer_t* L) {
   if (L->tables_host) cudaFreeHost(L->tables_host);
   if (L->ughist_host) cudaFreeHost(L->ughist_host);
   if (L->gslice_host) cudaFreeHost(L->gslice_host);
+  if (L->p2p_host) cudaFreeHost(L->p2p_host);
   delete L;
   return MOE_OK;
 }
@@ -986,6 +1021,140 @@ moe_status_t moe_layer_forward(moe_layer_t* L, const void* x, int64_t T, void* y
       CUDA_TRY(cudaMemcpyAsync(L->lr_usrc_d, tb + MOE_MAX_EXPERTS + 4, sizeof(int32_t) * (G + 1),
                                cudaMemcpyHostToDevice, st));
     }
+    // ---- a2a_p2p: this forward's put-kernel segments (rows of each chunk, per
+    // peer, at the peer's own offsets) and consumer flag addresses
+    const bool p2p = c.a2a_p2p != 0;
+    uint32_t epoch = 0;
+    int p2p_nseg[2][MOE_MAX_CHUNKS] = {};
+    int64_t p2p_total[2][MOE_MAX_CHUNKS] = {};
+    if (p2p) {
+      if (L->peer_ws.empty()) {  // first forward (collective): map the peers, learn their layouts
+        TR_TRY(L->tr->map_peers(L->ws_base, L->peer_ws));
+        const void* bufs[moe_layer::P2P_NBUF] = {L->recv, L->recvq, L->recvu, L->meta_recv, L->comb, L->p2p_flags};
+        int64_t mine[moe_layer::P2P_NBUF];
+        for (int b = 0; b < moe_layer::P2P_NBUF; ++b)
+          mine[b] = bufs[b] ? (int64_t)((const char*)bufs[b] - L->ws_base) : -1;
+        constexpr int W = 2 * moe_layer::P2P_NBUF;
+        int32_t* dev = nullptr;
+        CUDA_TRY(cudaMalloc(&dev, sizeof(int32_t) * W * (D + 1)));
+        CUDA_TRY(cudaMemcpy(dev, mine, sizeof(mine), cudaMemcpyHostToDevice));
+        int ge = L->tr->allgather_i32(dev, dev + W, W, st);
+        L->peer_off.assign((size_t)D * moe_layer::P2P_NBUF, -1);
+        if (!ge) {
+          CUDA_TRY(cudaStreamSynchronize(st));
+          CUDA_TRY(cudaMemcpy(L->peer_off.data(), dev + W, sizeof(int64_t) * D * moe_layer::P2P_NBUF,
+                              cudaMemcpyDeviceToHost));
+        }
+        cudaFree(dev);
+        if (ge) return (moe_status_t)ge;
+      }
+      epoch = ++L->p2p_epoch;
+      // address, in peer d's workspace, of byte `off` of its buffer b
+      auto peer_buf = [&](int d, int b, int64_t off) -> char* {
+        return L->peer_ws[d] + L->peer_off[(size_t)d * moe_layer::P2P_NBUF + b] + off;
+      };
+      // every rank's layout, from the same global counts
+      const size_t RP = (size_t)E_loc * S * D;
+      std::vector<int64_t> rpos_all((size_t)D * RP), spos_all((size_t)D * E * S);
+      for (int d = 0; d < D; ++d) {
+        int64_t row = 0;
+        for (int el = 0; el < E_loc; ++el)
+          for (int sl = 0; sl < S; ++sl)
+            for (int src = 0; src < D; ++src) {
+              rpos_all[d * RP + ((size_t)el * S + sl) * D + src] = row;
+              row += cnt(src, d * E_loc + el, sl);
+            }
+        row = 0;
+        for (int ex = 0; ex < E; ++ex)
+          for (int sl = 0; sl < S; ++sl) {
+            spos_all[(size_t)d * E * S + (size_t)ex * S + sl] = row;
+            row += cnt(d, ex, sl);
+          }
+      }
+      std::vector<int64_t> urecv_all, usend_all;
+      if (lr_ep) {
+        urecv_all.assign((size_t)D * (G + 1), 0);
+        usend_all.assign((size_t)D * (G + 1), 0);
+        for (int d = 0; d < D; ++d) {
+          int64_t row = 0;
+          for (int ch = 0; ch < plan.num_chunks; ++ch)
+            for (int src = 0; src < D; ++src) {
+              urecv_all[(size_t)d * (G + 1) + ch * D + src] = row;
+              row += ug[(size_t)src * G + ch * D + d];
+            }
+          for (int g = 0; g < G; ++g)
+            usend_all[(size_t)d * (G + 1) + g + 1] = usend_all[(size_t)d * (G + 1) + g] + ug[(size_t)d * G + g];
+        }
+      }
+      auto* hsegs = reinterpret_cast<epsmoe::P2PSeg*>(L->p2p_host);
+      auto* hpre = reinterpret_cast<int64_t*>(L->p2p_host + P2P_SEGS_BYTES);
+      auto* hfp = reinterpret_cast<uint32_t**>(L->p2p_host + P2P_SEGS_BYTES + P2P_PRE_BYTES);
+      const size_t rowb = (size_t)H * 2;
+      const size_t drowb = fp8 ? (size_t)L->qpitch : rowb;
+      const size_t metab = (size_t)lr_meta_pitch(k) * sizeof(int32_t);
+      char* ds = fp8 ? (char*)L->sendq : (char*)L->send;
+      const int dr_id = fp8 ? moe_layer::P2P_RECVQ : (lr_ep ? moe_layer::P2P_RECVU : moe_layer::P2P_RECV);
+      for (int dir = 0; dir < 2; ++dir)
+        for (int ch = 0; ch < plan.num_chunks; ++ch) {
+          const size_t slot = (size_t)dir * MOE_MAX_CHUNKS + ch;
+          epsmoe::P2PSeg* sg = hsegs + slot * moe_layer::P2P_MAXS;
+          int64_t* pr = hpre + slot * (moe_layer::P2P_MAXS + 1);
+          int n = 0;
+          pr[0] = 0;
+          auto add = [&](const char* src, char* dst, int64_t bytes) {
+            if (bytes <= 0 || n >= moe_layer::P2P_MAXS) return;
+            sg[n].src = reinterpret_cast<const uint4*>(src);
+            sg[n].dst = reinterpret_cast<uint4*>(dst);
+            pr[n + 1] = pr[n] + bytes / 16;
+            ++n;
+          };
+          for (int d = 0; d < D; ++d)
+            hfp[slot * D + d] =
+                reinterpret_cast<uint32_t*>(peer_buf(d, moe_layer::P2P_FLAGS, (int64_t)(slot * D + me) * 4));
+          const int sl = ch % S, g0 = plan.group_begin[ch / S], g1 = plan.group_begin[ch / S + 1];
+          for (int peer = 0; peer < D; ++peer) {
+            if (lr_ep && dir == 0) {
+              const int64_t s0 = usend_off[ch * D + peer], ns = ug[(size_t)me * G + ch * D + peer];
+              const int64_t r0 = urecv_all[(size_t)peer * (G + 1) + ch * D + me];
+              add(ds + s0 * drowb, peer_buf(peer, dr_id, r0 * drowb), ns * (int64_t)drowb);
+              add((char*)L->meta_send + s0 * metab, peer_buf(peer, moe_layer::P2P_META, r0 * metab), ns * (int64_t)metab);
+            } else if (lr_ep) {
+              const int64_t r0 = urecv[(size_t)ch * D + peer], nb = ug[(size_t)peer * G + ch * D + me];
+              const int64_t s0 = usend_all[(size_t)peer * (G + 1) + ch * D + me];
+              add((char*)L->recvu + r0 * rowb, peer_buf(peer, moe_layer::P2P_COMB, s0 * rowb), nb * (int64_t)rowb);
+            } else {
+              for (int el = g0; el < g1; ++el) {
+                if (dir == 0) {
+                  const int ex = peer * E_loc + el;
+                  add(ds + send_pos[(size_t)ex * S + sl] * drowb,
+                      peer_buf(peer, dr_id, rpos_all[peer * RP + ((size_t)el * S + sl) * D + me] * drowb),
+                      cnt(me, ex, sl) * (int64_t)drowb);
+                } else {
+                  const int ex = me * E_loc + el;
+                  add((char*)L->o + rpos(el, sl, peer) * rowb,
+                      peer_buf(peer, moe_layer::P2P_COMB, spos_all[(size_t)peer * E * S + (size_t)ex * S + sl] * rowb),
+                      cnt(peer, ex, sl) * (int64_t)rowb);
+                }
+              }
+            }
+          }
+          p2p_nseg[dir][ch] = n;
+          p2p_total[dir][ch] = pr[n];
+        }
+      CUDA_TRY(cudaMemcpyAsync(L->p2p_segs, L->p2p_host, p2p_table_bytes(D), cudaMemcpyHostToDevice, st));
+    }
+    auto p2p_put = [&](int dir, int ch, cudaStream_t ps) -> moe_status_t {
+      const size_t slot = (size_t)dir * MOE_MAX_CHUNKS + ch;
+      auto* dsegs = reinterpret_cast<epsmoe::P2PSeg*>(L->p2p_segs) + slot * moe_layer::P2P_MAXS;
+      auto* dpre = reinterpret_cast<int64_t*>(reinterpret_cast<char*>(L->p2p_segs) + P2P_SEGS_BYTES) +
+                   slot * (moe_layer::P2P_MAXS + 1);
+      auto* dfp = reinterpret_cast<uint32_t**>(reinterpret_cast<char*>(L->p2p_segs) + P2P_SEGS_BYTES + P2P_PRE_BYTES) +
+                  slot * D;
+      KERNEL_TRY(launch_p2p_put(dsegs, dpre, p2p_nseg[dir][ch], p2p_total[dir][ch], 2 * L->comm_ctas,
+                                L->p2p_done + slot, dfp, D, epoch, ps));
+      TR_TRY(L->tr->p2p_after_put((int)slot, ps));
+      return MOE_OK;
+    };
     CUDA_TRY(cudaEventRecord(L->ev_ready, st));
     CUDA_TRY(cudaStreamWaitEvent(L->s_disp, L->ev_ready, 0));
     CUDA_TRY(cudaStreamWaitEvent(L->s_comb, L->ev_ready, 0));
@@ -994,10 +1163,17 @@ moe_status_t moe_layer_forward(moe_layer_t* L, const void* x, int64_t T, void* y
     char* dsend = fp8 ? (char*)L->sendq : (char*)L->send;
     char* drecv = fp8 ? (char*)L->recvq : (char*)L->recv;
     const size_t drow = fp8 ? (size_t)L->qpitch : row_bytes;
-    const size_t meta_bytes = (size_t)2 * k * sizeof(int32_t);
+    const size_t meta_bytes = (size_t)lr_meta_pitch(k) * sizeof(int32_t);
     auto dispatch = [&](int ch) -> moe_status_t {
       const int sl = ch % S, g0 = plan.group_begin[ch / S], g1 = plan.group_begin[ch / S + 1];
       int d0 = prof_rec(L, L->s_disp);
+      if (p2p) {
+        moe_status_t r = p2p_put(0, ch, L->s_disp);
+        if (r) return r;
+        prof_mark(L, MOE_STAGE_DISPATCH, d0, prof_rec(L, L->s_disp));
+        CUDA_TRY(cudaEventRecord(L->ev_disp[ch], L->s_disp));
+        return MOE_OK;
+      }
       TR_TRY(L->tr->group_start(0));
       if (lr_ep) {  // one unique-row message + its meta per peer (R16)
         char* urows = fp8 ? (char*)L->recvq : (char*)L->recvu;
@@ -1032,6 +1208,12 @@ moe_status_t moe_layer_forward(moe_layer_t* L, const void* x, int64_t T, void* y
       const int sl = ch % S, g0 = plan.group_begin[ch / S], g1 = plan.group_begin[ch / S + 1];
       CUDA_TRY(cudaStreamWaitEvent(L->s_comb, L->ev_gemm[ch], 0));
       int b0 = prof_rec(L, L->s_comb);
+      if (p2p) {
+        moe_status_t r = p2p_put(1, ch, L->s_comb);
+        if (r) return r;
+        prof_mark(L, MOE_STAGE_COMB_A2A, b0, prof_rec(L, L->s_comb));
+        return MOE_OK;
+      }
       TR_TRY(L->tr->group_start(1));
       if (lr_ep) {  // each unique row returns as its LocalReduce partial (R16)
         for (int peer = 0; peer < D; ++peer) {
@@ -1058,7 +1240,11 @@ moe_status_t moe_layer_forward(moe_layer_t* L, const void* x, int64_t T, void* y
     };
     auto compute = [&](int ch) -> moe_status_t {
       const int sl = ch % S, g0 = plan.group_begin[ch / S], g1 = plan.group_begin[ch / S + 1];
-      CUDA_TRY(cudaStreamWaitEvent(st, L->ev_disp[ch], 0));
+      CUDA_TRY(cudaStreamWaitEvent(st, L->ev_disp[ch], 0));  // (p2p: my puts read `send`)
+      if (p2p) {  // every source's rows
+        TR_TRY(L->tr->p2p_before_wait(ch, 1, st));
+        KERNEL_TRY(launch_p2p_wait(L->p2p_flags + (size_t)ch * D, D, epoch, st));
+      }
       const int64_t u0 = urecv[(size_t)ch * D], u1 = urecv[(size_t)(ch + 1) * D];
       if (lr_ep) {  // unique rows -> expert-major GEMM rows (R6 order, so the GEMMs are unchanged)
         KERNEL_TRY(launch_lr_expand(L->recvu, fp8 ? L->recvq : nullptr, L->qpitch, u0, u1, H, k, D, ch, L->lr_usrc_d,
@@ -1103,6 +1289,10 @@ moe_status_t moe_layer_forward(moe_layer_t* L, const void* x, int64_t T, void* y
     CUDA_TRY(cudaEventRecord(L->ev_comb_done, L->s_comb));
     CUDA_TRY(cudaStreamWaitEvent(st, L->ev_comb_done, 0));
     if (side) CUDA_TRY(cudaStreamWaitEvent(st, L->ev_shared, 0));
+    if (p2p) {  // every chunk's combine rows from every expert rank
+      TR_TRY(L->tr->p2p_before_wait(MOE_MAX_CHUNKS, plan.num_chunks, st));
+      KERNEL_TRY(launch_p2p_wait(L->p2p_flags + (size_t)MOE_MAX_CHUNKS * D, plan.num_chunks * D, epoch, st));
+    }
     int c0 = prof_rec(L, st);
     if (lr_ep)
       KERNEL_TRY(launch_lr_combine(L->comb, L->SF ? L->s : nullptr, (int)T, H, k, L->posg, y, st));

@@ -142,7 +142,7 @@ lr_permute_kernel(const __nv_bfloat16* __restrict__ x, int T, int H, int k, cons
     if (tg.lead) posg[(int64_t)t * k + rank] = dest;
     // meta of row dest: the group's (code, w) in slot order, then -1 / 0 padding
     int n = 0;
-    int32_t* m = meta + (int64_t)dest * 2 * k;
+    int32_t* m = meta + (int64_t)dest * lr_meta_pitch(k);
 #pragma unroll
     for (int j = 0; j < MAX_K; ++j) {
       const int gj = __shfl_sync(FULL, tg.g, j);
@@ -228,9 +228,9 @@ lr_expand_kernel(const __nv_bfloat16* __restrict__ rows, const uint8_t* __restri
     if (usrc_start[c * D + s] <= u) src = s;
   int R = -1;
   if (lane < k) {
-    const int code = meta[u * 2 * k + lane];
+    const int code = meta[u * lr_meta_pitch(k) + lane];
     if (code >= 0) R = recv_off[(code >> 24) * D + src] + (code & 0xFFFFFF);
-    meta[u * 2 * k + lane] = R;
+    meta[u * lr_meta_pitch(k) + lane] = R;
   }
   int Rs[MAX_K];
 #pragma unroll
@@ -262,8 +262,8 @@ lr_reduce_kernel(const __nv_bfloat16* __restrict__ o, const int32_t* __restrict_
   int R = -1;
   float w = 0.f;
   if (lane < k) {
-    R = meta[u * 2 * k + lane];
-    w = __int_as_float(meta[u * 2 * k + k + lane]);
+    R = meta[u * lr_meta_pitch(k) + lane];
+    w = __int_as_float(meta[u * lr_meta_pitch(k) + k + lane]);
   }
   int Rs[MAX_K];
   float ws[MAX_K];

@@ -6,6 +6,10 @@
 
 namespace epsmoe {
 
+// Words per dedup-row meta record: k slot codes, k weights, padded to 16 B so
+// records move as whole vectors.
+__host__ __device__ inline int lr_meta_pitch(int k) { return (2 * k + 3) & ~3; }
+
 // The plan's chunks as local-expert groups (R8), passed by value.
 struct LrChunks {
   int n;               // PN
@@ -18,7 +22,7 @@ int launch_lr_count(const int32_t* topk_idx, int T, int k, int E_loc, int D, con
                     int32_t* range_hist, cudaStream_t st);
 // One send row per distinct (t, g), rows (g asc, t asc) from u_start + range_off;
 // posg [T, k]: row of t's i-th group (ascending g), -1 padded; meta [rows, 2k]:
-// k slot codes ((local expert << 24) | pos - seg_start[e]) then k weights.
+// k slot codes ((local expert << 24) | pos - seg_start[e]) then k weights (pitch lr_meta_pitch(k)).
 // sendq != nullptr: packed FP8 rows (R15) instead of bf16 rows into send.
 int launch_lr_permute(const void* x, int T, int H, int k, const int32_t* topk_idx, const float* topk_w,
                       const int32_t* pos, const int32_t* seg_start, int E_loc, int D, const LrChunks& ch,

@@ -2,6 +2,9 @@
 // MOE_ERR_NCCL / MOE_ERR_CUDA on failure (message via set_error).
 #include "transport.h"
 
+#include <cuda.h>
+
+#include <cstring>
 #include <string>
 
 #include "../../include/epsmoe.h"
@@ -10,16 +13,69 @@
 namespace epsmoe {
 
 // ------------------------------------------------------------------ NCCL
-NcclTransport::~NcclTransport() {
-  for (auto c : comm_)
-    if (c) ncclCommDestroy(c);
-}
-
 static int nccl_err(ncclResult_t r, const char* what) {
   if (r == ncclSuccess) return 0;
   set_error(std::string(what) + ": " + ncclGetErrorString(r));
   return MOE_ERR_NCCL;
 }
+
+NcclTransport::~NcclTransport() {
+  for (void* p : opened_) cudaIpcCloseMemHandle(p);
+  for (auto c : comm_)
+    if (c) ncclCommDestroy(c);
+}
+
+int NcclTransport::map_peers(void* mine, std::vector<char*>& out) {
+  int nranks = 0, me = 0;
+  if (int e = nccl_err(ncclCommCount(comm_[0], &nranks), "ncclCommCount")) return e;
+  if (int e = nccl_err(ncclCommUserRank(comm_[0], &me), "ncclCommUserRank")) return e;
+  // handle of the whole allocation + this pointer's offset inside it
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  using RangeFn = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
+  void* fp = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fp, cudaEnableDefault, &q) != cudaSuccess ||
+      q != cudaDriverEntryPointSuccess || reinterpret_cast<RangeFn>(fp)(&base, &size, (CUdeviceptr)mine) != CUDA_SUCCESS) {
+    set_error("map_peers: cuMemGetAddressRange failed");
+    return MOE_ERR_CUDA;
+  }
+  cudaIpcMemHandle_t h;
+  if (cudaIpcGetMemHandle(&h, (void*)base) != cudaSuccess) {
+    set_error("map_peers: cudaIpcGetMemHandle failed (workspace must come from cudaMalloc)");
+    return MOE_ERR_CUDA;
+  }
+  constexpr int W = (int)(sizeof(cudaIpcMemHandle_t) / 4) + 2;  // handle words + 64-bit offset
+  int32_t rec[W];
+  std::memcpy(rec, &h, sizeof(h));
+  const int64_t off = (int64_t)((CUdeviceptr)mine - base);
+  std::memcpy(rec + W - 2, &off, sizeof(off));
+  int32_t* dev = nullptr;
+  if (cudaMalloc(&dev, sizeof(int32_t) * W * (nranks + 1)) != cudaSuccess) return MOE_ERR_CUDA;
+  cudaMemcpy(dev, rec, sizeof(rec), cudaMemcpyHostToDevice);
+  int e = allgather_i32(dev, dev + W, W, 0);
+  std::vector<int32_t> all((size_t)W * nranks);
+  if (!e) e = cudaMemcpy(all.data(), dev + W, sizeof(int32_t) * W * nranks, cudaMemcpyDeviceToHost) ? MOE_ERR_CUDA : 0;
+  cudaFree(dev);
+  if (e) return e;
+  out.assign(nranks, nullptr);
+  for (int r = 0; r < nranks; ++r) {
+    if (r == me) { out[r] = (char*)mine; continue; }
+    cudaIpcMemHandle_t hr;
+    int64_t offr = 0;
+    std::memcpy(&hr, all.data() + (size_t)r * W, sizeof(hr));
+    std::memcpy(&offr, all.data() + (size_t)r * W + W - 2, sizeof(offr));
+    void* p = nullptr;
+    if (cudaIpcOpenMemHandle(&p, hr, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+      set_error("map_peers: cudaIpcOpenMemHandle failed for rank " + std::to_string(r));
+      return MOE_ERR_CUDA;
+    }
+    opened_.push_back(p);
+    out[r] = (char*)p + offr;
+  }
+  return 0;
+}
+
 
 int NcclTransport::allgather_i32(const int32_t* send, int32_t* recv, size_t count, cudaStream_t st) {
   return nccl_err(ncclAllGather(send, recv, count, ncclInt32, comm_[0], st), "ncclAllGather");
@@ -34,16 +90,20 @@ int NcclTransport::recv(void* buf, size_t bytes, int peer, int channel, cudaStre
 int NcclTransport::group_end(int, cudaStream_t) { return nccl_err(ncclGroupEnd(), "ncclGroupEnd"); }
 
 // ------------------------------------------------------------------ local
-LocalGroup::LocalGroup(int n) : ep(n), sends(n), recvs(n), gather_src(n), ev_ready(n), ev_done(n) {
+LocalGroup::LocalGroup(int n)
+    : ep(n), sends(n), recvs(n), gather_src(n), peer_ptr(n), ev_put(n), ev_ready(n), ev_done(n) {
   for (int r = 0; r < n; ++r) {
     cudaEventCreateWithFlags(&ev_ready[r], cudaEventDisableTiming);
     cudaEventCreateWithFlags(&ev_done[r], cudaEventDisableTiming);
+    ev_put[r].resize(2 * 64);
+    for (auto& e : ev_put[r]) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
   }
 }
 LocalGroup::~LocalGroup() {
   for (int r = 0; r < ep; ++r) {
     cudaEventDestroy(ev_ready[r]);
     cudaEventDestroy(ev_done[r]);
+    for (auto e : ev_put[r]) cudaEventDestroy(e);
   }
 }
 void LocalGroup::barrier() {
@@ -81,6 +141,28 @@ int LocalTransport::allgather_i32(const int32_t* send, int32_t* recv, size_t cou
   for (int p = 0; p < g.ep; ++p)  // sources stay untouched until every reader copied them
     if (int e = cuda_err(cudaStreamWaitEvent(st, g.ev_done[p], 0), "cudaStreamWaitEvent")) return e;
   g.barrier();
+  return 0;
+}
+
+int LocalTransport::map_peers(void* mine, std::vector<char*>& out) {
+  LocalGroup& g = *g_;
+  g.peer_ptr[rank_] = (char*)mine;
+  g.barrier();
+  out = g.peer_ptr;
+  g.barrier();
+  return 0;
+}
+
+int LocalTransport::p2p_after_put(int slot, cudaStream_t ps) {
+  return cuda_err(cudaEventRecord(g_->ev_put[rank_][slot], ps), "cudaEventRecord");
+}
+int LocalTransport::p2p_before_wait(int slot0, int nslots, cudaStream_t st) {
+  LocalGroup& g = *g_;
+  g.barrier();  // every rank has issued (recorded) these puts
+  for (int p = 0; p < g.ep; ++p)
+    for (int s = slot0; s < slot0 + nslots; ++s)
+      if (int e = cuda_err(cudaStreamWaitEvent(st, g.ev_put[p][s], 0), "cudaStreamWaitEvent")) return e;
+  g.barrier();  // nobody re-records before every rank waited
   return 0;
 }
 

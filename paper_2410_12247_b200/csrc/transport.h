@@ -31,6 +31,16 @@ class Transport {
   virtual int recv(void* buf, size_t bytes, int peer, int channel, cudaStream_t st) = 0;
   virtual int group_end(int channel, cudaStream_t st) = 0;
   virtual const char* name() const = 0;
+  // Collective: every rank's `mine` (a device allocation of identical layout on
+  // every rank) mapped into this process; out[rank] = mine.  For the put-kernel
+  // all2all (a2a_p2p).
+  virtual int map_peers(void* mine, std::vector<char*>& out) = 0;
+  // a2a_p2p hooks around the device flags (no-ops across processes).  The
+  // in-process test group shares one GPU's hardware queues between ranks, so a
+  // rank's spinning flag-wait kernel could sit in front of the put kernel it
+  // waits for; there the put is also ordered by a CUDA event.
+  virtual int p2p_after_put(int slot, cudaStream_t) { (void)slot; return 0; }
+  virtual int p2p_before_wait(int slot0, int nslots, cudaStream_t) { (void)slot0; (void)nslots; return 0; }
 };
 
 class NcclTransport : public Transport {
@@ -43,9 +53,13 @@ class NcclTransport : public Transport {
   int recv(void* buf, size_t bytes, int peer, int channel, cudaStream_t st) override;
   int group_end(int channel, cudaStream_t st) override;
   const char* name() const override { return "nccl"; }
+  // cudaIpc handles of the allocations holding `mine` (+ offset), allgathered
+  // over communicator 0 and opened with peer access.
+  int map_peers(void* mine, std::vector<char*>& out) override;
 
  private:
   ncclComm_t comm_[2];
+  std::vector<void*> opened_;  // cudaIpcOpenMemHandle results, closed on destruction
 };
 
 // Shared rendezvous state of the ep local ranks (moe_local_group_create).
@@ -66,6 +80,8 @@ struct LocalGroup {
   uint64_t generation = 0;
   std::vector<std::vector<Op>> sends, recvs;  // [rank] ops posted in the current group
   std::vector<const void*> gather_src;        // [rank] allgather source pointers
+  std::vector<char*> peer_ptr;                // [rank] map_peers slots
+  std::vector<std::vector<cudaEvent_t>> ev_put;  // [rank][slot] a2a_p2p put completions
   std::vector<cudaEvent_t> ev_ready, ev_done; // [rank]
 };
 
@@ -78,6 +94,9 @@ class LocalTransport : public Transport {
   int recv(void* buf, size_t bytes, int peer, int channel, cudaStream_t st) override;
   int group_end(int channel, cudaStream_t st) override;
   const char* name() const override { return "local"; }
+  int map_peers(void* mine, std::vector<char*>& out) override;  // same device: the pointers themselves
+  int p2p_after_put(int slot, cudaStream_t ps) override;
+  int p2p_before_wait(int slot0, int nslots, cudaStream_t st) override;
 
  private:
   LocalGroup* g_;

@@ -22,7 +22,7 @@ from .gpu_util import assert_close, dev_bf16, to_f32
 pytestmark = pytest.mark.gpu
 
 
-def _ep_forward(inp, k, norm, D, plan=None, skew_bias=None, fp8=False, lr=False):
+def _ep_forward(inp, k, norm, D, plan=None, skew_bias=None, fp8=False, lr=False, p2p=False):
     E, H, F, T = inp.E, inp.H, inp.F, inp.T
     E_loc = E // D
     start = oracle.token_shards(T, D)
@@ -38,7 +38,8 @@ def _ep_forward(inp, k, norm, D, plan=None, skew_bias=None, fp8=False, lr=False)
             w["router_bias"] = torch.from_numpy(skew_bias).cuda()
         T_loc = int(start[r + 1] - start[r])
         layers.append(MoELayer(E, k, H, F, w, S=inp.S, Fs=inp.Fs, ep=D, rank=r, max_tokens=max(T_loc, 1),
-                               norm_topk=norm, local_group=group, dispatch_fp8=fp8, local_reduce=lr))
+                               norm_topk=norm, local_group=group, dispatch_fp8=fp8, local_reduce=lr,
+                               a2a_p2p=p2p))
         xs.append(dev_bf16(inp.x[start[r]:start[r + 1]]))
     ys, bufs, errs = [None] * D, [None] * D, []
 
@@ -310,5 +311,80 @@ def test_ep_stage_profiling_and_exposed_a2a():
         assert st["dispatch_a2a"][1] == N and st["combine_a2a"][1] == N
         assert st["total"][0] > 0 and st["gateup"][0] > 0 and st["shared"][0] > 0
         assert 0.0 <= st["exposed_a2a"][0] <= st["total"][0]
+    for L in layers:
+        L.close()
+
+
+# ---------------------------------------------------------------- own put-kernel all2all (a2a_p2p)
+
+@pytest.mark.parametrize("D,N,S,fp8,lr", [(2, 2, 1, False, False), (4, 3, 1, False, False), (8, 2, 1, False, False),
+                                          (2, 1, 3, False, False), (4, 2, 1, True, False), (2, 2, 1, False, True),
+                                          (4, 1, 1, True, True)])
+def test_p2p_put_all2all(D, N, S, fp8, lr):
+    """a2a_p2p: each rank's put kernel stores its rows straight into the peers'
+    workspaces (here: the other ranks' workspaces on the same GPU) and raises
+    per-(chunk, source) flags; consumers wait on them.  y == the NCCL-path
+    layout's result: EP = 1 bit for bit (per-pair path) or the oracle's R16."""
+    E = 16
+    inp = Inputs(E=E, k=4, H=256, F=256, S=1, Fs=128, T=919, seed=100 + D + N, grid=True)
+    plan = make_plan(N * S, MOE_GEMM_GROUPED, token_slices=S)
+    y, bufs = _ep_forward(inp, 4, 1, D, plan, fp8=fp8, lr=lr, p2p=True)
+    # second forward on fresh layers again (flags / epochs start over) and a
+    # repeated forward on the same layers are covered by the layer reuse below
+    if lr:
+        ref = oracle.moe_layer(inp.x, inp.w_router, inp.w_gate, inp.w_up, inp.w_down, k=4, norm_topk=1,
+                               ws_gate_bits=inp.ws_gate, ws_up_bits=inp.ws_up, ws_down_bits=inp.ws_down, D=D, N=N,
+                               local_reduce=True, dispatch_fp8=fp8)
+        idx = np.concatenate([b["topk_idx"].cpu().numpy() for b in bufs])
+        same = (idx == ref["idx"]).all(axis=1)
+        assert same.mean() > 0.99
+        assert_close(y[same], ref["y"][same], f"p2p LR EP{D}")
+    else:
+        y1 = _ep1_forward(inp, 4, 1, make_plan(1, MOE_GEMM_GROUPED), fp8=fp8)
+        assert np.array_equal(y, y1)
+
+
+def test_p2p_repeated_forwards_same_layers():
+    """Epoch-tagged flags: back-to-back forwards on the same layers (no flag
+    reset) stay correct, with different inputs each time."""
+    D = 4
+    E_loc = 4
+    group = LocalGroup(D)
+    inps = [Inputs(E=16, k=2, H=256, F=256, T=640, seed=s, grid=True) for s in (1, 2, 3)]
+    inp0 = inps[0]
+    start = oracle.token_shards(640, D)
+    layers = []
+    for r in range(D):
+        w = dict(w_router=dev_bf16(inp0.w_router), w_gate=dev_bf16(inp0.w_gate[r * E_loc:(r + 1) * E_loc]),
+                 w_up=dev_bf16(inp0.w_up[r * E_loc:(r + 1) * E_loc]),
+                 w_down=dev_bf16(inp0.w_down[r * E_loc:(r + 1) * E_loc]))
+        layers.append(MoELayer(16, 2, 256, 256, w, ep=D, rank=r, max_tokens=160, norm_topk=1, local_group=group,
+                               a2a_p2p=True))
+    outs, errs = [[None] * D for _ in inps], []
+
+    def worker(r):
+        try:
+            torch.cuda.set_device(0)
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                for i, inp in enumerate(inps):
+                    x = dev_bf16(inp.x[start[r]:start[r + 1]])
+                    outs[i][r] = layers[r].forward(x, plan=make_plan(2, MOE_GEMM_GROUPED), stream=s)
+                s.synchronize()
+        except Exception as e:  # pragma: no cover
+            errs.append(repr(e))
+
+    th = [threading.Thread(target=worker, args=(r,), daemon=True) for r in range(D)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=120)
+    assert not errs, errs
+    for i, inp in enumerate(inps):   # same weights (seed-independent x only differs): compare with EP = 1
+        x_bits = inp.x
+        w_inp = Inputs(E=16, k=2, H=256, F=256, T=640, seed=1, grid=True)
+        w_inp.x = x_bits
+        y1 = _ep1_forward(w_inp, 2, 1, make_plan(1, MOE_GEMM_GROUPED))
+        assert np.array_equal(torch.cat(outs[i]).float().cpu().numpy(), y1)
     for L in layers:
         L.close()
