@@ -57,6 +57,8 @@ def parse():
     p.add_argument("--route-groups", type=int, default=0, help="device-limited routing groups (NEXT-4, R17)")
     p.add_argument("--route-topk-groups", type=int, default=0, help="M: groups a token may use (R17)")
     p.add_argument("--token-slices", type=int, default=1, help="with --chunks: chunks = groups x slices (R8)")
+    p.add_argument("--a2a", default="nccl", choices=["nccl", "p2p"],
+                   help="ep > 1 all2all: NCCL send/recv, or the layer's put kernels over NVLink peer memory")
     return p.parse_args()
 
 
@@ -203,6 +205,11 @@ def feature_opts(args):
                 route_groups=int(args.route_groups), route_topk_groups=int(args.route_topk_groups))
 
 
+def layer_opts(args):
+    """feature_opts + the all2all data plane (no effect on the arithmetic)."""
+    return dict(feature_opts(args), a2a_p2p=args.a2a == "p2p")
+
+
 def cpu_baseline(cfg, seed, skew, sample=0, opts=None):
     # sized for ~10-20 s of oracle work on a 16-core host (the contract's bounded sample)
     n = sample or {"tiny": 256, "dsv2_lite": 256, "mixtral": 24, "dsv2": 48, "dsv2_decode": 48,
@@ -301,7 +308,7 @@ def ours(args, cfg):
         uid_d, uid_c = ids
     opts = feature_opts(args)
     layer = MoELayer(E, k, H, F, w, S=S, Fs=Fs, ep=D, rank=rank, max_tokens=T_loc, norm_topk=cfg["norm_topk"],
-                     uid_dispatch=uid_d, uid_combine=uid_c, device=dev, **opts)
+                     uid_dispatch=uid_d, uid_combine=uid_c, device=dev, **layer_opts(args))
     plan = None
     if args.chunks or args.kind != "auto" or args.sm_gemm or args.tile_m:
         kind = {"auto": MOE_GEMM_AUTO, "grouped": MOE_GEMM_GROUPED, "dense": MOE_GEMM_DENSE}[args.kind]
@@ -452,7 +459,7 @@ def ours(args, cfg):
                 "config": {"workload": cfg["name"], "E": E, "k": k, "H": H, "F": F, "shared": S, "shared_ffn": Fs,
                            "global_tokens": T, "ep": D, "parallelism": f"ep{D}" + (f"+dp{D}" if D > 1 else ""),
                            "skew": args.skew, "l2": "inputs > L2 (x alone %.0f MB), no flush" % (T_loc * H * 2 / 1e6),
-                           **opts, "plan": plan_used},
+                           **opts, "a2a": args.a2a if D > 1 else None, "plan": plan_used},
                 "roofline": roofline, "layer_roofline": layer_roofline,
                 "exposed_a2a_ms": stages.get("exposed_a2a", 0.0), "stages_ms": stages,
                 "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk}
