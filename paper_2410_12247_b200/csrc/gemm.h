@@ -13,6 +13,14 @@ enum EpiKind : int {
                    // y = bf16(fmaf chain over slots j of w_j * o[pos[t][j]] on fp32(s))
 };
 
+// Output scatter of a DownGemm fused with the combine all2all (a2a_p2p): GEMM
+// rows [r0, r0 + n) go to consecutive rows starting at dst (bf16, row pitch
+// ldo), typically another rank's combine buffer in mapped peer memory.
+struct GemmRowSeg {
+  int64_t r0, n;
+  char* dst;
+};
+
 // One grouped GEMM launch: for each group g (an expert), rows
 // [row_start[g], row_start[g] + row_count[g]) of A (K-major, [rows, K] bf16)
 // times B_g^T where B_g = rows [(b_base + g) * b_group_rows, ...) of B
@@ -51,6 +59,14 @@ struct GemmArgs {
   const float* comb_w;
   int comb_k;                  // 1..8
   double rows_hint;            // expected rows per group (0 = unknown): picks the tile raster
+  // EPI_BF16 only: scatter the output rows (device table sorted by r0; rows in
+  // no segment are dropped) and, once every CTA's stores are system-visible,
+  // set *sig_flags[i] = sig_epoch (i < nsig) from the last CTA.
+  const GemmRowSeg* rseg;
+  int nrseg;
+  uint32_t* const* sig_flags;
+  int nsig;
+  uint32_t sig_epoch;
 };
 
 // Launch on `stream`.  Returns a cudaError_t-compatible code (0 = success).

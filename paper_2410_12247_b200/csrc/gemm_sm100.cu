@@ -81,6 +81,11 @@ struct KParams {
   const int32_t* a_row_index;
   const uint8_t* a_ptr;   // GATHER: A base (row pitch K * 2 bytes)
   int32_t* tile_counter;  // [2]: next ticket, CTAs finished (reset by the last CTA)
+  const GemmRowSeg* rseg;       // EPI_BF16 output scatter (see GemmArgs)
+  int nrseg;
+  uint32_t* const* sig_flags;
+  int nsig;
+  uint32_t sig_epoch;
   const __nv_bfloat16* comb_o;  // EPI_COMBINE (see GemmArgs)
   const int32_t* comb_pos;
   const float* comb_w;
@@ -541,6 +546,41 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
           store_chunk(pk, stg, out0 + c * 32, p.ldo, vr, lane, p.tma_store ? &tmO : nullptr, nt * 128 + c * 32,
                       (int)(grow - lane));
         }
+      } else if (EPI == EPI_BF16 && p.rseg) {
+        // DownGemm fused with the combine all2all: each row is stored straight
+        // into its destination (a peer's combine buffer) while later tiles compute
+        char* rowp = nullptr;
+        if (valid) {
+          int lo = 0, hi = p.nrseg - 1;
+          while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (p.rseg[mid].r0 <= grow) lo = mid; else hi = mid - 1;
+          }
+          const GemmRowSeg sg = p.rseg[lo];
+          if (grow >= sg.r0 && grow < sg.r0 + sg.n) rowp = sg.dst + (grow - sg.r0) * p.ldo * 2;
+        }
+        const int jq = lane & 3;
+#pragma unroll 1
+        for (int c = 0; c < BN / 32; ++c) {
+          const int col0 = nt * BN + c * 32;
+          if (col0 >= p.N) break;
+          uint32_t r[32], pk[16];
+          ptx::tmem_ld32(taddr + c * 32, r);
+          ptx::tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 16; ++i) pk[i] = pack_bf16(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1]));
+          stage_write(pk, stg, lane, false);
+          __syncwarp();
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int rr = i * 8 + (lane >> 2);
+            char* dp = reinterpret_cast<char*>(
+                __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(rowp), rr));
+            const uint4 v = *stage_piece(stg, rr, jq);
+            if (rr < vr && dp) reinterpret_cast<uint4*>(dp + (size_t)col0 * 2)[jq] = v;
+          }
+          __syncwarp();
+        }
       } else if (EPI == EPI_BF16) {
         __nv_bfloat16* out0 = reinterpret_cast<__nv_bfloat16*>(p.out) + (grow - lane) * p.ldo + nt * BN;
 #pragma unroll 1
@@ -657,16 +697,23 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
     }
   }
 
+  if (p.nsig) __threadfence_system();  // scattered rows visible to the peers before the flags
   ptx::tc_fence_before();
   __syncthreads();
   if constexpr (CG == 2) ptx::cluster_sync();  // no CTA leaves while its peer may still signal it
   ptx::tc_fence_after();
   if (warp == 1) ptx::tmem_dealloc<TMEM_COLS, CG>(tmem_base);
   if (warp >= 2 && lane == 0 && p.tma_store) ptx::bulk_wait0();  // output stores complete
-  if (p.dynamic && threadIdx.x == 0) {
-    // the last CTA to finish resets the ticket counter for the next launch
+  if ((p.dynamic || p.nsig) && threadIdx.x == 0) {
+    // the last CTA to finish resets the ticket counter for the next launch and
+    // raises the completion flags of a fused scatter
     __threadfence();
     if (atomicAdd(p.tile_counter + 1, 1) == (int)gridDim.x - 1) {
+      if (p.nsig) {
+        __threadfence_system();
+        for (int i = 0; i < p.nsig; ++i)
+          asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p.sig_flags[i]), "r"(p.sig_epoch) : "memory");
+      }
       p.tile_counter[0] = 0;
       p.tile_counter[1] = 0;
       __threadfence();
@@ -789,6 +836,11 @@ int launch_epi(const GemmArgs& a, cudaStream_t stream) {
   p.a_row_index = a.a_row_index;
   p.a_ptr = reinterpret_cast<const uint8_t*>(a.A);
   p.row_mode = a.row_mode;
+  p.rseg = (EPI == EPI_BF16) ? a.rseg : nullptr;
+  p.nrseg = a.nrseg;
+  p.sig_flags = a.sig_flags;
+  p.nsig = a.sig_flags ? a.nsig : 0;
+  p.sig_epoch = a.sig_epoch;
   p.comb_o = reinterpret_cast<const __nv_bfloat16*>(a.comb_o);
   p.comb_pos = a.comb_pos;
   p.comb_w = a.comb_w;
@@ -797,7 +849,7 @@ int launch_epi(const GemmArgs& a, cudaStream_t stream) {
   CUtensorMap tO;
   std::memset(&tO, 0, sizeof(tO));
   p.tma_store = 0;
-  if (EPI != EPI_F32 && env_int("EPSMOE_TMA_STORE", 1) &&
+  if (EPI != EPI_F32 && !p.rseg && env_int("EPSMOE_TMA_STORE", 1) &&
       make_tmap_out(&tO, a.out, a.out_rows > 0 ? a.out_rows : a.a_rows, a.ldo))
     p.tma_store = 1;
   // Launches that may run concurrently must use different counters (caller's).

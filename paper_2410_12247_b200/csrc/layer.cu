@@ -59,10 +59,11 @@ struct moe_layer {
   std::vector<int64_t> peer_off;
   uint32_t p2p_epoch = 0;
   uint32_t *p2p_flags = nullptr, *p2p_done = nullptr;
-  epsmoe::P2PSeg* p2p_segs = nullptr;  // device [2][64][P2P_MAXS]
-  int64_t* p2p_pre = nullptr;          // device [2][64][P2P_MAXS + 1]
-  uint32_t** p2p_fptr = nullptr;       // device [2][64][ep]: consumer flag addresses
-  char* p2p_host = nullptr;            // pinned mirror of segs | pre | fptr
+  // device tables [segs [2][64][P2P_MAXS] | pre [2][64][P2P_MAXS+1] | consumer flag
+  // addresses [2][64][ep] | fused-combine row segments [64][P2P_MAXS]], pinned mirror
+  char* p2p_tab = nullptr;
+  char* p2p_host = nullptr;
+  bool p2p_fuse = true;  // EPSMOE_P2P_FUSE=0: combine by put kernel instead of the DownGemm's scatter
   int32_t* ughist_host = nullptr;  // pinned [ep*256]
   void *x_dev = nullptr, *y_dev = nullptr;  // staging for forward_host
   // host
@@ -170,7 +171,9 @@ struct Carve {
 // a2a_p2p segment tables (host mirror == device layout): segs | pre | flag pointers
 constexpr size_t P2P_SEGS_BYTES = sizeof(epsmoe::P2PSeg) * 2 * MOE_MAX_CHUNKS * moe_layer::P2P_MAXS;
 constexpr size_t P2P_PRE_BYTES = sizeof(int64_t) * 2 * MOE_MAX_CHUNKS * (moe_layer::P2P_MAXS + 1);
-size_t p2p_table_bytes(int ep) { return P2P_SEGS_BYTES + P2P_PRE_BYTES + sizeof(uint32_t*) * 2 * MOE_MAX_CHUNKS * ep; }
+constexpr size_t P2P_RSEG_BYTES = sizeof(epsmoe::GemmRowSeg) * MOE_MAX_CHUNKS * moe_layer::P2P_MAXS;
+size_t p2p_fptr_bytes(int ep) { return sizeof(uint32_t*) * 2 * MOE_MAX_CHUNKS * ep; }
+size_t p2p_table_bytes(int ep) { return P2P_SEGS_BYTES + P2P_PRE_BYTES + p2p_fptr_bytes(ep) + P2P_RSEG_BYTES; }
 
 int validate(const moe_config_t* c) {
   if (!c) return MOE_ERR_INVALID;
@@ -251,9 +254,7 @@ size_t carve(moe_layer* L, char* base) {
   if (D > 1 && c.a2a_p2p) {
     L->p2p_flags = cv.take<uint32_t>(2 * MOE_MAX_CHUNKS * D);
     L->p2p_done = cv.take<uint32_t>(2 * MOE_MAX_CHUNKS);
-    L->p2p_segs = cv.take<epsmoe::P2PSeg>((size_t)2 * MOE_MAX_CHUNKS * moe_layer::P2P_MAXS);
-    L->p2p_pre = cv.take<int64_t>((size_t)2 * MOE_MAX_CHUNKS * (moe_layer::P2P_MAXS + 1));
-    L->p2p_fptr = cv.take<uint32_t*>((size_t)2 * MOE_MAX_CHUNKS * D);
+    L->p2p_tab = cv.take<char>(p2p_table_bytes((int)D));
   }
   L->hs = SF ? cv.take<uint16_t>(T * SF) : nullptr;
   L->s = SF ? cv.take<uint16_t>(T * H) : nullptr;
@@ -309,7 +310,8 @@ int pick_cta_pair(const moe_plan_t& plan, double mean_rows) {
 // then DownGemm.  Rows of expert g are [row_start[g], +row_count[g]) of A.
 int compute_moe(moe_layer* L, const void* A, int64_t a_rows, const int32_t* row_start, const int32_t* row_count,
                 int g0, int g1, int kind, int num_ctas, int cta_pair, double rows_per_group, cudaStream_t st,
-                const int32_t* a_row_index = nullptr) {
+                const int32_t* a_row_index = nullptr, const GemmRowSeg* down_rseg = nullptr, int down_nrseg = 0,
+                uint32_t* const* down_sig = nullptr, int down_nsig = 0, uint32_t down_epoch = 0) {
   const moe_config_t& c = L->cfg;
   GemmArgs g1a = base_args(EPI_SWIGLU, num_ctas);
   g1a.rows_hint = rows_per_group;
@@ -329,6 +331,11 @@ int compute_moe(moe_layer* L, const void* A, int64_t a_rows, const int32_t* row_
   g1a.out_rows = L->gemm_rows_cap;
   GemmArgs g2a = base_args(EPI_BF16, num_ctas);
   g2a.rows_hint = rows_per_group;
+  g2a.rseg = down_rseg;  // DownGemm fused with the combine all2all (a2a_p2p)
+  g2a.nrseg = down_nrseg;
+  g2a.sig_flags = down_sig;
+  g2a.nsig = down_nsig;
+  g2a.sig_epoch = down_epoch;
   g2a.cta_pair = cta_pair;
   g2a.tile_counter = L->tickets;
   g2a.A = L->h;
@@ -475,7 +482,7 @@ static moe_status_t create_impl(const moe_config_t* cfg, const moe_weights_t* w,
                     cudaHostAllocDefault) != cudaSuccess ||
       (cfg->ep > 1 && cudaHostAlloc(&L->gslice_host, sizeof(int32_t) * cfg->ep * cfg->num_experts * MOE_MAX_CHUNKS,
                                     cudaHostAllocDefault) != cudaSuccess) ||
-      (L->p2p_segs && cudaHostAlloc(&L->p2p_host, p2p_table_bytes(cfg->ep), cudaHostAllocDefault) != cudaSuccess) ||
+      (L->p2p_tab && cudaHostAlloc(&L->p2p_host, p2p_table_bytes(cfg->ep), cudaHostAllocDefault) != cudaSuccess) ||
       cudaHostAlloc(&L->ughist_host, sizeof(int32_t) * cfg->ep * MOE_MAX_EXPERTS, cudaHostAllocDefault) != cudaSuccess) {
     set_error("cudaHostAlloc failed");
     return fail(MOE_ERR_CUDA);
@@ -484,6 +491,7 @@ static moe_status_t create_impl(const moe_config_t* cfg, const moe_weights_t* w,
   if (const char* ov = std::getenv("EPSMOE_OVERLAP_SHARED")) L->overlap_shared = std::atoi(ov) != 0;
   if (const char* fc = std::getenv("EPSMOE_FUSE_COMBINE")) L->fuse_combine = std::atoi(fc);
   if (const char* gv = std::getenv("EPSMOE_GATHER")) L->gather_a = std::atoi(gv) != 0;
+  if (const char* pf = std::getenv("EPSMOE_P2P_FUSE")) L->p2p_fuse = std::atoi(pf) != 0;
   if (const char* sv = std::getenv("EPSMOE_SPLIT_REM")) L->split_rem = std::atoi(sv) != 0;
   if (cfg->ep > 1) {
     const char* cv = std::getenv("EPSMOE_COMM_CTAS");
@@ -1027,6 +1035,10 @@ moe_status_t moe_layer_forward(moe_layer_t* L, const void* x, int64_t T, void* y
     uint32_t epoch = 0;
     int p2p_nseg[2][MOE_MAX_CHUNKS] = {};
     int64_t p2p_total[2][MOE_MAX_CHUNKS] = {};
+    // fused combine: the chunk's DownGemm scatters its rows into the home ranks'
+    // combine buffers (one GEMM launch per chunk: its experts share one kind)
+    bool fuse_comb[MOE_MAX_CHUNKS] = {};
+    int fuse_nrseg[MOE_MAX_CHUNKS] = {};
     if (p2p) {
       if (L->peer_ws.empty()) {  // first forward (collective): map the peers, learn their layouts
         TR_TRY(L->tr->map_peers(L->ws_base, L->peer_ws));
@@ -1140,16 +1152,36 @@ moe_status_t moe_layer_forward(moe_layer_t* L, const void* x, int64_t T, void* y
           }
           p2p_nseg[dir][ch] = n;
           p2p_total[dir][ch] = pr[n];
+          if (dir == 1 && L->p2p_fuse && !lr_ep && !L->split_rem) {
+            bool one_kind = true;
+            for (int el = g0 + 1; el < g1; ++el) one_kind &= plan.expert_kind[el] == plan.expert_kind[g0];
+            if (one_kind) {
+              auto* rs = reinterpret_cast<epsmoe::GemmRowSeg*>(L->p2p_host + P2P_SEGS_BYTES + P2P_PRE_BYTES +
+                                                                 p2p_fptr_bytes(D)) +
+                         (size_t)ch * moe_layer::P2P_MAXS;
+              int nr = 0;
+              for (int el = g0; el < g1; ++el)  // GEMM rows (e_l, slice, src) ascending
+                for (int src = 0; src < D; ++src) {
+                  const int ex = me * E_loc + el;
+                  const int64_t rows = cnt(src, ex, sl);
+                  if (!rows || nr >= moe_layer::P2P_MAXS) continue;
+                  rs[nr].r0 = rpos(el, sl, src);
+                  rs[nr].n = rows;
+                  rs[nr].dst = peer_buf(src, moe_layer::P2P_COMB, spos_all[(size_t)src * E * S + (size_t)ex * S + sl] * rowb);
+                  ++nr;
+                }
+              fuse_comb[ch] = true;
+              fuse_nrseg[ch] = nr;
+            }
+          }
         }
-      CUDA_TRY(cudaMemcpyAsync(L->p2p_segs, L->p2p_host, p2p_table_bytes(D), cudaMemcpyHostToDevice, st));
+      CUDA_TRY(cudaMemcpyAsync(L->p2p_tab, L->p2p_host, p2p_table_bytes(D), cudaMemcpyHostToDevice, st));
     }
     auto p2p_put = [&](int dir, int ch, cudaStream_t ps) -> moe_status_t {
       const size_t slot = (size_t)dir * MOE_MAX_CHUNKS + ch;
-      auto* dsegs = reinterpret_cast<epsmoe::P2PSeg*>(L->p2p_segs) + slot * moe_layer::P2P_MAXS;
-      auto* dpre = reinterpret_cast<int64_t*>(reinterpret_cast<char*>(L->p2p_segs) + P2P_SEGS_BYTES) +
-                   slot * (moe_layer::P2P_MAXS + 1);
-      auto* dfp = reinterpret_cast<uint32_t**>(reinterpret_cast<char*>(L->p2p_segs) + P2P_SEGS_BYTES + P2P_PRE_BYTES) +
-                  slot * D;
+      auto* dsegs = reinterpret_cast<epsmoe::P2PSeg*>(L->p2p_tab) + slot * moe_layer::P2P_MAXS;
+      auto* dpre = reinterpret_cast<int64_t*>(L->p2p_tab + P2P_SEGS_BYTES) + slot * (moe_layer::P2P_MAXS + 1);
+      auto* dfp = reinterpret_cast<uint32_t**>(L->p2p_tab + P2P_SEGS_BYTES + P2P_PRE_BYTES) + slot * D;
       KERNEL_TRY(launch_p2p_put(dsegs, dpre, p2p_nseg[dir][ch], p2p_total[dir][ch], 2 * L->comm_ctas,
                                 L->p2p_done + slot, dfp, D, epoch, ps));
       TR_TRY(L->tr->p2p_after_put((int)slot, ps));
@@ -1209,8 +1241,10 @@ moe_status_t moe_layer_forward(moe_layer_t* L, const void* x, int64_t T, void* y
       CUDA_TRY(cudaStreamWaitEvent(L->s_comb, L->ev_gemm[ch], 0));
       int b0 = prof_rec(L, L->s_comb);
       if (p2p) {
-        moe_status_t r = p2p_put(1, ch, L->s_comb);
-        if (r) return r;
+        if (!fuse_comb[ch]) {
+          moe_status_t r = p2p_put(1, ch, L->s_comb);
+          if (r) return r;
+        }
         prof_mark(L, MOE_STAGE_COMB_A2A, b0, prof_rec(L, L->s_comb));
         return MOE_OK;
       }
@@ -1265,14 +1299,23 @@ moe_status_t moe_layer_forward(moe_layer_t* L, const void* x, int64_t T, void* y
         while (b < g1 && plan.expert_kind[b] == plan.expert_kind[a]) ++b;
         double rows = 0;
         for (int el = a; el < b; ++el) rows += tcount[ch * E_loc + el];
-        int err = compute_moe(L, L->recv, L->recv_cap, L->recv_start_d + ch * E_loc, L->recv_count_d + ch * E_loc,
-                              a, b, plan.expert_kind[a], num_ctas, pick_cta_pair(plan, rows / (b - a)), rows / (b - a),
-                              st);
+        const bool fz = p2p && fuse_comb[ch];
+        const size_t cslot = (size_t)MOE_MAX_CHUNKS + ch;
+        int err = compute_moe(
+            L, L->recv, L->recv_cap, L->recv_start_d + ch * E_loc, L->recv_count_d + ch * E_loc, a, b,
+            plan.expert_kind[a], num_ctas, pick_cta_pair(plan, rows / (b - a)), rows / (b - a), st, nullptr,
+            fz ? reinterpret_cast<const GemmRowSeg*>(L->p2p_tab + P2P_SEGS_BYTES + P2P_PRE_BYTES + p2p_fptr_bytes(D)) +
+                     (size_t)ch * moe_layer::P2P_MAXS
+               : nullptr,
+            fz ? fuse_nrseg[ch] : 0,
+            fz ? reinterpret_cast<uint32_t**>(L->p2p_tab + P2P_SEGS_BYTES + P2P_PRE_BYTES) + cslot * D : nullptr,
+            fz ? D : 0, epoch);
         if (err) { set_error(std::string("ComputeMoE: ") + cudaGetErrorString((cudaError_t)err)); return MOE_ERR_CUDA; }
         a = b;
       }
       // LocalReduce: the chunk's partial per unique row, in place of its x row
       if (lr_ep) KERNEL_TRY(launch_lr_reduce(L->o, L->meta_recv, u0, u1, H, k, L->recvu, st));
+      if (p2p && fuse_comb[ch]) TR_TRY(L->tr->p2p_after_put(MOE_MAX_CHUNKS + ch, st));  // combine rows are out
       CUDA_TRY(cudaEventRecord(L->ev_gemm[ch], st));
       return MOE_OK;
     };

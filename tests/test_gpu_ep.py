@@ -317,14 +317,18 @@ def test_ep_stage_profiling_and_exposed_a2a():
 
 # ---------------------------------------------------------------- own put-kernel all2all (a2a_p2p)
 
+@pytest.mark.parametrize("fuse", ["1", "0"])
 @pytest.mark.parametrize("D,N,S,fp8,lr", [(2, 2, 1, False, False), (4, 3, 1, False, False), (8, 2, 1, False, False),
                                           (2, 1, 3, False, False), (4, 2, 1, True, False), (2, 2, 1, False, True),
                                           (4, 1, 1, True, True)])
-def test_p2p_put_all2all(D, N, S, fp8, lr):
+def test_p2p_put_all2all(D, N, S, fp8, lr, fuse, monkeypatch):
     """a2a_p2p: each rank's put kernel stores its rows straight into the peers'
     workspaces (here: the other ranks' workspaces on the same GPU) and raises
-    per-(chunk, source) flags; consumers wait on them.  y == the NCCL-path
-    layout's result: EP = 1 bit for bit (per-pair path) or the oracle's R16."""
+    per-(chunk, source) flags; consumers wait on them.  fuse = 1: the combine is
+    the DownGemm's own epilogue scattering rows into the home ranks' buffers
+    (flags raised by its last CTA).  y == the NCCL-path layout's result: EP = 1
+    bit for bit (per-pair path) or the oracle's R16."""
+    monkeypatch.setenv("EPSMOE_P2P_FUSE", fuse)
     E = 16
     inp = Inputs(E=E, k=4, H=256, F=256, S=1, Fs=128, T=919, seed=100 + D + N, grid=True)
     plan = make_plan(N * S, MOE_GEMM_GROUPED, token_slices=S)
