@@ -748,13 +748,15 @@ int env_int(const char* name, int dflt) {
 // (measured: Mixtral GateUp DRAM reads ~4x lower, layer -4.5%; DSv2 shapes and
 // the dense shared GEMMs are faster with blocks of 4).  EPSMOE_RASTER_GM
 // overrides.
-int raster_gm(int epi, int N, int K, double rows_hint) {
+int raster_gm(int epi, int N, int K, double rows_hint, int tile_m) {
   static int v = env_int("EPSMOE_RASTER_GM", 0);
   if (v > 0) return v;
   if (rows_hint > 0) {
     const double a_bytes = rows_hint * K * 2.0;
     const double b_bytes = (epi == EPI_SWIGLU ? 2.0 : 1.0) * N * K * 2.0;
     if (b_bytes > 4.0 * a_bytes && a_bytes <= 48e6) return 1 << 20;
+    // a group's rows overflow L2: blocks holding ~64 MB of A, B streamed once per block
+    if (a_bytes > 48e6) return std::max(4, std::min(64, (int)(64e6 / ((double)tile_m * K * 2.0))));
   }
   return 4;
 }
@@ -827,7 +829,7 @@ int launch_epi(const GemmArgs& a, cudaStream_t stream) {
   p.m_single = a.m_single;
   p.b_group_rows = a.b_group_rows;
   p.b_base = a.b_base;
-  p.raster_gm = raster_gm(EPI, a.N, a.K, a.rows_hint);
+  p.raster_gm = raster_gm(EPI, a.N, a.K, a.rows_hint, BM * CG);
   p.ldo = a.ldo;
   p.out = a.out;
   p.bias = a.bias;

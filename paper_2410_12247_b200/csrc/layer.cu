@@ -791,6 +791,7 @@ moe_status_t moe_layer_forward(moe_layer_t* L, const void* x, int64_t T, void* y
     a.out = L->hs;
     a.ldo = L->SF;
     a.m_single = (int)T;
+    a.rows_hint = (double)T;
     a.tile_counter = (ss == L->s_side) ? L->tickets + 2 : L->tickets;
     int e = gemm_launch(a, ss);
     if (e) return e;
@@ -809,6 +810,7 @@ moe_status_t moe_layer_forward(moe_layer_t* L, const void* x, int64_t T, void* y
     b.out = L->s;
     b.ldo = H;
     b.m_single = (int)T;
+    b.rows_hint = (double)T;
     b.tile_counter = a.tile_counter;
     e = gemm_launch(b, ss);
     if (!e) ++L->last_launches;
@@ -1491,6 +1493,7 @@ moe_status_t moe_gemm_grouped(int32_t epi, const void* A, int64_t a_rows, const 
   a.G = groups;
   a.row_start = row_start;
   a.row_count = row_count;
+  a.rows_hint = (double)a_rows / groups;  // raster choice (the counts are on the device)
   int e = gemm_launch(a, (cudaStream_t)stream);
   if (e) { set_error(std::string("gemm: ") + cudaGetErrorString((cudaError_t)e)); return MOE_ERR_CUDA; }
   return MOE_OK;
