@@ -12,6 +12,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 
 #include "route.h"
 #include "rowops.cuh"
@@ -411,16 +412,25 @@ __global__ void pad_rows_kernel(const __nv_bfloat16* __restrict__ src, int rows,
 
 }  // namespace
 
+static int ranges_target() {
+  static const int v = [] {
+    const char* e = std::getenv("EPSMOE_RANGES");
+    return e ? std::max(64, std::atoi(e)) : 2048;
+  }();
+  return v;
+}
 int range_len(int64_t T) {
   int p = 1;
-  while (p < 32 && (T + p - 1) / p > 2048) p <<= 1;
+  while (p < 32 && (T + p - 1) / p > ranges_target()) p <<= 1;
   return p;
 }
 int num_ranges(int64_t T) {
   const int p = range_len(T);
   return (int)((T + p - 1) / p);
 }
-int max_ranges(int64_t T_max) { return (int)std::max<int64_t>(std::min<int64_t>(T_max, 2048), num_ranges(T_max)); }
+int max_ranges(int64_t T_max) {
+  return (int)std::max<int64_t>(std::min<int64_t>(T_max, ranges_target()), num_ranges(T_max));
+}
 
 int launch_gate_topk(const float* logits, int T, int E, int k, int norm_topk, float scale, int override_routing,
                      int route_groups, int route_topk_groups, int32_t* topk_idx, float* topk_w,
