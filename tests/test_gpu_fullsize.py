@@ -94,3 +94,70 @@ def test_full_size_parity(name):
         layer.close()
         del x, y, layer
         torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("name", ["dsv2", "mixtral"])
+def test_full_size_ep8_on_one_gpu(name):
+    """BASELINE's EP = 8 configuration at full size, the eight ranks as eight
+    layers on one B200 (in-process group), planner-chosen plan (Mixtral: one
+    expert per rank, so token slices), both all2all data planes: y == the EP = 1
+    layer's y, bit for bit, on every token."""
+    import threading
+
+    from paper_2410_12247_b200 import LocalGroup
+    c = CONFIGS[name]
+    E, k, H, F, S, Fs, T, norm = c["E"], c["k"], c["H"], c["F"], c["S"], c["Fs"], c["T"], c["norm_topk"]
+    D, E_loc = 8, c["E"] // 8
+    sH, sF = unif_scale(H), unif_scale(F)
+    w = dict(w_router=_gen((E, H), TID_WR, 0, MODE_UNIF, sH), w_gate=_gen((E, F, H), TID_WGATE, 0, MODE_UNIF, sH),
+             w_up=_gen((E, F, H), TID_WUP, 0, MODE_UNIF, sH), w_down=_gen((E, H, F), TID_WDOWN, 0, MODE_UNIF, sF))
+    SF = S * Fs
+    if SF:
+        w.update(ws_gate=_gen((SF, H), TID_WS_GATE, 0, MODE_UNIF, sH), ws_up=_gen((SF, H), TID_WS_UP, 0, MODE_UNIF, sH),
+                 ws_down=_gen((H, SF), TID_WS_DOWN, 0, MODE_UNIF, unif_scale(SF)))
+    x = _gen((T, H), TID_X, 0, MODE_UNIF, unif_scale(1))
+    ref_layer = MoELayer(E, k, H, F, w, S=S, Fs=Fs, max_tokens=T, norm_topk=norm)
+    y1 = ref_layer.forward(x)
+    torch.cuda.synchronize()
+    y1 = y1.cpu()
+    ref_layer.close()
+    del ref_layer
+    start = oracle.token_shards(T, D)
+    for p2p in (False, True):
+        group = LocalGroup(D)
+        layers = []
+        for r in range(D):
+            wr = {n: t for n, t in w.items() if not n.startswith("w_") or n == "w_router"}
+            for n in ("w_gate", "w_up", "w_down"):
+                wr[n] = w[n][r * E_loc:(r + 1) * E_loc]
+            layers.append(MoELayer(E, k, H, F, wr, S=S, Fs=Fs, ep=D, rank=r, max_tokens=int(start[r + 1] - start[r]),
+                                   norm_topk=norm, local_group=group, a2a_p2p=p2p))
+        ys, plans, errs = [None] * D, [None] * D, []
+
+        def worker(r):
+            try:
+                torch.cuda.set_device(0)
+                s = torch.cuda.Stream()
+                with torch.cuda.stream(s):
+                    d, b = layers[r].debug_buffers(int(start[r + 1] - start[r]))
+                    ys[r] = layers[r].forward(x[start[r]:start[r + 1]], stream=s, debug=d)
+                    s.synchronize()
+                    plans[r] = b["plan_used"].as_dict()
+            except Exception as e:  # pragma: no cover
+                errs.append(repr(e))
+
+        th = [threading.Thread(target=worker, args=(r,), daemon=True) for r in range(D)]
+        for t in th:
+            t.start()
+        for t in th:
+            t.join(timeout=300)
+        assert not errs, errs
+        assert all(p == plans[0] for p in plans)          # every rank ran the same plan
+        print(f"{name} EP8 p2p={p2p} plan: chunks={plans[0]['num_chunks']} slices={plans[0]['token_slices']} "
+              f"groups={plans[0]['group_begin']}")
+        y = torch.cat([v.cpu() for v in ys])
+        assert torch.equal(y, y1), f"{name} EP8 p2p={p2p} plan={plans[0]}"
+        for L in layers:
+            L.close()
+        del layers, ys
+        torch.cuda.empty_cache()
