@@ -721,34 +721,46 @@ moe_status_t moe_layer_stage_ms(const moe_layer_t* L, float* ms, int32_t* counts
   return MOE_OK;
 }
 
-moe_status_t moe_layer_forward(moe_layer_t* L, const void* x, int64_t T, void* y, const moe_plan_t* plan_in,
-                               void* stream_v, moe_debug_t* dbg) {
-  if (!L || (!x && T > 0) || (!y && T > 0) || T < 0) { set_error("null argument"); return MOE_ERR_INVALID; }
-  const moe_config_t& c = L->cfg;
-  if (T > c.max_tokens) { set_error("T_loc > max_tokens"); return MOE_ERR_CAPACITY; }
-  cudaStream_t st = (cudaStream_t)stream_v;
-  const int E = c.num_experts, k = c.top_k, H = c.hidden, D = c.ep, E_loc = L->E_loc;
-  L->last_launches = 0;
-  L->pev_used = 0;
-  L->marks.clear();
-  const int p_total = prof_rec(L, st);
-  const bool override_routing = dbg && dbg->override_routing;
-  if (override_routing && (!dbg->topk_idx || !dbg->topk_w)) { set_error("override needs topk_idx/topk_w"); return MOE_ERR_INVALID; }
-  int32_t* topk_idx = override_routing ? dbg->topk_idx : L->topk_idx;
-  float* topk_w = override_routing ? dbg->topk_w : L->topk_w;
+namespace {
 
+// One forward's context, shared by its phases (routing, EP = 1 compute + combine,
+// the EP > 1 pipeline, debug outputs).
+struct Fwd {
+  moe_layer* L;
+  const void* x;
+  int64_t T;
+  void* y;
+  const moe_plan_t* plan_in;
+  cudaStream_t st;
+  moe_debug_t* dbg;
   moe_plan_t plan;
-  if (plan_in) {
-    plan = *plan_in;
-    int pv = plan_normalise(c, &plan);
-    if (pv) { set_error("invalid plan"); return (moe_status_t)pv; }
-  }
-  // GEMM SM budget (A15, P:363-365, Table IV): a persistent GEMM owns every SM
-  // it runs on (~220 KB smem), so at ep > 1 it must leave SMs for the two
-  // communicators' kernels or the all2all could not overlap it at all.
-  const int default_ctas = (D > 1) ? L->num_sms - 2 * L->comm_ctas : L->num_sms;
-  int num_ctas = (plan_in && plan.sm_gemm > 0) ? std::min(plan.sm_gemm, L->num_sms) : default_ctas;
+  int num_ctas = 0;
+  int32_t* topk_idx = nullptr;
+  float* topk_w = nullptr;
+  bool override_routing = false;
+  // set by the routing phase
+  bool side = false, fp8 = false, gather = false, lr_ep = false;
+  int fuse = 0;
+};
 
+// Router (K1) + topKGating (K2) + histogram + split (K3), with the shared
+// experts launched alongside.
+moe_status_t fwd_routing(Fwd& F) {
+  moe_layer* L = F.L;
+  const moe_config_t& c = L->cfg;
+  const void* x = F.x;
+  const int64_t T = F.T;
+  void* y = F.y;
+  cudaStream_t st = F.st;
+  moe_debug_t* dbg = F.dbg;
+  moe_plan_t& plan = F.plan;
+  const moe_plan_t* plan_in = F.plan_in;
+  const int E = c.num_experts, k = c.top_k, H = c.hidden, D = c.ep, E_loc = L->E_loc;
+  const int num_ctas = F.num_ctas;
+  int32_t* topk_idx = F.topk_idx;
+  float* topk_w = F.topk_w;
+  const bool override_routing = F.override_routing;
+  (void)x; (void)y; (void)dbg; (void)plan_in; (void)E_loc; (void)override_routing; (void)topk_idx;
   // ---- Router (K1) + topKGating (K2) + histogram
   int p0 = prof_rec(L, st);
   if (T > 0 && !override_routing) {
@@ -853,504 +865,571 @@ moe_status_t moe_layer_forward(moe_layer_t* L, const void* x, int64_t T, void* y
     if (e) { set_error(std::string("shared experts: ") + cudaGetErrorString((cudaError_t)e)); return MOE_ERR_CUDA; }
   }
 
-  if (D == 1) {
-    // ---- EP = 1: no all2all; every chunk is local (C = 0 => PN = 1 is optimal)
-    if (!plan_in) plan_compute(c, L->cost, T, nullptr, &plan);
-    if (side) CUDA_TRY(cudaStreamWaitEvent(st, L->ev_shared, 0));
-    for (int ch = 0; T > 0 && ch < plan.num_chunks; ++ch) {
-      int g0 = plan.group_begin[ch], g1 = plan.group_begin[ch + 1];
-      // maximal runs of equal kind inside the chunk
-      int a = g0;
-      while (a < g1) {
-        int b = a + 1;
-        while (b < g1 && plan.expert_kind[b] == plan.expert_kind[a]) ++b;
-        int err = compute_moe(L, gather ? x : L->send, gather ? T : L->send_cap, L->seg_start, L->hist, a, b,
-                              plan.expert_kind[a], num_ctas, pick_cta_pair(plan, (double)T * k / E),
-                              (double)T * k / E, st, gather ? L->row_token : nullptr);
-        if (err) { set_error(std::string("ComputeMoE: ") + cudaGetErrorString((cudaError_t)err)); return MOE_ERR_CUDA; }
-        a = b;
-      }
+  F.side = side;
+  F.fp8 = fp8;
+  F.gather = gather;
+  F.lr_ep = lr_ep;
+  F.fuse = fuse;
+  return MOE_OK;
+}
+
+// EP = 1: ComputeMoE over the plan's chunks on local rows, then the combine.
+moe_status_t fwd_local(Fwd& F) {
+  moe_layer* L = F.L;
+  const moe_config_t& c = L->cfg;
+  const void* x = F.x;
+  const int64_t T = F.T;
+  void* y = F.y;
+  cudaStream_t st = F.st;
+  moe_debug_t* dbg = F.dbg;
+  moe_plan_t& plan = F.plan;
+  const moe_plan_t* plan_in = F.plan_in;
+  const int E = c.num_experts, k = c.top_k, H = c.hidden, D = c.ep, E_loc = L->E_loc;
+  const int num_ctas = F.num_ctas;
+  int32_t* topk_idx = F.topk_idx;
+  float* topk_w = F.topk_w;
+  const bool override_routing = F.override_routing;
+  (void)x; (void)y; (void)dbg; (void)plan_in; (void)E_loc; (void)override_routing; (void)topk_idx;
+  const bool side = F.side, fp8 = F.fp8, gather = F.gather, lr_ep = F.lr_ep;
+  const int fuse = F.fuse;
+  (void)side; (void)fp8; (void)gather; (void)lr_ep; (void)fuse;
+  // ---- EP = 1: no all2all; every chunk is local (C = 0 => PN = 1 is optimal)
+  if (!plan_in) plan_compute(c, L->cost, T, nullptr, &plan);
+  if (side) CUDA_TRY(cudaStreamWaitEvent(st, L->ev_shared, 0));
+  for (int ch = 0; T > 0 && ch < plan.num_chunks; ++ch) {
+    int g0 = plan.group_begin[ch], g1 = plan.group_begin[ch + 1];
+    // maximal runs of equal kind inside the chunk
+    int a = g0;
+    while (a < g1) {
+      int b = a + 1;
+      while (b < g1 && plan.expert_kind[b] == plan.expert_kind[a]) ++b;
+      int err = compute_moe(L, gather ? x : L->send, gather ? T : L->send_cap, L->seg_start, L->hist, a, b,
+                            plan.expert_kind[a], num_ctas, pick_cta_pair(plan, (double)T * k / E),
+                            (double)T * k / E, st, gather ? L->row_token : nullptr);
+      if (err) { set_error(std::string("ComputeMoE: ") + cudaGetErrorString((cudaError_t)err)); return MOE_ERR_CUDA; }
+      a = b;
     }
-    int c0 = prof_rec(L, st);
-    if (fuse == 2) {
-      // shared DownGemm in token pieces; piece p's combine (HBM-bound) runs on
-      // s_side next to piece p+1's DownGemm (compute-bound) on the other SMs' slack
-      const int P = (T >= 8192) ? moe_layer::COMB_PIECES : 1;
-      for (int pc = 0; pc < P; ++pc) {
-        const int64_t t0 = T * pc / P, t1 = T * (pc + 1) / P;
-        if (t1 == t0) continue;
-        GemmArgs b = base_args(EPI_BF16, num_ctas);
-        b.A = static_cast<const uint16_t*>(L->hs) + t0 * L->SF;
-        b.a_rows = t1 - t0;
-        b.B0 = L->w.ws_down;
-        b.b_rows = H;
-        b.K = L->SF;
-        b.N = H;
-        b.out = static_cast<uint16_t*>(L->s) + t0 * H;
-        b.ldo = H;
-        b.m_single = (int)(t1 - t0);
-        b.tile_counter = L->tickets;
-        int e = gemm_launch(b, st);
-        if (e) { set_error(std::string("shared DownGemm: ") + cudaGetErrorString((cudaError_t)e)); return MOE_ERR_CUDA; }
-        ++L->last_launches;
-        CUDA_TRY(cudaEventRecord(L->ev_piece[pc], st));
-        CUDA_TRY(cudaStreamWaitEvent(L->s_side, L->ev_piece[pc], 0));
-        KERNEL_TRY(launch_combine(L->o, static_cast<const uint16_t*>(L->s) + t0 * H, (int)(t1 - t0), H, k, L->pos + t0 * k, topk_w + t0 * k,
-                                  reinterpret_cast<uint16_t*>(y) + t0 * H, L->s_side));
-      }
-      CUDA_TRY(cudaEventRecord(L->ev_shared, L->s_side));
-      CUDA_TRY(cudaStreamWaitEvent(st, L->ev_shared, 0));
-    } else if (fuse == 1) {
-      // shared DownGemm + K7 in one kernel: y = bf16(fmaf_j(w_j, o[pos[t][j]], fp32(bf16(hs W_sdown^T))))
-      GemmArgs b = base_args(EPI_COMBINE, num_ctas);
-      b.A = L->hs;
-      b.a_rows = T;
+  }
+  int c0 = prof_rec(L, st);
+  if (fuse == 2) {
+    // shared DownGemm in token pieces; piece p's combine (HBM-bound) runs on
+    // s_side next to piece p+1's DownGemm (compute-bound) on the other SMs' slack
+    const int P = (T >= 8192) ? moe_layer::COMB_PIECES : 1;
+    for (int pc = 0; pc < P; ++pc) {
+      const int64_t t0 = T * pc / P, t1 = T * (pc + 1) / P;
+      if (t1 == t0) continue;
+      GemmArgs b = base_args(EPI_BF16, num_ctas);
+      b.A = static_cast<const uint16_t*>(L->hs) + t0 * L->SF;
+      b.a_rows = t1 - t0;
       b.B0 = L->w.ws_down;
       b.b_rows = H;
       b.K = L->SF;
       b.N = H;
-      b.out = y;
+      b.out = static_cast<uint16_t*>(L->s) + t0 * H;
       b.ldo = H;
-      b.m_single = (int)T;
+      b.m_single = (int)(t1 - t0);
       b.tile_counter = L->tickets;
-      b.comb_o = L->o;
-      b.comb_pos = L->pos;
-      b.comb_w = topk_w;
-      b.comb_k = k;
       int e = gemm_launch(b, st);
-      if (e) { set_error(std::string("shared DownGemm + combine: ") + cudaGetErrorString((cudaError_t)e)); return MOE_ERR_CUDA; }
+      if (e) { set_error(std::string("shared DownGemm: ") + cudaGetErrorString((cudaError_t)e)); return MOE_ERR_CUDA; }
       ++L->last_launches;
-    } else if (c.local_reduce) {
-      // R16 at ep == 1: groups = chunks; LocalReduce partials + home sum in one pass
-      LrChunks chs;
-      chs.n = plan.num_chunks;
-      for (int i = 0; i <= plan.num_chunks; ++i) chs.begin[i] = plan.group_begin[i];
-      KERNEL_TRY(launch_lr_combine_local(L->o, L->SF ? L->s : nullptr, (int)T, H, k, topk_idx, L->pos, topk_w, E,
-                                         chs, y, st));
-    } else {
-      KERNEL_TRY(launch_combine(L->o, L->SF ? L->s : nullptr, (int)T, H, k, L->pos, topk_w, y, st));
+      CUDA_TRY(cudaEventRecord(L->ev_piece[pc], st));
+      CUDA_TRY(cudaStreamWaitEvent(L->s_side, L->ev_piece[pc], 0));
+      KERNEL_TRY(launch_combine(L->o, static_cast<const uint16_t*>(L->s) + t0 * H, (int)(t1 - t0), H, k, L->pos + t0 * k, topk_w + t0 * k,
+                                reinterpret_cast<uint16_t*>(y) + t0 * H, L->s_side));
     }
-    prof_mark(L, MOE_STAGE_COMBINE, c0, prof_rec(L, st));
+    CUDA_TRY(cudaEventRecord(L->ev_shared, L->s_side));
+    CUDA_TRY(cudaStreamWaitEvent(st, L->ev_shared, 0));
+  } else if (fuse == 1) {
+    // shared DownGemm + K7 in one kernel: y = bf16(fmaf_j(w_j, o[pos[t][j]], fp32(bf16(hs W_sdown^T))))
+    GemmArgs b = base_args(EPI_COMBINE, num_ctas);
+    b.A = L->hs;
+    b.a_rows = T;
+    b.B0 = L->w.ws_down;
+    b.b_rows = H;
+    b.K = L->SF;
+    b.N = H;
+    b.out = y;
+    b.ldo = H;
+    b.m_single = (int)T;
+    b.tile_counter = L->tickets;
+    b.comb_o = L->o;
+    b.comb_pos = L->pos;
+    b.comb_w = topk_w;
+    b.comb_k = k;
+    int e = gemm_launch(b, st);
+    if (e) { set_error(std::string("shared DownGemm + combine: ") + cudaGetErrorString((cudaError_t)e)); return MOE_ERR_CUDA; }
+    ++L->last_launches;
+  } else if (c.local_reduce) {
+    // R16 at ep == 1: groups = chunks; LocalReduce partials + home sum in one pass
+    LrChunks chs;
+    chs.n = plan.num_chunks;
+    for (int i = 0; i <= plan.num_chunks; ++i) chs.begin[i] = plan.group_begin[i];
+    KERNEL_TRY(launch_lr_combine_local(L->o, L->SF ? L->s : nullptr, (int)T, H, k, topk_idx, L->pos, topk_w, E,
+                                       chs, y, st));
   } else {
-    // ---- EP > 1: count exchange (C3), plan, chunked dispatch / compute / combine
-    TR_TRY(L->tr->allgather_i32(L->hist, L->ghist, E, st));
-    CUDA_TRY(cudaMemcpyAsync(L->ghist_host, L->ghist, sizeof(int32_t) * D * E, cudaMemcpyDeviceToHost, st));
+    KERNEL_TRY(launch_combine(L->o, L->SF ? L->s : nullptr, (int)T, H, k, L->pos, topk_w, y, st));
+  }
+  prof_mark(L, MOE_STAGE_COMBINE, c0, prof_rec(L, st));
+  return MOE_OK;
+}
+
+// EP > 1: count exchange (C3), plan, layouts, and Algorithm 1's chunked
+// dispatch / ComputeMoE / combine over the transport or the put kernels.
+moe_status_t fwd_ep(Fwd& F) {
+  moe_layer* L = F.L;
+  const moe_config_t& c = L->cfg;
+  const void* x = F.x;
+  const int64_t T = F.T;
+  void* y = F.y;
+  cudaStream_t st = F.st;
+  moe_debug_t* dbg = F.dbg;
+  moe_plan_t& plan = F.plan;
+  const moe_plan_t* plan_in = F.plan_in;
+  const int E = c.num_experts, k = c.top_k, H = c.hidden, D = c.ep, E_loc = L->E_loc;
+  const int num_ctas = F.num_ctas;
+  int32_t* topk_idx = F.topk_idx;
+  float* topk_w = F.topk_w;
+  const bool override_routing = F.override_routing;
+  (void)x; (void)y; (void)dbg; (void)plan_in; (void)E_loc; (void)override_routing; (void)topk_idx;
+  const bool side = F.side, fp8 = F.fp8, gather = F.gather, lr_ep = F.lr_ep;
+  const int fuse = F.fuse;
+  (void)side; (void)fp8; (void)gather; (void)lr_ep; (void)fuse;
+  // ---- EP > 1: count exchange (C3), plan, chunked dispatch / compute / combine
+  TR_TRY(L->tr->allgather_i32(L->hist, L->ghist, E, st));
+  CUDA_TRY(cudaMemcpyAsync(L->ghist_host, L->ghist, sizeof(int32_t) * D * E, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaEventRecord(L->ev_hist, st));
+  CUDA_TRY(cudaEventSynchronize(L->ev_hist));
+  const int32_t* gh = L->ghist_host;
+  if (!plan_in) {
+    int64_t m = 0;
+    for (int i = 0; i < D * E; ++i) m += gh[i];
+    plan_compute(c, L->cost, m / k, gh, &plan);
+  }
+  const int me = c.rank;
+  // send offsets (local, expert-major) and recv layout [e_l][src] (R6)
+  std::vector<int64_t> send_off(E + 1, 0);
+  std::vector<int64_t> recv_off((size_t)E_loc * D + 1, 0);
+  exchange_layout(c, gh, send_off.data(), recv_off.data());
+  if (recv_off.back() > L->recv_cap) { set_error("recv rows exceed capacity"); return MOE_ERR_CAPACITY; }
+  // Token-sliced chunks (R8 extension, S > 1): chunk c = (expert group c / S,
+  // source-token slice c % S); the (expert, slice) counts of every rank take
+  // one more exchange.  Send rows stay (e, t), so (e, s) is contiguous; recv
+  // rows become (e_l, s, src, t), so each expert's rows of a chunk are.  Every
+  // row still meets the same weights and returns to the same send row, so
+  // slicing changes no bit of y.
+  const int S = plan.token_slices;
+  const int NG = plan.num_chunks / S;
+  const int32_t* hsl = gh;  // [D][E * S]
+  if (S > 1) {
+    KERNEL_TRY(launch_slice_hist(topk_idx, (int)T, k, E, S, L->slice_hist, st));
+    TR_TRY(L->tr->allgather_i32(L->slice_hist, L->gslice, E * S, st));
+    CUDA_TRY(cudaMemcpyAsync(L->gslice_host, L->gslice, sizeof(int32_t) * D * E * S, cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaEventRecord(L->ev_hist, st));
     CUDA_TRY(cudaEventSynchronize(L->ev_hist));
-    const int32_t* gh = L->ghist_host;
-    if (!plan_in) {
-      int64_t m = 0;
-      for (int i = 0; i < D * E; ++i) m += gh[i];
-      plan_compute(c, L->cost, m / k, gh, &plan);
+    hsl = L->gslice_host;
+  }
+  auto cnt = [&](int src, int ex, int sl) -> int64_t { return hsl[((int64_t)src * E + ex) * S + sl]; };
+  std::vector<int64_t> send_pos((size_t)E * S);
+  for (int ex = 0; ex < E; ++ex) {
+    int64_t p0 = send_off[ex];
+    for (int sl = 0; sl < S; ++sl) {
+      send_pos[(size_t)ex * S + sl] = p0;
+      p0 += cnt(me, ex, sl);
     }
-    const int me = c.rank;
-    // send offsets (local, expert-major) and recv layout [e_l][src] (R6)
-    std::vector<int64_t> send_off(E + 1, 0);
-    std::vector<int64_t> recv_off((size_t)E_loc * D + 1, 0);
-    exchange_layout(c, gh, send_off.data(), recv_off.data());
-    if (recv_off.back() > L->recv_cap) { set_error("recv rows exceed capacity"); return MOE_ERR_CAPACITY; }
-    // Token-sliced chunks (R8 extension, S > 1): chunk c = (expert group c / S,
-    // source-token slice c % S); the (expert, slice) counts of every rank take
-    // one more exchange.  Send rows stay (e, t), so (e, s) is contiguous; recv
-    // rows become (e_l, s, src, t), so each expert's rows of a chunk are.  Every
-    // row still meets the same weights and returns to the same send row, so
-    // slicing changes no bit of y.
-    const int S = plan.token_slices;
-    const int NG = plan.num_chunks / S;
-    const int32_t* hsl = gh;  // [D][E * S]
-    if (S > 1) {
-      KERNEL_TRY(launch_slice_hist(topk_idx, (int)T, k, E, S, L->slice_hist, st));
-      TR_TRY(L->tr->allgather_i32(L->slice_hist, L->gslice, E * S, st));
-      CUDA_TRY(cudaMemcpyAsync(L->gslice_host, L->gslice, sizeof(int32_t) * D * E * S, cudaMemcpyDeviceToHost, st));
-      CUDA_TRY(cudaEventRecord(L->ev_hist, st));
-      CUDA_TRY(cudaEventSynchronize(L->ev_hist));
-      hsl = L->gslice_host;
+  }
+  std::vector<int64_t> recv_pos((size_t)E_loc * S * D + 1, 0);  // (e_l, s, src)
+  for (int el = 0, i = 0; el < E_loc; ++el)
+    for (int sl = 0; sl < S; ++sl)
+      for (int src = 0; src < D; ++src, ++i) recv_pos[i + 1] = recv_pos[i] + cnt(src, me * E_loc + el, sl);
+  auto rpos = [&](int el, int sl, int src) -> int64_t { return recv_pos[((size_t)el * S + sl) * D + src]; };
+  // per-chunk GEMM row tables: chunk c's experts at [c * E_loc + e_l]
+  int32_t* tstart = L->tables_host;
+  int32_t* tcount = L->tables_host + moe_layer::TBL;
+  for (int ch = 0; ch < plan.num_chunks; ++ch) {
+    const int grp = ch / S, sl = ch % S;
+    for (int el = plan.group_begin[grp]; el < plan.group_begin[grp + 1]; ++el) {
+      tstart[ch * E_loc + el] = (int32_t)rpos(el, sl, 0);
+      tcount[ch * E_loc + el] = (int32_t)(rpos(el, sl, D - 1) + cnt(D - 1, me * E_loc + el, sl) - rpos(el, sl, 0));
     }
-    auto cnt = [&](int src, int ex, int sl) -> int64_t { return hsl[((int64_t)src * E + ex) * S + sl]; };
-    std::vector<int64_t> send_pos((size_t)E * S);
-    for (int ex = 0; ex < E; ++ex) {
-      int64_t p0 = send_off[ex];
-      for (int sl = 0; sl < S; ++sl) {
-        send_pos[(size_t)ex * S + sl] = p0;
-        p0 += cnt(me, ex, sl);
+  }
+  const size_t tbytes = sizeof(int32_t) * (size_t)plan.num_chunks * E_loc;
+  CUDA_TRY(cudaMemcpyAsync(L->recv_start_d, tstart, tbytes, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaMemcpyAsync(L->recv_count_d, tcount, tbytes, cudaMemcpyHostToDevice, st));
+  (void)NG;
+  // ---- local_reduce (R16): the dedup layout needs the plan's chunks, and the
+  // unique-row counts per (chunk, peer) need a second (G-int) exchange
+  const int G = plan.num_chunks * D;
+  std::vector<int64_t> usend_off(G + 1, 0);                     // my send rows of group g = c*D + peer
+  std::vector<int64_t> urecv((size_t)plan.num_chunks * D + 1, 0);  // first unique recv row of (c, src)
+  const int32_t* ug = L->ughist_host;                           // [D][G]
+  if (lr_ep) {
+    int q0 = prof_rec(L, st);
+    LrChunks chs;
+    chs.n = plan.num_chunks;
+    for (int i = 0; i <= plan.num_chunks; ++i) chs.begin[i] = plan.group_begin[i];
+    KERNEL_TRY(launch_lr_count(topk_idx, (int)T, k, E_loc, D, chs, L->range_hist, st));
+    KERNEL_TRY(launch_range_scan(L->range_hist, (int)T, G, L->range_off, L->u_hist, L->u_start, st));
+    KERNEL_TRY(launch_lr_permute(x, (int)T, H, k, topk_idx, topk_w, L->pos, L->seg_start, E_loc, D, chs,
+                                 L->range_off, L->u_start, fp8 ? nullptr : L->send, fp8 ? L->sendq : nullptr,
+                                 L->qpitch, L->posg, L->meta_send, st));
+    prof_mark(L, MOE_STAGE_ROUTE, q0, prof_rec(L, st));
+    TR_TRY(L->tr->allgather_i32(L->u_hist, L->ughist, G, st));
+    CUDA_TRY(cudaMemcpyAsync(L->ughist_host, L->ughist, sizeof(int32_t) * D * G, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaEventRecord(L->ev_hist, st));
+    CUDA_TRY(cudaEventSynchronize(L->ev_hist));
+    for (int g = 0; g < G; ++g) usend_off[g + 1] = usend_off[g] + ug[(size_t)me * G + g];
+    int64_t row = 0;
+    for (int ch = 0; ch < plan.num_chunks; ++ch)
+      for (int src = 0; src < D; ++src) {
+        urecv[(size_t)ch * D + src] = row;
+        row += ug[(size_t)src * G + ch * D + me];
       }
-    }
-    std::vector<int64_t> recv_pos((size_t)E_loc * S * D + 1, 0);  // (e_l, s, src)
-    for (int el = 0, i = 0; el < E_loc; ++el)
-      for (int sl = 0; sl < S; ++sl)
-        for (int src = 0; src < D; ++src, ++i) recv_pos[i + 1] = recv_pos[i] + cnt(src, me * E_loc + el, sl);
-    auto rpos = [&](int el, int sl, int src) -> int64_t { return recv_pos[((size_t)el * S + sl) * D + src]; };
-    // per-chunk GEMM row tables: chunk c's experts at [c * E_loc + e_l]
-    int32_t* tstart = L->tables_host;
-    int32_t* tcount = L->tables_host + moe_layer::TBL;
-    for (int ch = 0; ch < plan.num_chunks; ++ch) {
-      const int grp = ch / S, sl = ch % S;
-      for (int el = plan.group_begin[grp]; el < plan.group_begin[grp + 1]; ++el) {
-        tstart[ch * E_loc + el] = (int32_t)rpos(el, sl, 0);
-        tcount[ch * E_loc + el] = (int32_t)(rpos(el, sl, D - 1) + cnt(D - 1, me * E_loc + el, sl) - rpos(el, sl, 0));
+    urecv[G] = row;
+    if (row > L->recv_cap) { set_error("unique recv rows exceed capacity"); return MOE_ERR_CAPACITY; }
+    int32_t* tb = L->tables_host + 2 * moe_layer::TBL;  // [E_loc*D+1] recv_off, then [G+1] urecv
+    for (int i = 0; i <= E_loc * D; ++i) tb[i] = (int32_t)recv_off[i];
+    for (int i = 0; i <= G; ++i) tb[MOE_MAX_EXPERTS + 4 + i] = (int32_t)urecv[i];
+    CUDA_TRY(cudaMemcpyAsync(L->lr_recv_off_d, tb, sizeof(int32_t) * (E_loc * D + 1), cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemcpyAsync(L->lr_usrc_d, tb + MOE_MAX_EXPERTS + 4, sizeof(int32_t) * (G + 1),
+                             cudaMemcpyHostToDevice, st));
+  }
+  // ---- a2a_p2p: this forward's put-kernel segments (rows of each chunk, per
+  // peer, at the peer's own offsets) and consumer flag addresses
+  const bool p2p = c.a2a_p2p != 0;
+  uint32_t epoch = 0;
+  int p2p_nseg[2][MOE_MAX_CHUNKS] = {};
+  int64_t p2p_total[2][MOE_MAX_CHUNKS] = {};
+  // fused combine: the chunk's DownGemm scatters its rows into the home ranks'
+  // combine buffers (one GEMM launch per chunk: its experts share one kind)
+  bool fuse_comb[MOE_MAX_CHUNKS] = {};
+  int fuse_nrseg[MOE_MAX_CHUNKS] = {};
+  if (p2p) {
+    if (L->peer_ws.empty()) {  // first forward (collective): map the peers, learn their layouts
+      TR_TRY(L->tr->map_peers(L->ws_base, L->peer_ws));
+      const void* bufs[moe_layer::P2P_NBUF] = {L->recv, L->recvq, L->recvu, L->meta_recv, L->comb, L->p2p_flags};
+      int64_t mine[moe_layer::P2P_NBUF];
+      for (int b = 0; b < moe_layer::P2P_NBUF; ++b)
+        mine[b] = bufs[b] ? (int64_t)((const char*)bufs[b] - L->ws_base) : -1;
+      constexpr int W = 2 * moe_layer::P2P_NBUF;
+      int32_t* dev = nullptr;
+      CUDA_TRY(cudaMalloc(&dev, sizeof(int32_t) * W * (D + 1)));
+      CUDA_TRY(cudaMemcpy(dev, mine, sizeof(mine), cudaMemcpyHostToDevice));
+      int ge = L->tr->allgather_i32(dev, dev + W, W, st);
+      L->peer_off.assign((size_t)D * moe_layer::P2P_NBUF, -1);
+      if (!ge) {
+        CUDA_TRY(cudaStreamSynchronize(st));
+        CUDA_TRY(cudaMemcpy(L->peer_off.data(), dev + W, sizeof(int64_t) * D * moe_layer::P2P_NBUF,
+                            cudaMemcpyDeviceToHost));
       }
+      cudaFree(dev);
+      if (ge) return (moe_status_t)ge;
     }
-    const size_t tbytes = sizeof(int32_t) * (size_t)plan.num_chunks * E_loc;
-    CUDA_TRY(cudaMemcpyAsync(L->recv_start_d, tstart, tbytes, cudaMemcpyHostToDevice, st));
-    CUDA_TRY(cudaMemcpyAsync(L->recv_count_d, tcount, tbytes, cudaMemcpyHostToDevice, st));
-    (void)NG;
-    // ---- local_reduce (R16): the dedup layout needs the plan's chunks, and the
-    // unique-row counts per (chunk, peer) need a second (G-int) exchange
-    const int G = plan.num_chunks * D;
-    std::vector<int64_t> usend_off(G + 1, 0);                     // my send rows of group g = c*D + peer
-    std::vector<int64_t> urecv((size_t)plan.num_chunks * D + 1, 0);  // first unique recv row of (c, src)
-    const int32_t* ug = L->ughist_host;                           // [D][G]
-    if (lr_ep) {
-      int q0 = prof_rec(L, st);
-      LrChunks chs;
-      chs.n = plan.num_chunks;
-      for (int i = 0; i <= plan.num_chunks; ++i) chs.begin[i] = plan.group_begin[i];
-      KERNEL_TRY(launch_lr_count(topk_idx, (int)T, k, E_loc, D, chs, L->range_hist, st));
-      KERNEL_TRY(launch_range_scan(L->range_hist, (int)T, G, L->range_off, L->u_hist, L->u_start, st));
-      KERNEL_TRY(launch_lr_permute(x, (int)T, H, k, topk_idx, topk_w, L->pos, L->seg_start, E_loc, D, chs,
-                                   L->range_off, L->u_start, fp8 ? nullptr : L->send, fp8 ? L->sendq : nullptr,
-                                   L->qpitch, L->posg, L->meta_send, st));
-      prof_mark(L, MOE_STAGE_ROUTE, q0, prof_rec(L, st));
-      TR_TRY(L->tr->allgather_i32(L->u_hist, L->ughist, G, st));
-      CUDA_TRY(cudaMemcpyAsync(L->ughist_host, L->ughist, sizeof(int32_t) * D * G, cudaMemcpyDeviceToHost, st));
-      CUDA_TRY(cudaEventRecord(L->ev_hist, st));
-      CUDA_TRY(cudaEventSynchronize(L->ev_hist));
-      for (int g = 0; g < G; ++g) usend_off[g + 1] = usend_off[g] + ug[(size_t)me * G + g];
+    epoch = ++L->p2p_epoch;
+    // address, in peer d's workspace, of byte `off` of its buffer b
+    auto peer_buf = [&](int d, int b, int64_t off) -> char* {
+      return L->peer_ws[d] + L->peer_off[(size_t)d * moe_layer::P2P_NBUF + b] + off;
+    };
+    // every rank's layout, from the same global counts
+    const size_t RP = (size_t)E_loc * S * D;
+    std::vector<int64_t> rpos_all((size_t)D * RP), spos_all((size_t)D * E * S);
+    for (int d = 0; d < D; ++d) {
       int64_t row = 0;
-      for (int ch = 0; ch < plan.num_chunks; ++ch)
-        for (int src = 0; src < D; ++src) {
-          urecv[(size_t)ch * D + src] = row;
-          row += ug[(size_t)src * G + ch * D + me];
+      for (int el = 0; el < E_loc; ++el)
+        for (int sl = 0; sl < S; ++sl)
+          for (int src = 0; src < D; ++src) {
+            rpos_all[d * RP + ((size_t)el * S + sl) * D + src] = row;
+            row += cnt(src, d * E_loc + el, sl);
+          }
+      row = 0;
+      for (int ex = 0; ex < E; ++ex)
+        for (int sl = 0; sl < S; ++sl) {
+          spos_all[(size_t)d * E * S + (size_t)ex * S + sl] = row;
+          row += cnt(d, ex, sl);
         }
-      urecv[G] = row;
-      if (row > L->recv_cap) { set_error("unique recv rows exceed capacity"); return MOE_ERR_CAPACITY; }
-      int32_t* tb = L->tables_host + 2 * moe_layer::TBL;  // [E_loc*D+1] recv_off, then [G+1] urecv
-      for (int i = 0; i <= E_loc * D; ++i) tb[i] = (int32_t)recv_off[i];
-      for (int i = 0; i <= G; ++i) tb[MOE_MAX_EXPERTS + 4 + i] = (int32_t)urecv[i];
-      CUDA_TRY(cudaMemcpyAsync(L->lr_recv_off_d, tb, sizeof(int32_t) * (E_loc * D + 1), cudaMemcpyHostToDevice, st));
-      CUDA_TRY(cudaMemcpyAsync(L->lr_usrc_d, tb + MOE_MAX_EXPERTS + 4, sizeof(int32_t) * (G + 1),
-                               cudaMemcpyHostToDevice, st));
     }
-    // ---- a2a_p2p: this forward's put-kernel segments (rows of each chunk, per
-    // peer, at the peer's own offsets) and consumer flag addresses
-    const bool p2p = c.a2a_p2p != 0;
-    uint32_t epoch = 0;
-    int p2p_nseg[2][MOE_MAX_CHUNKS] = {};
-    int64_t p2p_total[2][MOE_MAX_CHUNKS] = {};
-    // fused combine: the chunk's DownGemm scatters its rows into the home ranks'
-    // combine buffers (one GEMM launch per chunk: its experts share one kind)
-    bool fuse_comb[MOE_MAX_CHUNKS] = {};
-    int fuse_nrseg[MOE_MAX_CHUNKS] = {};
-    if (p2p) {
-      if (L->peer_ws.empty()) {  // first forward (collective): map the peers, learn their layouts
-        TR_TRY(L->tr->map_peers(L->ws_base, L->peer_ws));
-        const void* bufs[moe_layer::P2P_NBUF] = {L->recv, L->recvq, L->recvu, L->meta_recv, L->comb, L->p2p_flags};
-        int64_t mine[moe_layer::P2P_NBUF];
-        for (int b = 0; b < moe_layer::P2P_NBUF; ++b)
-          mine[b] = bufs[b] ? (int64_t)((const char*)bufs[b] - L->ws_base) : -1;
-        constexpr int W = 2 * moe_layer::P2P_NBUF;
-        int32_t* dev = nullptr;
-        CUDA_TRY(cudaMalloc(&dev, sizeof(int32_t) * W * (D + 1)));
-        CUDA_TRY(cudaMemcpy(dev, mine, sizeof(mine), cudaMemcpyHostToDevice));
-        int ge = L->tr->allgather_i32(dev, dev + W, W, st);
-        L->peer_off.assign((size_t)D * moe_layer::P2P_NBUF, -1);
-        if (!ge) {
-          CUDA_TRY(cudaStreamSynchronize(st));
-          CUDA_TRY(cudaMemcpy(L->peer_off.data(), dev + W, sizeof(int64_t) * D * moe_layer::P2P_NBUF,
-                              cudaMemcpyDeviceToHost));
-        }
-        cudaFree(dev);
-        if (ge) return (moe_status_t)ge;
-      }
-      epoch = ++L->p2p_epoch;
-      // address, in peer d's workspace, of byte `off` of its buffer b
-      auto peer_buf = [&](int d, int b, int64_t off) -> char* {
-        return L->peer_ws[d] + L->peer_off[(size_t)d * moe_layer::P2P_NBUF + b] + off;
-      };
-      // every rank's layout, from the same global counts
-      const size_t RP = (size_t)E_loc * S * D;
-      std::vector<int64_t> rpos_all((size_t)D * RP), spos_all((size_t)D * E * S);
+    std::vector<int64_t> urecv_all, usend_all;
+    if (lr_ep) {
+      urecv_all.assign((size_t)D * (G + 1), 0);
+      usend_all.assign((size_t)D * (G + 1), 0);
       for (int d = 0; d < D; ++d) {
         int64_t row = 0;
-        for (int el = 0; el < E_loc; ++el)
-          for (int sl = 0; sl < S; ++sl)
-            for (int src = 0; src < D; ++src) {
-              rpos_all[d * RP + ((size_t)el * S + sl) * D + src] = row;
-              row += cnt(src, d * E_loc + el, sl);
-            }
-        row = 0;
-        for (int ex = 0; ex < E; ++ex)
-          for (int sl = 0; sl < S; ++sl) {
-            spos_all[(size_t)d * E * S + (size_t)ex * S + sl] = row;
-            row += cnt(d, ex, sl);
+        for (int ch = 0; ch < plan.num_chunks; ++ch)
+          for (int src = 0; src < D; ++src) {
+            urecv_all[(size_t)d * (G + 1) + ch * D + src] = row;
+            row += ug[(size_t)src * G + ch * D + d];
           }
+        for (int g = 0; g < G; ++g)
+          usend_all[(size_t)d * (G + 1) + g + 1] = usend_all[(size_t)d * (G + 1) + g] + ug[(size_t)d * G + g];
       }
-      std::vector<int64_t> urecv_all, usend_all;
-      if (lr_ep) {
-        urecv_all.assign((size_t)D * (G + 1), 0);
-        usend_all.assign((size_t)D * (G + 1), 0);
-        for (int d = 0; d < D; ++d) {
-          int64_t row = 0;
-          for (int ch = 0; ch < plan.num_chunks; ++ch)
-            for (int src = 0; src < D; ++src) {
-              urecv_all[(size_t)d * (G + 1) + ch * D + src] = row;
-              row += ug[(size_t)src * G + ch * D + d];
-            }
-          for (int g = 0; g < G; ++g)
-            usend_all[(size_t)d * (G + 1) + g + 1] = usend_all[(size_t)d * (G + 1) + g] + ug[(size_t)d * G + g];
-        }
-      }
-      auto* hsegs = reinterpret_cast<epsmoe::P2PSeg*>(L->p2p_host);
-      auto* hpre = reinterpret_cast<int64_t*>(L->p2p_host + P2P_SEGS_BYTES);
-      auto* hfp = reinterpret_cast<uint32_t**>(L->p2p_host + P2P_SEGS_BYTES + P2P_PRE_BYTES);
-      const size_t rowb = (size_t)H * 2;
-      const size_t drowb = fp8 ? (size_t)L->qpitch : rowb;
-      const size_t metab = (size_t)lr_meta_pitch(k) * sizeof(int32_t);
-      char* ds = fp8 ? (char*)L->sendq : (char*)L->send;
-      const int dr_id = fp8 ? moe_layer::P2P_RECVQ : (lr_ep ? moe_layer::P2P_RECVU : moe_layer::P2P_RECV);
-      for (int dir = 0; dir < 2; ++dir)
-        for (int ch = 0; ch < plan.num_chunks; ++ch) {
-          const size_t slot = (size_t)dir * MOE_MAX_CHUNKS + ch;
-          epsmoe::P2PSeg* sg = hsegs + slot * moe_layer::P2P_MAXS;
-          int64_t* pr = hpre + slot * (moe_layer::P2P_MAXS + 1);
-          int n = 0;
-          pr[0] = 0;
-          auto add = [&](const char* src, char* dst, int64_t bytes) {
-            if (bytes <= 0 || n >= moe_layer::P2P_MAXS) return;
-            sg[n].src = reinterpret_cast<const uint4*>(src);
-            sg[n].dst = reinterpret_cast<uint4*>(dst);
-            pr[n + 1] = pr[n] + bytes / 16;
-            ++n;
-          };
-          for (int d = 0; d < D; ++d)
-            hfp[slot * D + d] =
-                reinterpret_cast<uint32_t*>(peer_buf(d, moe_layer::P2P_FLAGS, (int64_t)(slot * D + me) * 4));
-          const int sl = ch % S, g0 = plan.group_begin[ch / S], g1 = plan.group_begin[ch / S + 1];
-          for (int peer = 0; peer < D; ++peer) {
-            if (lr_ep && dir == 0) {
-              const int64_t s0 = usend_off[ch * D + peer], ns = ug[(size_t)me * G + ch * D + peer];
-              const int64_t r0 = urecv_all[(size_t)peer * (G + 1) + ch * D + me];
-              add(ds + s0 * drowb, peer_buf(peer, dr_id, r0 * drowb), ns * (int64_t)drowb);
-              add((char*)L->meta_send + s0 * metab, peer_buf(peer, moe_layer::P2P_META, r0 * metab), ns * (int64_t)metab);
-            } else if (lr_ep) {
-              const int64_t r0 = urecv[(size_t)ch * D + peer], nb = ug[(size_t)peer * G + ch * D + me];
-              const int64_t s0 = usend_all[(size_t)peer * (G + 1) + ch * D + me];
-              add((char*)L->recvu + r0 * rowb, peer_buf(peer, moe_layer::P2P_COMB, s0 * rowb), nb * (int64_t)rowb);
-            } else {
-              for (int el = g0; el < g1; ++el) {
-                if (dir == 0) {
-                  const int ex = peer * E_loc + el;
-                  add(ds + send_pos[(size_t)ex * S + sl] * drowb,
-                      peer_buf(peer, dr_id, rpos_all[peer * RP + ((size_t)el * S + sl) * D + me] * drowb),
-                      cnt(me, ex, sl) * (int64_t)drowb);
-                } else {
-                  const int ex = me * E_loc + el;
-                  add((char*)L->o + rpos(el, sl, peer) * rowb,
-                      peer_buf(peer, moe_layer::P2P_COMB, spos_all[(size_t)peer * E * S + (size_t)ex * S + sl] * rowb),
-                      cnt(peer, ex, sl) * (int64_t)rowb);
-                }
+    }
+    auto* hsegs = reinterpret_cast<epsmoe::P2PSeg*>(L->p2p_host);
+    auto* hpre = reinterpret_cast<int64_t*>(L->p2p_host + P2P_SEGS_BYTES);
+    auto* hfp = reinterpret_cast<uint32_t**>(L->p2p_host + P2P_SEGS_BYTES + P2P_PRE_BYTES);
+    const size_t rowb = (size_t)H * 2;
+    const size_t drowb = fp8 ? (size_t)L->qpitch : rowb;
+    const size_t metab = (size_t)lr_meta_pitch(k) * sizeof(int32_t);
+    char* ds = fp8 ? (char*)L->sendq : (char*)L->send;
+    const int dr_id = fp8 ? moe_layer::P2P_RECVQ : (lr_ep ? moe_layer::P2P_RECVU : moe_layer::P2P_RECV);
+    for (int dir = 0; dir < 2; ++dir)
+      for (int ch = 0; ch < plan.num_chunks; ++ch) {
+        const size_t slot = (size_t)dir * MOE_MAX_CHUNKS + ch;
+        epsmoe::P2PSeg* sg = hsegs + slot * moe_layer::P2P_MAXS;
+        int64_t* pr = hpre + slot * (moe_layer::P2P_MAXS + 1);
+        int n = 0;
+        pr[0] = 0;
+        auto add = [&](const char* src, char* dst, int64_t bytes) {
+          if (bytes <= 0 || n >= moe_layer::P2P_MAXS) return;
+          sg[n].src = reinterpret_cast<const uint4*>(src);
+          sg[n].dst = reinterpret_cast<uint4*>(dst);
+          pr[n + 1] = pr[n] + bytes / 16;
+          ++n;
+        };
+        for (int d = 0; d < D; ++d)
+          hfp[slot * D + d] =
+              reinterpret_cast<uint32_t*>(peer_buf(d, moe_layer::P2P_FLAGS, (int64_t)(slot * D + me) * 4));
+        const int sl = ch % S, g0 = plan.group_begin[ch / S], g1 = plan.group_begin[ch / S + 1];
+        for (int peer = 0; peer < D; ++peer) {
+          if (lr_ep && dir == 0) {
+            const int64_t s0 = usend_off[ch * D + peer], ns = ug[(size_t)me * G + ch * D + peer];
+            const int64_t r0 = urecv_all[(size_t)peer * (G + 1) + ch * D + me];
+            add(ds + s0 * drowb, peer_buf(peer, dr_id, r0 * drowb), ns * (int64_t)drowb);
+            add((char*)L->meta_send + s0 * metab, peer_buf(peer, moe_layer::P2P_META, r0 * metab), ns * (int64_t)metab);
+          } else if (lr_ep) {
+            const int64_t r0 = urecv[(size_t)ch * D + peer], nb = ug[(size_t)peer * G + ch * D + me];
+            const int64_t s0 = usend_all[(size_t)peer * (G + 1) + ch * D + me];
+            add((char*)L->recvu + r0 * rowb, peer_buf(peer, moe_layer::P2P_COMB, s0 * rowb), nb * (int64_t)rowb);
+          } else {
+            for (int el = g0; el < g1; ++el) {
+              if (dir == 0) {
+                const int ex = peer * E_loc + el;
+                add(ds + send_pos[(size_t)ex * S + sl] * drowb,
+                    peer_buf(peer, dr_id, rpos_all[peer * RP + ((size_t)el * S + sl) * D + me] * drowb),
+                    cnt(me, ex, sl) * (int64_t)drowb);
+              } else {
+                const int ex = me * E_loc + el;
+                add((char*)L->o + rpos(el, sl, peer) * rowb,
+                    peer_buf(peer, moe_layer::P2P_COMB, spos_all[(size_t)peer * E * S + (size_t)ex * S + sl] * rowb),
+                    cnt(peer, ex, sl) * (int64_t)rowb);
               }
             }
           }
-          p2p_nseg[dir][ch] = n;
-          p2p_total[dir][ch] = pr[n];
-          if (dir == 1 && L->p2p_fuse && !lr_ep && !L->split_rem) {
-            bool one_kind = true;
-            for (int el = g0 + 1; el < g1; ++el) one_kind &= plan.expert_kind[el] == plan.expert_kind[g0];
-            if (one_kind) {
-              auto* rs = reinterpret_cast<epsmoe::GemmRowSeg*>(L->p2p_host + P2P_SEGS_BYTES + P2P_PRE_BYTES +
-                                                                 p2p_fptr_bytes(D)) +
-                         (size_t)ch * moe_layer::P2P_MAXS;
-              int nr = 0;
-              for (int el = g0; el < g1; ++el)  // GEMM rows (e_l, slice, src) ascending
-                for (int src = 0; src < D; ++src) {
-                  const int ex = me * E_loc + el;
-                  const int64_t rows = cnt(src, ex, sl);
-                  if (!rows || nr >= moe_layer::P2P_MAXS) continue;
-                  rs[nr].r0 = rpos(el, sl, src);
-                  rs[nr].n = rows;
-                  rs[nr].dst = peer_buf(src, moe_layer::P2P_COMB, spos_all[(size_t)src * E * S + (size_t)ex * S + sl] * rowb);
-                  ++nr;
-                }
-              fuse_comb[ch] = true;
-              fuse_nrseg[ch] = nr;
-            }
-          }
         }
-      CUDA_TRY(cudaMemcpyAsync(L->p2p_tab, L->p2p_host, p2p_table_bytes(D), cudaMemcpyHostToDevice, st));
-    }
-    auto p2p_put = [&](int dir, int ch, cudaStream_t ps) -> moe_status_t {
-      const size_t slot = (size_t)dir * MOE_MAX_CHUNKS + ch;
-      auto* dsegs = reinterpret_cast<epsmoe::P2PSeg*>(L->p2p_tab) + slot * moe_layer::P2P_MAXS;
-      auto* dpre = reinterpret_cast<int64_t*>(L->p2p_tab + P2P_SEGS_BYTES) + slot * (moe_layer::P2P_MAXS + 1);
-      auto* dfp = reinterpret_cast<uint32_t**>(L->p2p_tab + P2P_SEGS_BYTES + P2P_PRE_BYTES) + slot * D;
-      KERNEL_TRY(launch_p2p_put(dsegs, dpre, p2p_nseg[dir][ch], p2p_total[dir][ch], 2 * L->comm_ctas,
-                                L->p2p_done + slot, dfp, D, epoch, ps));
-      TR_TRY(L->tr->p2p_after_put((int)slot, ps));
-      return MOE_OK;
-    };
-    CUDA_TRY(cudaEventRecord(L->ev_ready, st));
-    CUDA_TRY(cudaStreamWaitEvent(L->s_disp, L->ev_ready, 0));
-    CUDA_TRY(cudaStreamWaitEvent(L->s_comb, L->ev_ready, 0));
-    const size_t row_bytes = (size_t)H * 2;
-    // dispatch payload: bf16 rows, or packed FP8 rows (NEXT-2) dequantised per chunk on arrival
-    char* dsend = fp8 ? (char*)L->sendq : (char*)L->send;
-    char* drecv = fp8 ? (char*)L->recvq : (char*)L->recv;
-    const size_t drow = fp8 ? (size_t)L->qpitch : row_bytes;
-    const size_t meta_bytes = (size_t)lr_meta_pitch(k) * sizeof(int32_t);
-    auto dispatch = [&](int ch) -> moe_status_t {
-      const int sl = ch % S, g0 = plan.group_begin[ch / S], g1 = plan.group_begin[ch / S + 1];
-      int d0 = prof_rec(L, L->s_disp);
-      if (p2p) {
-        moe_status_t r = p2p_put(0, ch, L->s_disp);
-        if (r) return r;
-        prof_mark(L, MOE_STAGE_DISPATCH, d0, prof_rec(L, L->s_disp));
-        CUDA_TRY(cudaEventRecord(L->ev_disp[ch], L->s_disp));
-        return MOE_OK;
-      }
-      TR_TRY(L->tr->group_start(0));
-      if (lr_ep) {  // one unique-row message + its meta per peer (R16)
-        char* urows = fp8 ? (char*)L->recvq : (char*)L->recvu;
-        for (int peer = 0; peer < D; ++peer) {
-          const int64_t s0 = usend_off[ch * D + peer], ns = ug[(size_t)me * G + ch * D + peer];
-          if (ns) {
-            TR_TRY(L->tr->send(dsend + s0 * drow, ns * drow, peer, 0, L->s_disp));
-            TR_TRY(L->tr->send((char*)L->meta_send + s0 * meta_bytes, ns * meta_bytes, peer, 0, L->s_disp));
-          }
-          const int64_t r0 = urecv[(size_t)ch * D + peer], nr = ug[(size_t)peer * G + ch * D + me];
-          if (nr) {
-            TR_TRY(L->tr->recv(urows + r0 * drow, nr * drow, peer, 0, L->s_disp));
-            TR_TRY(L->tr->recv((char*)L->meta_recv + r0 * meta_bytes, nr * meta_bytes, peer, 0, L->s_disp));
+        p2p_nseg[dir][ch] = n;
+        p2p_total[dir][ch] = pr[n];
+        if (dir == 1 && L->p2p_fuse && !lr_ep && !L->split_rem) {
+          bool one_kind = true;
+          for (int el = g0 + 1; el < g1; ++el) one_kind &= plan.expert_kind[el] == plan.expert_kind[g0];
+          if (one_kind) {
+            auto* rs = reinterpret_cast<epsmoe::GemmRowSeg*>(L->p2p_host + P2P_SEGS_BYTES + P2P_PRE_BYTES +
+                                                               p2p_fptr_bytes(D)) +
+                       (size_t)ch * moe_layer::P2P_MAXS;
+            int nr = 0;
+            for (int el = g0; el < g1; ++el)  // GEMM rows (e_l, slice, src) ascending
+              for (int src = 0; src < D; ++src) {
+                const int ex = me * E_loc + el;
+                const int64_t rows = cnt(src, ex, sl);
+                if (!rows || nr >= moe_layer::P2P_MAXS) continue;
+                rs[nr].r0 = rpos(el, sl, src);
+                rs[nr].n = rows;
+                rs[nr].dst = peer_buf(src, moe_layer::P2P_COMB, spos_all[(size_t)src * E * S + (size_t)ex * S + sl] * rowb);
+                ++nr;
+              }
+            fuse_comb[ch] = true;
+            fuse_nrseg[ch] = nr;
           }
         }
       }
-      for (int peer = 0; peer < D && !lr_ep; ++peer)
-        for (int el = g0; el < g1; ++el) {
-          const int ex = peer * E_loc + el;
-          const int64_t n_send = cnt(me, ex, sl);
-          if (n_send)
-            TR_TRY(L->tr->send(dsend + send_pos[(size_t)ex * S + sl] * drow, n_send * drow, peer, 0, L->s_disp));
-          const int64_t n_recv = cnt(peer, me * E_loc + el, sl);
-          if (n_recv) TR_TRY(L->tr->recv(drecv + rpos(el, sl, peer) * drow, n_recv * drow, peer, 0, L->s_disp));
-        }
-      TR_TRY(L->tr->group_end(0, L->s_disp));
+    CUDA_TRY(cudaMemcpyAsync(L->p2p_tab, L->p2p_host, p2p_table_bytes(D), cudaMemcpyHostToDevice, st));
+  }
+  auto p2p_put = [&](int dir, int ch, cudaStream_t ps) -> moe_status_t {
+    const size_t slot = (size_t)dir * MOE_MAX_CHUNKS + ch;
+    auto* dsegs = reinterpret_cast<epsmoe::P2PSeg*>(L->p2p_tab) + slot * moe_layer::P2P_MAXS;
+    auto* dpre = reinterpret_cast<int64_t*>(L->p2p_tab + P2P_SEGS_BYTES) + slot * (moe_layer::P2P_MAXS + 1);
+    auto* dfp = reinterpret_cast<uint32_t**>(L->p2p_tab + P2P_SEGS_BYTES + P2P_PRE_BYTES) + slot * D;
+    KERNEL_TRY(launch_p2p_put(dsegs, dpre, p2p_nseg[dir][ch], p2p_total[dir][ch], 2 * L->comm_ctas,
+                              L->p2p_done + slot, dfp, D, epoch, ps));
+    TR_TRY(L->tr->p2p_after_put((int)slot, ps));
+    return MOE_OK;
+  };
+  CUDA_TRY(cudaEventRecord(L->ev_ready, st));
+  CUDA_TRY(cudaStreamWaitEvent(L->s_disp, L->ev_ready, 0));
+  CUDA_TRY(cudaStreamWaitEvent(L->s_comb, L->ev_ready, 0));
+  const size_t row_bytes = (size_t)H * 2;
+  // dispatch payload: bf16 rows, or packed FP8 rows (NEXT-2) dequantised per chunk on arrival
+  char* dsend = fp8 ? (char*)L->sendq : (char*)L->send;
+  char* drecv = fp8 ? (char*)L->recvq : (char*)L->recv;
+  const size_t drow = fp8 ? (size_t)L->qpitch : row_bytes;
+  const size_t meta_bytes = (size_t)lr_meta_pitch(k) * sizeof(int32_t);
+  auto dispatch = [&](int ch) -> moe_status_t {
+    const int sl = ch % S, g0 = plan.group_begin[ch / S], g1 = plan.group_begin[ch / S + 1];
+    int d0 = prof_rec(L, L->s_disp);
+    if (p2p) {
+      moe_status_t r = p2p_put(0, ch, L->s_disp);
+      if (r) return r;
       prof_mark(L, MOE_STAGE_DISPATCH, d0, prof_rec(L, L->s_disp));
       CUDA_TRY(cudaEventRecord(L->ev_disp[ch], L->s_disp));
       return MOE_OK;
-    };
-    auto combine_send = [&](int ch) -> moe_status_t {
-      const int sl = ch % S, g0 = plan.group_begin[ch / S], g1 = plan.group_begin[ch / S + 1];
-      CUDA_TRY(cudaStreamWaitEvent(L->s_comb, L->ev_gemm[ch], 0));
-      int b0 = prof_rec(L, L->s_comb);
-      if (p2p) {
-        if (!fuse_comb[ch]) {
-          moe_status_t r = p2p_put(1, ch, L->s_comb);
-          if (r) return r;
+    }
+    TR_TRY(L->tr->group_start(0));
+    if (lr_ep) {  // one unique-row message + its meta per peer (R16)
+      char* urows = fp8 ? (char*)L->recvq : (char*)L->recvu;
+      for (int peer = 0; peer < D; ++peer) {
+        const int64_t s0 = usend_off[ch * D + peer], ns = ug[(size_t)me * G + ch * D + peer];
+        if (ns) {
+          TR_TRY(L->tr->send(dsend + s0 * drow, ns * drow, peer, 0, L->s_disp));
+          TR_TRY(L->tr->send((char*)L->meta_send + s0 * meta_bytes, ns * meta_bytes, peer, 0, L->s_disp));
         }
-        prof_mark(L, MOE_STAGE_COMB_A2A, b0, prof_rec(L, L->s_comb));
-        return MOE_OK;
-      }
-      TR_TRY(L->tr->group_start(1));
-      if (lr_ep) {  // each unique row returns as its LocalReduce partial (R16)
-        for (int peer = 0; peer < D; ++peer) {
-          const int64_t r0 = urecv[(size_t)ch * D + peer], nb = ug[(size_t)peer * G + ch * D + me];
-          if (nb) TR_TRY(L->tr->send((char*)L->recvu + r0 * row_bytes, nb * row_bytes, peer, 1, L->s_comb));
-          const int64_t s0 = usend_off[ch * D + peer], nh = ug[(size_t)me * G + ch * D + peer];
-          if (nh) TR_TRY(L->tr->recv((char*)L->comb + s0 * row_bytes, nh * row_bytes, peer, 1, L->s_comb));
+        const int64_t r0 = urecv[(size_t)ch * D + peer], nr = ug[(size_t)peer * G + ch * D + me];
+        if (nr) {
+          TR_TRY(L->tr->recv(urows + r0 * drow, nr * drow, peer, 0, L->s_disp));
+          TR_TRY(L->tr->recv((char*)L->meta_recv + r0 * meta_bytes, nr * meta_bytes, peer, 0, L->s_disp));
         }
       }
-      for (int peer = 0; peer < D && !lr_ep; ++peer)
-        for (int el = g0; el < g1; ++el) {
-          const int64_t n_back = cnt(peer, me * E_loc + el, sl);
-          if (n_back)
-            TR_TRY(L->tr->send((char*)L->o + rpos(el, sl, peer) * row_bytes, n_back * row_bytes, peer, 1, L->s_comb));
-          const int ex = peer * E_loc + el;
-          const int64_t n_home = cnt(me, ex, sl);
-          if (n_home)
-            TR_TRY(L->tr->recv((char*)L->comb + send_pos[(size_t)ex * S + sl] * row_bytes, n_home * row_bytes, peer, 1,
-                               L->s_comb));
-        }
-      TR_TRY(L->tr->group_end(1, L->s_comb));
+    }
+    for (int peer = 0; peer < D && !lr_ep; ++peer)
+      for (int el = g0; el < g1; ++el) {
+        const int ex = peer * E_loc + el;
+        const int64_t n_send = cnt(me, ex, sl);
+        if (n_send)
+          TR_TRY(L->tr->send(dsend + send_pos[(size_t)ex * S + sl] * drow, n_send * drow, peer, 0, L->s_disp));
+        const int64_t n_recv = cnt(peer, me * E_loc + el, sl);
+        if (n_recv) TR_TRY(L->tr->recv(drecv + rpos(el, sl, peer) * drow, n_recv * drow, peer, 0, L->s_disp));
+      }
+    TR_TRY(L->tr->group_end(0, L->s_disp));
+    prof_mark(L, MOE_STAGE_DISPATCH, d0, prof_rec(L, L->s_disp));
+    CUDA_TRY(cudaEventRecord(L->ev_disp[ch], L->s_disp));
+    return MOE_OK;
+  };
+  auto combine_send = [&](int ch) -> moe_status_t {
+    const int sl = ch % S, g0 = plan.group_begin[ch / S], g1 = plan.group_begin[ch / S + 1];
+    CUDA_TRY(cudaStreamWaitEvent(L->s_comb, L->ev_gemm[ch], 0));
+    int b0 = prof_rec(L, L->s_comb);
+    if (p2p) {
+      if (!fuse_comb[ch]) {
+        moe_status_t r = p2p_put(1, ch, L->s_comb);
+        if (r) return r;
+      }
       prof_mark(L, MOE_STAGE_COMB_A2A, b0, prof_rec(L, L->s_comb));
       return MOE_OK;
-    };
-    auto compute = [&](int ch) -> moe_status_t {
-      const int sl = ch % S, g0 = plan.group_begin[ch / S], g1 = plan.group_begin[ch / S + 1];
-      CUDA_TRY(cudaStreamWaitEvent(st, L->ev_disp[ch], 0));  // (p2p: my puts read `send`)
-      if (p2p) {  // every source's rows
-        TR_TRY(L->tr->p2p_before_wait(ch, 1, st));
-        KERNEL_TRY(launch_p2p_wait(L->p2p_flags + (size_t)ch * D, D, epoch, st));
-      }
-      const int64_t u0 = urecv[(size_t)ch * D], u1 = urecv[(size_t)(ch + 1) * D];
-      if (lr_ep) {  // unique rows -> expert-major GEMM rows (R6 order, so the GEMMs are unchanged)
-        KERNEL_TRY(launch_lr_expand(L->recvu, fp8 ? L->recvq : nullptr, L->qpitch, u0, u1, H, k, D, ch, L->lr_usrc_d,
-                                    L->lr_recv_off_d, L->meta_recv, L->recv, st));
-      } else if (fp8) {  // the chunk's rows: one range per expert, merged where contiguous (all, if S == 1)
-        int el = g0;
-        while (el < g1) {
-          const int64_t r0 = rpos(el, sl, 0);
-          int64_t r1 = rpos(el, sl, D - 1) + cnt(D - 1, me * E_loc + el, sl);
-          while (++el < g1 && rpos(el, sl, 0) == r1) r1 = rpos(el, sl, D - 1) + cnt(D - 1, me * E_loc + el, sl);
-          KERNEL_TRY(launch_dequant_rows(drecv + r0 * drow, r1 - r0, H, L->qpitch, (char*)L->recv + r0 * row_bytes,
-                                         st));
-        }
-      }
-      int a = g0;
-      while (a < g1) {
-        int b = a + 1;
-        while (b < g1 && plan.expert_kind[b] == plan.expert_kind[a]) ++b;
-        double rows = 0;
-        for (int el = a; el < b; ++el) rows += tcount[ch * E_loc + el];
-        const bool fz = p2p && fuse_comb[ch];
-        const size_t cslot = (size_t)MOE_MAX_CHUNKS + ch;
-        int err = compute_moe(
-            L, L->recv, L->recv_cap, L->recv_start_d + ch * E_loc, L->recv_count_d + ch * E_loc, a, b,
-            plan.expert_kind[a], num_ctas, pick_cta_pair(plan, rows / (b - a)), rows / (b - a), st, nullptr,
-            fz ? reinterpret_cast<const GemmRowSeg*>(L->p2p_tab + P2P_SEGS_BYTES + P2P_PRE_BYTES + p2p_fptr_bytes(D)) +
-                     (size_t)ch * moe_layer::P2P_MAXS
-               : nullptr,
-            fz ? fuse_nrseg[ch] : 0,
-            fz ? reinterpret_cast<uint32_t**>(L->p2p_tab + P2P_SEGS_BYTES + P2P_PRE_BYTES) + cslot * D : nullptr,
-            fz ? D : 0, epoch);
-        if (err) { set_error(std::string("ComputeMoE: ") + cudaGetErrorString((cudaError_t)err)); return MOE_ERR_CUDA; }
-        a = b;
-      }
-      // LocalReduce: the chunk's partial per unique row, in place of its x row
-      if (lr_ep) KERNEL_TRY(launch_lr_reduce(L->o, L->meta_recv, u0, u1, H, k, L->recvu, st));
-      if (p2p && fuse_comb[ch]) TR_TRY(L->tr->p2p_after_put(MOE_MAX_CHUNKS + ch, st));  // combine rows are out
-      CUDA_TRY(cudaEventRecord(L->ev_gemm[ch], st));
-      return MOE_OK;
-    };
-    // Algorithm 1 issue order
-    const int PN = plan.num_chunks;
-    moe_status_t s_ = dispatch(0);
-    if (s_) return s_;
-    for (int p = 1; p <= PN; ++p) {
-      if (p <= PN - 1 && (s_ = dispatch(p))) return s_;
-      if ((s_ = compute(p - 1))) return s_;
-      if (p - 2 >= 0 && (s_ = combine_send(p - 2))) return s_;
     }
-    if ((s_ = combine_send(PN - 1))) return s_;
-    CUDA_TRY(cudaEventRecord(L->ev_comb_done, L->s_comb));
-    CUDA_TRY(cudaStreamWaitEvent(st, L->ev_comb_done, 0));
-    if (side) CUDA_TRY(cudaStreamWaitEvent(st, L->ev_shared, 0));
-    if (p2p) {  // every chunk's combine rows from every expert rank
-      TR_TRY(L->tr->p2p_before_wait(MOE_MAX_CHUNKS, plan.num_chunks, st));
-      KERNEL_TRY(launch_p2p_wait(L->p2p_flags + (size_t)MOE_MAX_CHUNKS * D, plan.num_chunks * D, epoch, st));
+    TR_TRY(L->tr->group_start(1));
+    if (lr_ep) {  // each unique row returns as its LocalReduce partial (R16)
+      for (int peer = 0; peer < D; ++peer) {
+        const int64_t r0 = urecv[(size_t)ch * D + peer], nb = ug[(size_t)peer * G + ch * D + me];
+        if (nb) TR_TRY(L->tr->send((char*)L->recvu + r0 * row_bytes, nb * row_bytes, peer, 1, L->s_comb));
+        const int64_t s0 = usend_off[ch * D + peer], nh = ug[(size_t)me * G + ch * D + peer];
+        if (nh) TR_TRY(L->tr->recv((char*)L->comb + s0 * row_bytes, nh * row_bytes, peer, 1, L->s_comb));
+      }
     }
-    int c0 = prof_rec(L, st);
-    if (lr_ep)
-      KERNEL_TRY(launch_lr_combine(L->comb, L->SF ? L->s : nullptr, (int)T, H, k, L->posg, y, st));
-    else
-      KERNEL_TRY(launch_combine(L->comb, L->SF ? L->s : nullptr, (int)T, H, k, L->pos, topk_w, y, st));
-    prof_mark(L, MOE_STAGE_COMBINE, c0, prof_rec(L, st));
-    if (dbg && lr_ep) {
-      if (dbg->lr_pos) CUDA_TRY(cudaMemcpyAsync(dbg->lr_pos, L->posg, sizeof(int32_t) * T * k, cudaMemcpyDeviceToDevice, st));
-      if (dbg->lr_hist) CUDA_TRY(cudaMemcpyAsync(dbg->lr_hist, L->u_hist, sizeof(int32_t) * G, cudaMemcpyDeviceToDevice, st));
+    for (int peer = 0; peer < D && !lr_ep; ++peer)
+      for (int el = g0; el < g1; ++el) {
+        const int64_t n_back = cnt(peer, me * E_loc + el, sl);
+        if (n_back)
+          TR_TRY(L->tr->send((char*)L->o + rpos(el, sl, peer) * row_bytes, n_back * row_bytes, peer, 1, L->s_comb));
+        const int ex = peer * E_loc + el;
+        const int64_t n_home = cnt(me, ex, sl);
+        if (n_home)
+          TR_TRY(L->tr->recv((char*)L->comb + send_pos[(size_t)ex * S + sl] * row_bytes, n_home * row_bytes, peer, 1,
+                             L->s_comb));
+      }
+    TR_TRY(L->tr->group_end(1, L->s_comb));
+    prof_mark(L, MOE_STAGE_COMB_A2A, b0, prof_rec(L, L->s_comb));
+    return MOE_OK;
+  };
+  auto compute = [&](int ch) -> moe_status_t {
+    const int sl = ch % S, g0 = plan.group_begin[ch / S], g1 = plan.group_begin[ch / S + 1];
+    CUDA_TRY(cudaStreamWaitEvent(st, L->ev_disp[ch], 0));  // (p2p: my puts read `send`)
+    if (p2p) {  // every source's rows
+      TR_TRY(L->tr->p2p_before_wait(ch, 1, st));
+      KERNEL_TRY(launch_p2p_wait(L->p2p_flags + (size_t)ch * D, D, epoch, st));
     }
+    const int64_t u0 = urecv[(size_t)ch * D], u1 = urecv[(size_t)(ch + 1) * D];
+    if (lr_ep) {  // unique rows -> expert-major GEMM rows (R6 order, so the GEMMs are unchanged)
+      KERNEL_TRY(launch_lr_expand(L->recvu, fp8 ? L->recvq : nullptr, L->qpitch, u0, u1, H, k, D, ch, L->lr_usrc_d,
+                                  L->lr_recv_off_d, L->meta_recv, L->recv, st));
+    } else if (fp8) {  // the chunk's rows: one range per expert, merged where contiguous (all, if S == 1)
+      int el = g0;
+      while (el < g1) {
+        const int64_t r0 = rpos(el, sl, 0);
+        int64_t r1 = rpos(el, sl, D - 1) + cnt(D - 1, me * E_loc + el, sl);
+        while (++el < g1 && rpos(el, sl, 0) == r1) r1 = rpos(el, sl, D - 1) + cnt(D - 1, me * E_loc + el, sl);
+        KERNEL_TRY(launch_dequant_rows(drecv + r0 * drow, r1 - r0, H, L->qpitch, (char*)L->recv + r0 * row_bytes,
+                                       st));
+      }
+    }
+    int a = g0;
+    while (a < g1) {
+      int b = a + 1;
+      while (b < g1 && plan.expert_kind[b] == plan.expert_kind[a]) ++b;
+      double rows = 0;
+      for (int el = a; el < b; ++el) rows += tcount[ch * E_loc + el];
+      const bool fz = p2p && fuse_comb[ch];
+      const size_t cslot = (size_t)MOE_MAX_CHUNKS + ch;
+      int err = compute_moe(
+          L, L->recv, L->recv_cap, L->recv_start_d + ch * E_loc, L->recv_count_d + ch * E_loc, a, b,
+          plan.expert_kind[a], num_ctas, pick_cta_pair(plan, rows / (b - a)), rows / (b - a), st, nullptr,
+          fz ? reinterpret_cast<const GemmRowSeg*>(L->p2p_tab + P2P_SEGS_BYTES + P2P_PRE_BYTES + p2p_fptr_bytes(D)) +
+                   (size_t)ch * moe_layer::P2P_MAXS
+             : nullptr,
+          fz ? fuse_nrseg[ch] : 0,
+          fz ? reinterpret_cast<uint32_t**>(L->p2p_tab + P2P_SEGS_BYTES + P2P_PRE_BYTES) + cslot * D : nullptr,
+          fz ? D : 0, epoch);
+      if (err) { set_error(std::string("ComputeMoE: ") + cudaGetErrorString((cudaError_t)err)); return MOE_ERR_CUDA; }
+      a = b;
+    }
+    // LocalReduce: the chunk's partial per unique row, in place of its x row
+    if (lr_ep) KERNEL_TRY(launch_lr_reduce(L->o, L->meta_recv, u0, u1, H, k, L->recvu, st));
+    if (p2p && fuse_comb[ch]) TR_TRY(L->tr->p2p_after_put(MOE_MAX_CHUNKS + ch, st));  // combine rows are out
+    CUDA_TRY(cudaEventRecord(L->ev_gemm[ch], st));
+    return MOE_OK;
+  };
+  // Algorithm 1 issue order
+  const int PN = plan.num_chunks;
+  moe_status_t s_ = dispatch(0);
+  if (s_) return s_;
+  for (int p = 1; p <= PN; ++p) {
+    if (p <= PN - 1 && (s_ = dispatch(p))) return s_;
+    if ((s_ = compute(p - 1))) return s_;
+    if (p - 2 >= 0 && (s_ = combine_send(p - 2))) return s_;
   }
-  prof_mark(L, MOE_STAGE_TOTAL, p_total, prof_rec(L, st));
+  if ((s_ = combine_send(PN - 1))) return s_;
+  CUDA_TRY(cudaEventRecord(L->ev_comb_done, L->s_comb));
+  CUDA_TRY(cudaStreamWaitEvent(st, L->ev_comb_done, 0));
+  if (side) CUDA_TRY(cudaStreamWaitEvent(st, L->ev_shared, 0));
+  if (p2p) {  // every chunk's combine rows from every expert rank
+    TR_TRY(L->tr->p2p_before_wait(MOE_MAX_CHUNKS, plan.num_chunks, st));
+    KERNEL_TRY(launch_p2p_wait(L->p2p_flags + (size_t)MOE_MAX_CHUNKS * D, plan.num_chunks * D, epoch, st));
+  }
+  int c0 = prof_rec(L, st);
+  if (lr_ep)
+    KERNEL_TRY(launch_lr_combine(L->comb, L->SF ? L->s : nullptr, (int)T, H, k, L->posg, y, st));
+  else
+    KERNEL_TRY(launch_combine(L->comb, L->SF ? L->s : nullptr, (int)T, H, k, L->pos, topk_w, y, st));
+  prof_mark(L, MOE_STAGE_COMBINE, c0, prof_rec(L, st));
+  if (dbg && lr_ep) {
+    if (dbg->lr_pos) CUDA_TRY(cudaMemcpyAsync(dbg->lr_pos, L->posg, sizeof(int32_t) * T * k, cudaMemcpyDeviceToDevice, st));
+    if (dbg->lr_hist) CUDA_TRY(cudaMemcpyAsync(dbg->lr_hist, L->u_hist, sizeof(int32_t) * G, cudaMemcpyDeviceToDevice, st));
+  }
+  return MOE_OK;
+}
 
+// Debug outputs (moe_debug_t).
+moe_status_t fwd_debug(Fwd& F) {
+  moe_layer* L = F.L;
+  const moe_config_t& c = L->cfg;
+  const void* x = F.x;
+  const int64_t T = F.T;
+  void* y = F.y;
+  cudaStream_t st = F.st;
+  moe_debug_t* dbg = F.dbg;
+  moe_plan_t& plan = F.plan;
+  const moe_plan_t* plan_in = F.plan_in;
+  const int E = c.num_experts, k = c.top_k, H = c.hidden, D = c.ep, E_loc = L->E_loc;
+  const int num_ctas = F.num_ctas;
+  int32_t* topk_idx = F.topk_idx;
+  float* topk_w = F.topk_w;
+  const bool override_routing = F.override_routing;
+  (void)x; (void)y; (void)dbg; (void)plan_in; (void)E_loc; (void)override_routing; (void)topk_idx;
   if (dbg) {
     if (dbg->logits && !override_routing)
       CUDA_TRY(cudaMemcpyAsync(dbg->logits, L->logits, sizeof(float) * T * E, cudaMemcpyDeviceToDevice, st));
@@ -1379,6 +1458,47 @@ moe_status_t moe_layer_forward(moe_layer_t* L, const void* x, int64_t T, void* y
     }
   }
   return MOE_OK;
+}
+
+}  // namespace
+
+moe_status_t moe_layer_forward(moe_layer_t* L, const void* x, int64_t T, void* y, const moe_plan_t* plan_in,
+                               void* stream_v, moe_debug_t* dbg) {
+  if (!L || (!x && T > 0) || (!y && T > 0) || T < 0) { set_error("null argument"); return MOE_ERR_INVALID; }
+  const moe_config_t& c = L->cfg;
+  if (T > c.max_tokens) { set_error("T_loc > max_tokens"); return MOE_ERR_CAPACITY; }
+  cudaStream_t st = (cudaStream_t)stream_v;
+  const int D = c.ep;
+  L->last_launches = 0;
+  L->pev_used = 0;
+  L->marks.clear();
+  const int p_total = prof_rec(L, st);
+  const bool override_routing = dbg && dbg->override_routing;
+  if (override_routing && (!dbg->topk_idx || !dbg->topk_w)) { set_error("override needs topk_idx/topk_w"); return MOE_ERR_INVALID; }
+  int32_t* topk_idx = override_routing ? dbg->topk_idx : L->topk_idx;
+  float* topk_w = override_routing ? dbg->topk_w : L->topk_w;
+
+  moe_plan_t plan;
+  if (plan_in) {
+    plan = *plan_in;
+    int pv = plan_normalise(c, &plan);
+    if (pv) { set_error("invalid plan"); return (moe_status_t)pv; }
+  }
+  // GEMM SM budget (A15, P:363-365, Table IV): a persistent GEMM owns every SM
+  // it runs on (~220 KB smem), so at ep > 1 it must leave SMs for the two
+  // communicators' kernels or the all2all could not overlap it at all.
+  const int default_ctas = (D > 1) ? L->num_sms - 2 * L->comm_ctas : L->num_sms;
+  int num_ctas = (plan_in && plan.sm_gemm > 0) ? std::min(plan.sm_gemm, L->num_sms) : default_ctas;
+
+  Fwd F{L, x, T, y, plan_in, st, dbg, plan};
+  F.num_ctas = num_ctas;
+  F.topk_idx = topk_idx;
+  F.topk_w = topk_w;
+  F.override_routing = override_routing;
+  if (moe_status_t r = fwd_routing(F)) return r;
+  if (moe_status_t r = (D == 1) ? fwd_local(F) : fwd_ep(F)) return r;
+  prof_mark(L, MOE_STAGE_TOTAL, p_total, prof_rec(L, st));
+  return dbg ? fwd_debug(F) : MOE_OK;
 }
 
 // Token-slice schedule of moe_layer_forward_host: relative slice sizes chosen
