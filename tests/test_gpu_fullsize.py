@@ -96,12 +96,14 @@ def test_full_size_parity(name):
         torch.cuda.empty_cache()
 
 
-@pytest.mark.parametrize("name", ["dsv2", "mixtral"])
-def test_full_size_ep8_on_one_gpu(name):
+@pytest.mark.parametrize("name,skew,fp8", [("dsv2", 0.0, False), ("mixtral", 0.0, False), ("dsv2", 1.0, True)])
+def test_full_size_ep8_on_one_gpu(name, skew, fp8):
     """BASELINE's EP = 8 configuration at full size, the eight ranks as eight
     layers on one B200 (in-process group), planner-chosen plan (Mixtral: one
     expert per rank, so token slices), both all2all data planes: y == the EP = 1
-    layer's y, bit for bit, on every token."""
+    layer's y, bit for bit, on every token.  Also under skewed (Zipf-like)
+    routing with the FP8 dispatch payload (R15: EP = D == EP = 1 holds in FP8)."""
+    from gen import router_skew_bias
     import threading
 
     from paper_2410_12247_b200 import LocalGroup
@@ -116,7 +118,9 @@ def test_full_size_ep8_on_one_gpu(name):
         w.update(ws_gate=_gen((SF, H), TID_WS_GATE, 0, MODE_UNIF, sH), ws_up=_gen((SF, H), TID_WS_UP, 0, MODE_UNIF, sH),
                  ws_down=_gen((H, SF), TID_WS_DOWN, 0, MODE_UNIF, unif_scale(SF)))
     x = _gen((T, H), TID_X, 0, MODE_UNIF, unif_scale(1))
-    ref_layer = MoELayer(E, k, H, F, w, S=S, Fs=Fs, max_tokens=T, norm_topk=norm)
+    if skew:
+        w["router_bias"] = torch.from_numpy(router_skew_bias(E, skew, SEED)).cuda()
+    ref_layer = MoELayer(E, k, H, F, w, S=S, Fs=Fs, max_tokens=T, norm_topk=norm, dispatch_fp8=fp8)
     y1 = ref_layer.forward(x)
     torch.cuda.synchronize()
     y1 = y1.cpu()
@@ -127,11 +131,11 @@ def test_full_size_ep8_on_one_gpu(name):
         group = LocalGroup(D)
         layers = []
         for r in range(D):
-            wr = {n: t for n, t in w.items() if not n.startswith("w_") or n == "w_router"}
+            wr = {n: t for n, t in w.items() if n not in ("w_gate", "w_up", "w_down")}
             for n in ("w_gate", "w_up", "w_down"):
                 wr[n] = w[n][r * E_loc:(r + 1) * E_loc]
             layers.append(MoELayer(E, k, H, F, wr, S=S, Fs=Fs, ep=D, rank=r, max_tokens=int(start[r + 1] - start[r]),
-                                   norm_topk=norm, local_group=group, a2a_p2p=p2p))
+                                   norm_topk=norm, local_group=group, a2a_p2p=p2p, dispatch_fp8=fp8))
         ys, plans, errs = [None] * D, [None] * D, []
 
         def worker(r):
@@ -153,10 +157,10 @@ def test_full_size_ep8_on_one_gpu(name):
             t.join(timeout=300)
         assert not errs, errs
         assert all(p == plans[0] for p in plans)          # every rank ran the same plan
-        print(f"{name} EP8 p2p={p2p} plan: chunks={plans[0]['num_chunks']} slices={plans[0]['token_slices']} "
+        print(f"{name} skew={skew} fp8={fp8} EP8 p2p={p2p} plan: chunks={plans[0]['num_chunks']} slices={plans[0]['token_slices']} "
               f"groups={plans[0]['group_begin']}")
         y = torch.cat([v.cpu() for v in ys])
-        assert torch.equal(y, y1), f"{name} EP8 p2p={p2p} plan={plans[0]}"
+        assert torch.equal(y, y1), f"{name} skew={skew} fp8={fp8} EP8 p2p={p2p} plan={plans[0]}"
         for L in layers:
             L.close()
         del layers, ys
