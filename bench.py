@@ -57,6 +57,9 @@ def parse():
     p.add_argument("--route-groups", type=int, default=0, help="device-limited routing groups (NEXT-4, R17)")
     p.add_argument("--route-topk-groups", type=int, default=0, help="M: groups a token may use (R17)")
     p.add_argument("--token-slices", type=int, default=1, help="with --chunks: chunks = groups x slices (R8)")
+    p.add_argument("--graph", default="auto", choices=["auto", "on", "off"],
+                   help="ep == 1: replay the forward as a CUDA graph (auto: batches <= 4096 tokens, where "
+                        "launch gaps matter)")
     p.add_argument("--a2a", default="nccl", choices=["nccl", "p2p"],
                    help="ep > 1 all2all: NCCL send/recv, or the layer's put kernels over NVLink peer memory")
     return p.parse_args()
@@ -321,8 +324,21 @@ def ours(args, cfg):
     for _ in range(args.warmup):
         layer.forward(x, y, plan=plan)
     torch.cuda.synchronize()
+    # CUDA graph of one whole forward (ep == 1 has no host synchronisation); per-
+    # stage timings then come from eager forwards after the timed region
+    use_graph = D == 1 and (args.graph == "on" or (args.graph == "auto" and T_loc <= 4096))
+    graph = None
+    if use_graph:
+        if plan is None:
+            plan = layer.plan(T)   # the planner runs on the host: fix its plan for the capture
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            layer.forward(x, y, plan=plan)
+        graph.replay()
+        torch.cuda.synchronize()
+        launches_per_forward = layer.last_launches()
 
-    layer.set_profiling(True)
+    layer.set_profiling(not use_graph)
     gpu_idx = local
     vis = os.environ.get("CUDA_VISIBLE_DEVICES")
     if vis:
@@ -343,6 +359,10 @@ def ours(args, cfg):
     t_start = clocks.mark()
     ev0.record(stream)
     for _ in range(args.steps):
+        if use_graph:
+            graph.replay()
+            launches += launches_per_forward
+            continue
         layer.forward(x, y, plan=plan)
         launches += layer.last_launches()
         for name, (ms, cnt) in layer.stage_ms().items():
@@ -354,6 +374,14 @@ def ours(args, cfg):
     if D > 1:
         dist.barrier()
     clk = clocks.stop(t_start, t_end)
+    if use_graph:  # stage timings from eager forwards (informational)
+        layer.set_profiling(True)
+        for _ in range(args.steps):
+            layer.forward(x, y, plan=plan)
+            for name, (ms, cnt) in layer.stage_ms().items():
+                stage_sum[name] = stage_sum.get(name, 0.0) + ms
+                stage_cnt[name] = stage_cnt.get(name, 0) + cnt
+        torch.cuda.synchronize()
     layer.set_profiling(False)
     ms_total = ev0.elapsed_time(ev1)
     t = torch.tensor([ms_total], dtype=torch.float64, device=dev)
@@ -459,7 +487,8 @@ def ours(args, cfg):
                 "config": {"workload": cfg["name"], "E": E, "k": k, "H": H, "F": F, "shared": S, "shared_ffn": Fs,
                            "global_tokens": T, "ep": D, "parallelism": f"ep{D}" + (f"+dp{D}" if D > 1 else ""),
                            "skew": args.skew, "l2": "inputs > L2 (x alone %.0f MB), no flush" % (T_loc * H * 2 / 1e6),
-                           **opts, "a2a": args.a2a if D > 1 else None, "plan": plan_used},
+                           **opts, "a2a": args.a2a if D > 1 else None, "cuda_graph": bool(use_graph),
+                           "plan": plan_used},
                 "roofline": roofline, "layer_roofline": layer_roofline,
                 "exposed_a2a_ms": stages.get("exposed_a2a", 0.0), "stages_ms": stages,
                 "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk}
