@@ -392,3 +392,48 @@ def test_p2p_repeated_forwards_same_layers():
         assert np.array_equal(torch.cat(outs[i]).float().cpu().numpy(), y1)
     for L in layers:
         L.close()
+
+
+def test_forward_host_ep2_sliced():
+    """moe_layer_forward_host at ep > 1: every rank splits its tokens by the same
+    config-derived slice schedule (each slice forward is a collective); y equals
+    the device-buffer forward, bit for bit."""
+    D, E_loc = 2, 8
+    inp = Inputs(E=16, k=2, H=256, F=256, S=1, Fs=128, T=20000, seed=17)
+    start = oracle.token_shards(inp.T, D)
+    group = LocalGroup(D)
+    layers = []
+    for r in range(D):
+        w = dict(w_router=dev_bf16(inp.w_router), w_gate=dev_bf16(inp.w_gate[r * E_loc:(r + 1) * E_loc]),
+                 w_up=dev_bf16(inp.w_up[r * E_loc:(r + 1) * E_loc]),
+                 w_down=dev_bf16(inp.w_down[r * E_loc:(r + 1) * E_loc]),
+                 ws_gate=dev_bf16(inp.ws_gate), ws_up=dev_bf16(inp.ws_up), ws_down=dev_bf16(inp.ws_down))
+        layers.append(MoELayer(16, 2, 256, 256, w, S=1, Fs=128, ep=D, rank=r, max_tokens=10000, norm_topk=1,
+                               local_group=group))
+    dev_out, host_out, errs = [None] * D, [None] * D, []
+
+    def worker(r):
+        try:
+            torch.cuda.set_device(0)
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                x = dev_bf16(inp.x[start[r]:start[r + 1]])
+                s.synchronize()
+                dev_out[r] = layers[r].forward(x, plan=make_plan(2, MOE_GEMM_GROUPED), stream=s).cpu()
+                xh = x.cpu().pin_memory()
+                yh = torch.empty_like(xh).pin_memory()
+                layers[r].forward_host(xh, yh, plan=make_plan(2, MOE_GEMM_GROUPED), stream=s)
+                host_out[r] = yh.clone()
+        except Exception as e:  # pragma: no cover
+            errs.append(repr(e))
+
+    th = [threading.Thread(target=worker, args=(r,), daemon=True) for r in range(D)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=120)
+    assert not errs, errs
+    for r in range(D):
+        assert torch.equal(dev_out[r], host_out[r])
+    for L in layers:
+        L.close()
