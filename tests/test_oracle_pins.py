@@ -532,3 +532,30 @@ def test_device_limited_routing_special_cases_and_bound():
     # the restriction can only lower the selected logits
     idx2, _ = oracle.topk_gating(lg, 4, 1, route_groups=4, route_topk_groups=2)
     assert (np.take_along_axis(lg, idx2, 1).sum(1) <= np.take_along_axis(lg, plain[0], 1).sum(1)).all()
+
+
+def test_comm_volume_bounds_p265():
+    """with tokens routed to g devices, the DP+EP all2all volume lies
+    in [2P(D-1)/D, g 2P(D-1)/D] (P = the batch's activation bytes; dispatch +
+    combine).  With the dedup of R16 (one row per destination) and device-
+    limited routing (R17) with groups = ranks, M = g: a token reaches at most g
+    ranks (almost always exactly g once k >= g), so the volume sits at the upper
+    bound; g = 1 is the lower bound."""
+    D, E, k, T = 8, 64, 6, 20000
+    rng = np.random.default_rng(11)
+    logits = rng.standard_normal((T, E)).astype(np.float32)
+    P = T * 1.0                                      # in units of one activation row
+    for g in (1, 2, 3):
+        idx, _ = oracle.topk_gating(logits, k, 1, route_groups=D, route_topk_groups=g)
+        lay = oracle.lr_layout(idx, E, D, 1)
+        start = lay["token_start"]
+        remote = 0
+        for r in range(D):                           # rows each rank sends to other ranks
+            remote += int(lay["u_hist"][r].sum() - lay["u_hist"][r][r])
+        V = 2 * remote                               # dispatch + combine
+        lo, hi = 2 * P * (D - 1) / D, g * 2 * P * (D - 1) / D
+        assert lo - 1e-9 <= V * (1 + 0.02) and V <= hi * 1.02
+        assert abs(V - hi) / hi < 0.02               # a token's g devices: (D-1)/D of them remote on average
+        # per token: at most g destination ranks, almost always exactly g
+        ng = np.array([len(set((row // (E // D)).tolist())) for row in idx])
+        assert ng.max() <= g and (ng == g).mean() > 0.99
