@@ -271,6 +271,17 @@ moe_status_t moe_layer_forward(moe_layer_t* layer, const void* x, int64_t T_loc,
 moe_status_t moe_layer_forward_host(moe_layer_t* layer, const void* x_host, int64_t T_loc, void* y_host,
                                     const moe_plan_t* plan, void* stream);
 
+/* moe_layer_forward_host without the final wait: enqueues the copies and the
+ * layer and returns.  Consecutive calls overlap: the layer double-buffers its
+ * device staging, so call i+1's host->device copy runs while call i computes
+ * and call i's device->host copy drains while call i+1 computes.  x_host and
+ * y_host belong to the layer until moe_layer_host_sync returns; y_host is not
+ * valid before that.  ep > 1: collective like moe_layer_forward. */
+moe_status_t moe_layer_forward_host_async(moe_layer_t* layer, const void* x_host, int64_t T_loc, void* y_host,
+                                          const moe_plan_t* plan, void* stream);
+/* Wait for every host-buffer call issued so far (`stream` = the calls' stream). */
+moe_status_t moe_layer_host_sync(moe_layer_t* layer, void* stream);
+
 /* Per-stage device timing of the last forward (CUDA events recorded on the
  * stream each stage is launched on).  enable = 1 turns recording on. */
 enum {

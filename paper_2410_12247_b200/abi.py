@@ -92,6 +92,9 @@ _SIGS = {
                                     C.c_void_p, C.POINTER(moe_debug_t)]),
     "moe_layer_forward_host": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p,
                                          C.POINTER(moe_plan_t), C.c_void_p]),
+    "moe_layer_forward_host_async": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p,
+                                               C.POINTER(moe_plan_t), C.c_void_p]),
+    "moe_layer_host_sync": (C.c_int, [C.c_void_p, C.c_void_p]),
     "moe_layer_last_launches": (C.c_int32, [C.c_void_p]),
     "moe_layer_set_profiling": (C.c_int, [C.c_void_p, C.c_int32]),
     "moe_layer_stage_ms": (C.c_int, [C.c_void_p, C.POINTER(C.c_float), C.POINTER(C.c_int32)]),

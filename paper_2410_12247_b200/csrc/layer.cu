@@ -65,7 +65,9 @@ struct moe_layer {
   char* p2p_host = nullptr;
   bool p2p_fuse = true;  // EPSMOE_P2P_FUSE=0: combine by put kernel instead of the DownGemm's scatter
   int32_t* ughist_host = nullptr;  // pinned [ep*256]
-  void *x_dev = nullptr, *y_dev = nullptr;  // staging for forward_host
+  void *x_dev[2] = {}, *y_dev[2] = {};  // forward_host staging, double-buffered across calls
+  int hb = 0;                            // staging buffer of the next host call
+  cudaEvent_t ev_xfree[2] = {}, ev_yfree[2] = {};  // staging buffer b consumed / drained
   // host
   int32_t* ghist_host = nullptr;    // pinned [ep*E]
   // pinned: per-chunk GEMM row tables [2][TBL] (start, count; chunk c at c*E_loc), then the
@@ -79,7 +81,7 @@ struct moe_layer {
   cudaStream_t s_side = nullptr;  // shared experts, concurrent with routing / dispatch
   cudaStream_t s_h2d = nullptr, s_d2h = nullptr;  // forward_host copy streams
   static constexpr int MAX_HOST_SLICES = 8;
-  cudaEvent_t ev_host_start = nullptr, ev_in[MAX_HOST_SLICES] = {}, ev_out[MAX_HOST_SLICES] = {};
+  cudaEvent_t ev_in[MAX_HOST_SLICES] = {}, ev_out[MAX_HOST_SLICES] = {};
   cudaEvent_t ev_router = nullptr, ev_shared = nullptr;
   // ep == 1 with shared experts, how the shared DownGemm meets the combine
   // (EPSMOE_FUSE_COMBINE): 0 in order (default); 1 one kernel (EPI_COMBINE
@@ -258,8 +260,10 @@ size_t carve(moe_layer* L, char* base) {
   }
   L->hs = SF ? cv.take<uint16_t>(T * SF) : nullptr;
   L->s = SF ? cv.take<uint16_t>(T * H) : nullptr;
-  L->x_dev = cv.take<uint16_t>(T * H);
-  L->y_dev = cv.take<uint16_t>(T * H);
+  for (int b = 0; b < 2; ++b) {
+    L->x_dev[b] = cv.take<uint16_t>(T * H);
+    L->y_dev[b] = cv.take<uint16_t>(T * H);
+  }
   return cv.off + ALIGN;
 }
 
@@ -498,11 +502,16 @@ static moe_status_t create_impl(const moe_config_t* cfg, const moe_weights_t* w,
     L->comm_ctas = std::max(1, std::min(32, cv ? std::atoi(cv) : 8));
   }
   if (cudaStreamCreateWithFlags(&L->s_h2d, cudaStreamNonBlocking) != cudaSuccess ||
-      cudaStreamCreateWithFlags(&L->s_d2h, cudaStreamNonBlocking) != cudaSuccess ||
-      cudaEventCreateWithFlags(&L->ev_host_start, cudaEventDisableTiming) != cudaSuccess) {
+      cudaStreamCreateWithFlags(&L->s_d2h, cudaStreamNonBlocking) != cudaSuccess) {
     set_error("copy stream creation failed");
     return fail(MOE_ERR_CUDA);
   }
+  for (int b = 0; b < 2; ++b)
+    if (cudaEventCreateWithFlags(&L->ev_xfree[b], cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&L->ev_yfree[b], cudaEventDisableTiming) != cudaSuccess) {
+      set_error("event creation failed");
+      return fail(MOE_ERR_CUDA);
+    }
   for (int i = 0; i < moe_layer::MAX_HOST_SLICES; ++i)
     if (cudaEventCreateWithFlags(&L->ev_in[i], cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&L->ev_out[i], cudaEventDisableTiming) != cudaSuccess) {
@@ -600,12 +609,11 @@ moe_status_t moe_layer_destroy(moe_layer_t* L) {
   if (L->s_side) cudaStreamDestroy(L->s_side);
   if (L->s_h2d) cudaStreamDestroy(L->s_h2d);
   if (L->s_d2h) cudaStreamDestroy(L->s_d2h);
-  if (L->ev_host_start) cudaEventDestroy(L->ev_host_start);
   for (int i = 0; i < moe_layer::MAX_HOST_SLICES; ++i) {
     if (L->ev_in[i]) cudaEventDestroy(L->ev_in[i]);
     if (L->ev_out[i]) cudaEventDestroy(L->ev_out[i]);
   }
-  for (cudaEvent_t e : {L->ev_router, L->ev_shared})
+  for (cudaEvent_t e : {L->ev_router, L->ev_shared, L->ev_xfree[0], L->ev_xfree[1], L->ev_yfree[0], L->ev_yfree[1]})
     if (e) cudaEventDestroy(e);
   for (cudaEvent_t e : L->ev_piece)
     if (e) cudaEventDestroy(e);
@@ -1508,7 +1516,13 @@ moe_status_t moe_layer_forward(moe_layer_t* L, const void* x, int64_t T, void* y
 // inflated by the 256-row tile padding of a slice's rows per expert, plus a
 // fixed ~0.3 ms per forward.  A function of the config only, so every rank
 // (each slice is a collective when ep > 1) derives the same schedule.
-std::vector<double> host_slice_schedule(const moe_config_t& c) {
+std::vector<double> host_slice_schedule(const moe_config_t& c, bool overlapped) {
+  // Overlapped calls (async) run the copy streams ahead across calls: a call
+  // then costs its busiest stream and slicing only shortens the one-off fill and
+  // drain while inflating the GEMMs' tile padding, so one slice (measured: DSv2
+  // e2e 23.6 ms per call over 8 calls unsliced vs 24.9-26.8 sliced; Mixtral 8.7
+  // vs 9.1-11.1).
+  if (overlapped) return {1.0};
   const double T = (double)c.max_tokens, H = c.hidden, F = c.ffn, k = c.top_k, E = c.num_experts;
   const double SF = (double)c.num_shared * c.shared_ffn;
   const double copy_tok = 2.0 * H / 50e9;
@@ -1538,17 +1552,21 @@ std::vector<double> host_slice_schedule(const moe_config_t& c) {
   return best;
 }
 
-moe_status_t moe_layer_forward_host(moe_layer_t* L, const void* x_host, int64_t T, void* y_host,
-                                    const moe_plan_t* plan, void* stream_v) {
+namespace {
+// One host-buffer call: token slices of x_host -> staging buffer b (s_h2d) ->
+// layer (st) -> y_host (s_d2h), each stream in order, event-chained per slice.
+// The staging pair alternates between calls, so a call's copies overlap the
+// previous call's compute; buffer b is reused only after the call two back
+// consumed (x) and drained (y) it.
+moe_status_t host_call(moe_layer* L, const void* x_host, int64_t T, void* y_host, const moe_plan_t* plan,
+                       void* stream_v, bool overlapped) {
   if (!L || T < 0 || T > L->cfg.max_tokens) { set_error("bad argument"); return MOE_ERR_INVALID; }
   cudaStream_t st = (cudaStream_t)stream_v;
   const int64_t row = (int64_t)L->cfg.hidden * 2;
-  // y_t depends only on x_t, so the batch is processed in token
-  // slices: the H2D copy of slice s+1 and the D2H copy of slice s-1 run on
-  // their own streams while the layer computes slice s.  The slice count is a
-  // function of max_tokens (identical on every rank: each slice's forward is
-  // a collective when ep > 1), chosen so slices keep >= 16K tokens.
-  // EPSMOE_HOST_SLICES="w0,w1,..." (<= 8 relative weights) overrides the schedule.
+  // y_t depends only on x_t: slices of the batch pipeline the
+  // copies against the layer.  The schedule is a function of the config only
+  // (identical on every rank: each slice's forward is a collective when ep > 1).
+  // EPSMOE_HOST_SLICES="w0,w1,..." (<= 8 relative weights) overrides it.
   std::vector<double> wts;
   if (const char* hs = std::getenv("EPSMOE_HOST_SLICES")) {
     for (const char* p = hs; *p && (int)wts.size() < moe_layer::MAX_HOST_SLICES;) {
@@ -1559,7 +1577,7 @@ moe_status_t moe_layer_forward_host(moe_layer_t* L, const void* x_host, int64_t 
       p = (*end == ',') ? end + 1 : end;
     }
   }
-  if (wts.empty()) wts = host_slice_schedule(L->cfg);
+  if (wts.empty()) wts = host_slice_schedule(L->cfg, overlapped);
   const int S = (int)wts.size();
   std::vector<int64_t> bound(S + 1, 0);
   double wsum = 0, acc = 0;
@@ -1568,12 +1586,14 @@ moe_status_t moe_layer_forward_host(moe_layer_t* L, const void* x_host, int64_t 
     acc += wts[s];
     bound[s + 1] = (s + 1 == S) ? T : std::min<int64_t>(T, (int64_t)std::llround(T * acc / wsum));
   }
-  CUDA_TRY(cudaEventRecord(L->ev_host_start, st));  // x_dev / y_dev free once prior work on st is done
-  CUDA_TRY(cudaStreamWaitEvent(L->s_h2d, L->ev_host_start, 0));
+  const int b = L->hb;
+  L->hb ^= 1;
+  CUDA_TRY(cudaStreamWaitEvent(L->s_h2d, L->ev_xfree[b], 0));  // x staging b read by the call two back
+  CUDA_TRY(cudaStreamWaitEvent(st, L->ev_yfree[b], 0));        // y staging b copied out by the call two back
   for (int s = 0; s < S; ++s) {
     const int64_t t0 = bound[s], n = bound[s + 1] - t0;
-    char* xd = (char*)L->x_dev + t0 * row;
-    char* yd = (char*)L->y_dev + t0 * row;
+    char* xd = (char*)L->x_dev[b] + t0 * row;
+    char* yd = (char*)L->y_dev[b] + t0 * row;
     if (n) CUDA_TRY(cudaMemcpyAsync(xd, (const char*)x_host + t0 * row, n * row, cudaMemcpyHostToDevice, L->s_h2d));
     CUDA_TRY(cudaEventRecord(L->ev_in[s], L->s_h2d));
     CUDA_TRY(cudaStreamWaitEvent(st, L->ev_in[s], 0));
@@ -1583,8 +1603,30 @@ moe_status_t moe_layer_forward_host(moe_layer_t* L, const void* x_host, int64_t 
     CUDA_TRY(cudaStreamWaitEvent(L->s_d2h, L->ev_out[s], 0));
     if (n) CUDA_TRY(cudaMemcpyAsync((char*)y_host + t0 * row, yd, n * row, cudaMemcpyDeviceToHost, L->s_d2h));
   }
+  CUDA_TRY(cudaEventRecord(L->ev_xfree[b], st));
+  CUDA_TRY(cudaEventRecord(L->ev_yfree[b], L->s_d2h));
+  if (!overlapped) {
+    CUDA_TRY(cudaStreamSynchronize(L->s_d2h));
+    CUDA_TRY(cudaStreamSynchronize(st));
+  }
+  return MOE_OK;
+}
+}  // namespace
+
+moe_status_t moe_layer_forward_host(moe_layer_t* L, const void* x_host, int64_t T, void* y_host,
+                                    const moe_plan_t* plan, void* stream_v) {
+  return host_call(L, x_host, T, y_host, plan, stream_v, false);
+}
+
+moe_status_t moe_layer_forward_host_async(moe_layer_t* L, const void* x_host, int64_t T, void* y_host,
+                                          const moe_plan_t* plan, void* stream_v) {
+  return host_call(L, x_host, T, y_host, plan, stream_v, true);
+}
+
+moe_status_t moe_layer_host_sync(moe_layer_t* L, void* stream_v) {
+  if (!L) { set_error("null layer"); return MOE_ERR_INVALID; }
   CUDA_TRY(cudaStreamSynchronize(L->s_d2h));
-  CUDA_TRY(cudaStreamSynchronize(st));
+  CUDA_TRY(cudaStreamSynchronize((cudaStream_t)stream_v));
   return MOE_OK;
 }
 

@@ -125,6 +125,21 @@ class MoELayer:
                   "moe_layer_forward_host")
         return y_host
 
+    def forward_host_async(self, x_host: torch.Tensor, y_host: torch.Tensor, plan=None, stream=None) -> None:
+        """forward_host without the final wait: consecutive calls overlap their copies with the
+        previous call's compute; x_host / y_host stay owned by the layer until host_sync()."""
+        T = x_host.shape[0]
+        st = stream if stream is not None else torch.cuda.current_stream(self.device)
+        abi.check(self.lib.moe_layer_forward_host_async(self.handle, C.c_void_p(x_host.data_ptr()), T,
+                                                        C.c_void_p(y_host.data_ptr()),
+                                                        C.byref(plan) if plan is not None else None,
+                                                        C.c_void_p(st.cuda_stream)),
+                  "moe_layer_forward_host_async")
+
+    def host_sync(self, stream=None) -> None:
+        st = stream if stream is not None else torch.cuda.current_stream(self.device)
+        abi.check(self.lib.moe_layer_host_sync(self.handle, C.c_void_p(st.cuda_stream)), "moe_layer_host_sync")
+
     def set_profiling(self, on: bool = True) -> None:
         abi.check(self.lib.moe_layer_set_profiling(self.handle, 1 if on else 0), "moe_layer_set_profiling")
 

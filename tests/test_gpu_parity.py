@@ -333,3 +333,23 @@ def test_device_limited_routing_exact(E, k, G, M, H):
     assert not np.array_equal(idx, oracle.topk_gating(ref["logits"], k, 1)[0])   # the limit bites
     assert_close(to_f32(y), ref["y"], f"device-limited E{E} G{G} M{M}")
     L.close()
+
+
+def test_forward_host_async_overlapped_calls():
+    """moe_layer_forward_host_async: consecutive calls share the double-buffered
+    staging (call i+1's copies overlap call i's compute); after host_sync every
+    call's y_host equals the device-buffer forward of its x."""
+    kw, k, norm = CASES["mid_shared"]
+    inps = [Inputs(seed=60 + i, **dict(kw, T=3000)) for i in range(5)]
+    base = inps[0]
+    L = layer_from_inputs(base, k, norm, max_tokens=3000)
+    xs_h = [torch.from_numpy(np.ascontiguousarray(i.x).view(np.int16)).view(torch.bfloat16).pin_memory() for i in inps]
+    ys_h = [torch.empty_like(x) .pin_memory() for x in xs_h]
+    for xh, yh in zip(xs_h, ys_h):
+        L.forward_host_async(xh, yh)
+    L.host_sync()
+    for xh, yh in zip(xs_h, ys_h):
+        ref = L.forward(xh.cuda())
+        torch.cuda.synchronize()
+        assert torch.equal(yh, ref.cpu())
+    L.close()
