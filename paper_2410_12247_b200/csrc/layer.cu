@@ -1701,9 +1701,61 @@ moe_status_t moe_layer_calibrate(moe_layer_t* L, void* stream, moe_cost_model_t*
     np = i + 1;
   }
   m.n_points = np;
+  if (c.ep > 1) {
+    // All2all cost (dispatch channel): every rank sends `per` bytes to every
+    // peer; time vs the bytes crossing one rank gives a2a_fixed_ms + 1/a2a_gbps.
+    const int D = c.ep;
+    const int64_t cap = std::min<int64_t>(L->send_cap, L->recv_cap) * c.hidden * 2 / D;
+    std::vector<double> xs, ys;
+    for (int64_t per : {int64_t(1) << 18, int64_t(1) << 21, int64_t(1) << 23, int64_t(1) << 25}) {
+      if (per > cap) break;
+      float best = 1e30f;
+      for (int rep = 0; rep < 3; ++rep) {
+        TR_TRY(L->tr->allgather_i32(L->hist, L->ghist, 1, st));  // ranks start together
+        CUDA_TRY(cudaStreamSynchronize(st));
+        CUDA_TRY(cudaEventRecord(e0, L->s_disp));
+        TR_TRY(L->tr->group_start(0));
+        for (int peer = 0; peer < D; ++peer) {
+          TR_TRY(L->tr->send((char*)L->send + peer * per, per, peer, 0, L->s_disp));
+          TR_TRY(L->tr->recv((char*)L->recv + peer * per, per, peer, 0, L->s_disp));
+        }
+        TR_TRY(L->tr->group_end(0, L->s_disp));
+        CUDA_TRY(cudaEventRecord(e1, L->s_disp));
+        CUDA_TRY(cudaEventSynchronize(e1));
+        float ms = 0;
+        cudaEventElapsedTime(&ms, e0, e1);
+        best = std::min(best, ms);
+      }
+      xs.push_back((double)per * (D - 1));
+      ys.push_back(best);
+    }
+    if (xs.size() >= 2) {  // least squares: ms = a + x / (gbps * 1e6)
+      double sx = 0, sy = 0, sxx = 0, sxy = 0;
+      const double n = (double)xs.size();
+      for (size_t i = 0; i < xs.size(); ++i) {
+        sx += xs[i]; sy += ys[i]; sxx += xs[i] * xs[i]; sxy += xs[i] * ys[i];
+      }
+      const double slope = (n * sxy - sx * sy) / std::max(1e-30, n * sxx - sx * sx);
+      const double icpt = (sy - slope * sx) / n;
+      if (slope > 0) m.a2a_gbps = (float)(1.0 / (slope * 1e6));
+      m.a2a_fixed_ms = (float)std::max(0.002, icpt);
+      m.k_ms = 2.0f * m.a2a_fixed_ms;  // a chunk adds one dispatch and one combine group
+    }
+    // every rank must plan identically: adopt rank 0's model
+    constexpr int W = (int)(sizeof(moe_cost_model_t) / sizeof(int32_t));
+    int32_t* dev = nullptr;
+    CUDA_TRY(cudaMalloc(&dev, sizeof(int32_t) * W * (D + 1)));
+    CUDA_TRY(cudaMemcpy(dev, &m, sizeof(m), cudaMemcpyHostToDevice));
+    int ge = L->tr->allgather_i32(dev, dev + W, W, st);
+    if (!ge) {
+      CUDA_TRY(cudaStreamSynchronize(st));
+      CUDA_TRY(cudaMemcpy(&m, dev + W, sizeof(m), cudaMemcpyDeviceToHost));  // rank 0's record
+    }
+    cudaFree(dev);
+    if (ge) return (moe_status_t)ge;
+  }
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
-  (void)c;
   L->cost = m;
   if (out) *out = m;
   return MOE_OK;

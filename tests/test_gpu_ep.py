@@ -437,3 +437,51 @@ def test_forward_host_ep2_sliced():
         assert torch.equal(dev_out[r], host_out[r])
     for L in layers:
         L.close()
+
+
+def test_ep_calibration_collective_and_shared():
+    """moe_layer_calibrate at ep > 1 is collective: it measures the GEMMs and the
+    all2all (bytes vs time fit), then every rank adopts rank 0's model, so the
+    planner derives one plan everywhere; the forward with that plan is correct."""
+    D, E_loc = 4, 4
+    inp = Inputs(E=16, k=4, H=256, F=256, S=1, Fs=128, T=4000, seed=23, grid=True)
+    start = oracle.token_shards(inp.T, D)
+    group = LocalGroup(D)
+    layers = []
+    for r in range(D):
+        w = dict(w_router=dev_bf16(inp.w_router), w_gate=dev_bf16(inp.w_gate[r * E_loc:(r + 1) * E_loc]),
+                 w_up=dev_bf16(inp.w_up[r * E_loc:(r + 1) * E_loc]),
+                 w_down=dev_bf16(inp.w_down[r * E_loc:(r + 1) * E_loc]),
+                 ws_gate=dev_bf16(inp.ws_gate), ws_up=dev_bf16(inp.ws_up), ws_down=dev_bf16(inp.ws_down))
+        layers.append(MoELayer(16, 4, 256, 256, w, S=1, Fs=128, ep=D, rank=r, max_tokens=1000, norm_topk=0,
+                               local_group=group))
+    models, ys, plans, errs = [None] * D, [None] * D, [None] * D, []
+
+    def worker(r):
+        try:
+            torch.cuda.set_device(0)
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                models[r] = bytes(layers[r].calibrate(stream=s))
+                d, b = layers[r].debug_buffers(1000)
+                ys[r] = layers[r].forward(dev_bf16(inp.x[start[r]:start[r + 1]]), stream=s, debug=d)
+                s.synchronize()
+                plans[r] = bytes(b["plan_used"])
+        except Exception as e:  # pragma: no cover
+            errs.append(repr(e))
+
+    th = [threading.Thread(target=worker, args=(r,), daemon=True) for r in range(D)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=300)
+    assert not errs, errs
+    assert all(m == models[0] for m in models) and all(p == plans[0] for p in plans)
+    from paper_2410_12247_b200 import abi
+    m = abi.moe_cost_model_t.from_buffer_copy(models[0])
+    assert m.n_points >= 2 and m.a2a_gbps > 0 and m.a2a_fixed_ms > 0
+    ref = oracle.moe_layer(inp.x, inp.w_router, inp.w_gate, inp.w_up, inp.w_down, k=4, norm_topk=0,
+                           ws_gate_bits=inp.ws_gate, ws_up_bits=inp.ws_up, ws_down_bits=inp.ws_down, D=D)
+    assert_close(torch.cat(ys).float().cpu().numpy(), ref["y"], "calibrated EP4")
+    for L in layers:
+        L.close()
