@@ -245,10 +245,13 @@ moe_status_t moe_plan_pipeline(const moe_layer_t* layer, int64_t global_tokens,
                                const int32_t* global_hist, moe_plan_t* out);
 
 /* Measure the B200 cost model (GEMM time vs rows per expert for both kinds;
- * all2all time vs bytes and chunk count when ep > 1) and install it in the
- * layer.  Collective when ep > 1.  Optional; without it a built-in model
+ * all2all fixed cost and bandwidth from a time-vs-bytes fit when ep > 1, the
+ * per-chunk overhead k from the fixed cost) and install it in the layer.
+ * Collective when ep > 1: every rank ends with rank 0's model.  Optional; without it a built-in model
  * is used.  `out` (host, may be NULL) receives the model. */
 moe_status_t moe_layer_calibrate(moe_layer_t* layer, void* stream, moe_cost_model_t* out);
+/* Install a caller's model.  ep > 1: must be the same on every rank (each
+ * rank plans from its own copy; calibrate() guarantees it by adopting rank 0's). */
 moe_status_t moe_layer_set_cost_model(moe_layer_t* layer, const moe_cost_model_t* cost);
 
 /* ------------------------------------------------------------------ forward */
