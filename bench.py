@@ -60,6 +60,8 @@ def parse():
     p.add_argument("--graph", default="auto", choices=["auto", "on", "off"],
                    help="ep == 1: replay the forward as a CUDA graph (auto: batches <= 4096 tokens, where "
                         "launch gaps matter)")
+    p.add_argument("--calibrate", default="auto", choices=["auto", "on", "off"],
+                   help="measure the planner's cost model first (auto: ep > 1, where NVLink costs matter)")
     p.add_argument("--a2a", default="nccl", choices=["nccl", "p2p"],
                    help="ep > 1 all2all: NCCL send/recv, or the layer's put kernels over NVLink peer memory")
     return p.parse_args()
@@ -312,6 +314,9 @@ def ours(args, cfg):
     opts = feature_opts(args)
     layer = MoELayer(E, k, H, F, w, S=S, Fs=Fs, ep=D, rank=rank, max_tokens=T_loc, norm_topk=cfg["norm_topk"],
                      uid_dispatch=uid_d, uid_combine=uid_c, device=dev, **layer_opts(args))
+    if args.calibrate == "on" or (args.calibrate == "auto" and D > 1):
+        layer.calibrate()        # collective at ep > 1; every rank ends with rank 0's model
+        torch.cuda.synchronize()
     plan = None
     if args.chunks or args.kind != "auto" or args.sm_gemm or args.tile_m:
         kind = {"auto": MOE_GEMM_AUTO, "grouped": MOE_GEMM_GROUPED, "dense": MOE_GEMM_DENSE}[args.kind]
