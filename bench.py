@@ -343,7 +343,11 @@ def ours(args, cfg):
         torch.cuda.synchronize()
         launches_per_forward = layer.last_launches()
 
-    layer.set_profiling(not use_graph)
+    # per-stage CUDA events are recorded in the LAST timed forward only and read
+    # after the loop: querying them every step would synchronise the host each
+    # step and leave the GPU idle between forwards
+    layer.set_profiling(True)      # creates the event pool now, outside the timed region
+    layer.set_profiling(False)
     gpu_idx = local
     vis = os.environ.get("CUDA_VISIBLE_DEVICES")
     if vis:
@@ -363,23 +367,28 @@ def ours(args, cfg):
     launches = 0
     t_start = clocks.mark()
     ev0.record(stream)
-    for _ in range(args.steps):
+    for i in range(args.steps):
         if use_graph:
             graph.replay()
             launches += launches_per_forward
             continue
+        if i == args.steps - 1:
+            layer.set_profiling(True)
         layer.forward(x, y, plan=plan)
         launches += layer.last_launches()
-        for name, (ms, cnt) in layer.stage_ms().items():
-            stage_sum[name] = stage_sum.get(name, 0.0) + ms
-            stage_cnt[name] = stage_cnt.get(name, 0) + cnt
     ev1.record(stream)
     torch.cuda.synchronize()
     t_end = clocks.mark()
     if D > 1:
         dist.barrier()
     clk = clocks.stop(t_start, t_end)
-    if use_graph:  # stage timings from eager forwards (informational)
+    stages_src = "last timed forward"
+    if not use_graph:
+        for name, (ms, cnt) in layer.stage_ms().items():
+            stage_sum[name] = ms * args.steps       # per-step averages below divide by steps
+            stage_cnt[name] = cnt * args.steps
+    else:  # events cannot be read inside a graph: profiled eager forwards after the timed region
+        stages_src = "eager forwards after the timed graph replays"
         layer.set_profiling(True)
         for _ in range(args.steps):
             layer.forward(x, y, plan=plan)
@@ -501,7 +510,7 @@ def ours(args, cfg):
                            **opts, "a2a": args.a2a if D > 1 else None, "cuda_graph": bool(use_graph),
                            "plan": plan_used},
                 "roofline": roofline, "layer_roofline": layer_roofline,
-                "exposed_a2a_ms": stages.get("exposed_a2a", 0.0), "stages_ms": stages,
+                "exposed_a2a_ms": stages.get("exposed_a2a", 0.0), "stages_ms": stages, "stages_source": stages_src,
                 "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk}
         print(json.dumps(line), flush=True)
     layer.close()
