@@ -180,6 +180,10 @@ typedef struct {
                                g = chunk*ep + rank), -1 past its group count */
   int32_t* lr_hist;         /* out [PN*ep] (local_reduce, ep > 1): send rows
                                per group g                                   */
+  int64_t* chunk_rows_host; /* out HOST [2][64][ep] (ep > 1): rows this rank
+                               sends to [0][c] / receives from [1][c] each
+                               peer in chunk c < PN (dedup rows under
+                               local_reduce)                                 */
 } moe_debug_t;
 
 /* ---------------------------------------------------------------- lifecycle */

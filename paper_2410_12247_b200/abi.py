@@ -68,7 +68,7 @@ class moe_debug_t(C.Structure):
                 ("topk_w", C.c_void_p), ("pos", C.c_void_p), ("hist", C.c_void_p),
                 ("seg_start", C.c_void_p), ("shared_out", C.c_void_p),
                 ("global_hist_host", C.c_void_p), ("plan_used", C.POINTER(moe_plan_t)),
-                ("lr_pos", C.c_void_p), ("lr_hist", C.c_void_p)]
+                ("lr_pos", C.c_void_p), ("lr_hist", C.c_void_p), ("chunk_rows_host", C.c_void_p)]
 
 
 _SIGS = {

@@ -1414,6 +1414,25 @@ moe_status_t fwd_ep(Fwd& F) {
   else
     KERNEL_TRY(launch_combine(L->comb, L->SF ? L->s : nullptr, (int)T, H, k, L->pos, topk_w, y, st));
   prof_mark(L, MOE_STAGE_COMBINE, c0, prof_rec(L, st));
+  if (dbg && dbg->chunk_rows_host) {
+    for (int ch = 0; ch < plan.num_chunks; ++ch) {
+      const int sl = ch % S, g0 = plan.group_begin[ch / S], g1 = plan.group_begin[ch / S + 1];
+      for (int peer = 0; peer < D; ++peer) {
+        int64_t sent = 0, got = 0;
+        if (lr_ep) {
+          sent = ug[(size_t)me * G + ch * D + peer];
+          got = ug[(size_t)peer * G + ch * D + me];
+        } else {
+          for (int el = g0; el < g1; ++el) {
+            sent += cnt(me, peer * E_loc + el, sl);
+            got += cnt(peer, me * E_loc + el, sl);
+          }
+        }
+        dbg->chunk_rows_host[(size_t)ch * D + peer] = sent;
+        dbg->chunk_rows_host[((size_t)MOE_MAX_CHUNKS + ch) * D + peer] = got;
+      }
+    }
+  }
   if (dbg && lr_ep) {
     if (dbg->lr_pos) CUDA_TRY(cudaMemcpyAsync(dbg->lr_pos, L->posg, sizeof(int32_t) * T * k, cudaMemcpyDeviceToDevice, st));
     if (dbg->lr_hist) CUDA_TRY(cudaMemcpyAsync(dbg->lr_hist, L->u_hist, sizeof(int32_t) * G, cudaMemcpyDeviceToDevice, st));

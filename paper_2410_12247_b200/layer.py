@@ -174,11 +174,13 @@ class MoELayer:
         import numpy as np
         ghist = np.zeros((self.ep, self.E), dtype=np.int32)
         plan_used = abi.moe_plan_t()
+        chunk_rows = np.full((2, abi.MOE_MAX_CHUNKS, self.ep), -1, dtype=np.int64)
         d = abi.moe_debug_t(1 if override is not None else 0,
                             *[_ptr(bufs[n]) for n in ("logits", "topk_idx", "topk_w", "pos", "hist",
                                                        "seg_start", "shared_out")],
                             ghist.ctypes.data_as(C.c_void_p), C.pointer(plan_used),
-                            _ptr(bufs["lr_pos"]), _ptr(bufs["lr_hist"]))
+                            _ptr(bufs["lr_pos"]), _ptr(bufs["lr_hist"]), chunk_rows.ctypes.data_as(C.c_void_p))
+        bufs["chunk_rows"] = chunk_rows
         bufs["global_hist"] = ghist
         bufs["plan_used"] = plan_used
         bufs["_struct"] = d

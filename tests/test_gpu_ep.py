@@ -103,6 +103,10 @@ def test_ep_equals_ep1_and_oracle(D, N, kind, tile_m):
         # SM partition (NEXT-1): the GEMM grid leaves 2 x comm_ctas SMs to the all2all
         pu = bufs[r]["plan_used"]
         assert pu.comm_ctas == 8 and pu.sm_gemm == torch.cuda.get_device_properties(0).multi_processor_count - 16
+        # per-(chunk, peer) rows sent / received == the oracle's all2all sizes (bit-exact ints)
+        cr = bufs[r]["chunk_rows"]
+        assert np.array_equal(cr[0, :N], ref["send_counts"][:, r, :])
+        assert np.array_equal(cr[1, :N], ref["send_counts"][:, :, r])
     assert_close(y, ref["y"], f"EP{D} N{N}")
 
 
@@ -165,6 +169,9 @@ def test_local_reduce_ep_vs_oracle(D, N, kind, tile_m):
     for r in range(D):
         assert np.array_equal(bufs[r]["lr_hist"].cpu().numpy()[:N * D], lay["u_hist"][r])
         assert np.array_equal(bufs[r]["lr_pos"].cpu().numpy(), lay["posg"][r])
+        cr = bufs[r]["chunk_rows"]   # dedup rows per (chunk, peer), both directions
+        assert np.array_equal(cr[0, :N], lay["u_hist"][r].reshape(N, D))
+        assert np.array_equal(cr[1, :N], lay["u_hist"][:, [c * D + r for c in range(N)]].T)
     if N < 16 // D:                                 # groups of >1 expert: the dedup saved rows
         assert lay["u_hist"].sum() < 997 * 4
     else:                                           # one expert per group: one row per pair
@@ -266,6 +273,11 @@ def test_token_sliced_chunks_equal_unchunked(E, k, D, N, S, fp8):
                            ws_gate_bits=inp.ws_gate, ws_up_bits=inp.ws_up, ws_down_bits=inp.ws_down, D=D, N=N,
                            token_slices=S, dispatch_fp8=fp8)
     assert_close(y, ref["y"], f"sliced EP{D} N{N} S{S}")
+    same = (ref["idx"] == np.concatenate([b["topk_idx"].cpu().numpy() for b in bufs])).all(axis=1)
+    if same.all():  # grid routing: the per-(slice chunk, peer) sizes are the oracle's, bit for bit
+        for r in range(D):
+            assert np.array_equal(bufs[r]["chunk_rows"][0, :N * S], ref["send_counts"][:, r, :])
+            assert np.array_equal(bufs[r]["chunk_rows"][1, :N * S], ref["send_counts"][:, :, r])
 
 
 def test_ep_stage_profiling_and_exposed_a2a():
