@@ -5,7 +5,7 @@ Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s cpu_baseline /
 CUDA path (``paper_2410_12247_b200/``) and never imports it.
 
 Citations: ``P:n`` = line n of the paper's LaTeX (arXiv 2410.12247, PAPER.md);
-readings ``R1..R14`` are listed in DESIGN.md §3.
+readings ``R1..R17`` are listed in DESIGN.md §3.
 
 EPS-MoE is an exact *schedule* (P:221-222): it computes the plain MoE
 layer
@@ -33,7 +33,11 @@ Library primitives used as steps: numpy matmul (fp64) and exp.
 Pins (tests/test_oracle_pins.py): brute force per token, dense-MLP special case
 vs torch fp64, exact-logit grid, tie fixture, k=E, activated-experts formula
 (P:133), the fig:eps_overview worked example, conservation,
-chunked == unchunked, EP=D == EP=1.
+chunked == unchunked, EP=D == EP=1; FP8 codec vs the e4m3 format definition;
+LocalReduce (R16): the worked example's dedup counts by hand, exact-mode
+regrouping identity, single-group special case, the hypergeometric
+distinct-rank closed form; device-limited routing (R17): a hand fixture, the
+M = groups special case; the P:265 all2all volume bounds.
 """
 from __future__ import annotations
 
