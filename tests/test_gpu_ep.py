@@ -497,3 +497,51 @@ def test_ep_calibration_collective_and_shared():
     assert_close(torch.cat(ys).float().cpu().numpy(), ref["y"], "calibrated EP4")
     for L in layers:
         L.close()
+
+
+@pytest.mark.parametrize("p2p", [False, True])
+def test_ep_ranks_with_no_tokens(p2p):
+    """Ragged extreme: T = 3 over 4 ranks (one rank has no tokens, the others one
+    each) and T = 0 everywhere; both all2all planes; y == EP 1 bit for bit."""
+    D, E_loc = 4, 4
+    for T in (3, 0):
+        inp = Inputs(E=16, k=4, H=256, F=256, S=1, Fs=128, T=max(T, 1), seed=31, grid=True)
+        x_all = inp.x[:T]
+        start = oracle.token_shards(T, D)
+        group = LocalGroup(D)
+        layers = []
+        for r in range(D):
+            w = dict(w_router=dev_bf16(inp.w_router), w_gate=dev_bf16(inp.w_gate[r * E_loc:(r + 1) * E_loc]),
+                     w_up=dev_bf16(inp.w_up[r * E_loc:(r + 1) * E_loc]),
+                     w_down=dev_bf16(inp.w_down[r * E_loc:(r + 1) * E_loc]),
+                     ws_gate=dev_bf16(inp.ws_gate), ws_up=dev_bf16(inp.ws_up), ws_down=dev_bf16(inp.ws_down))
+            layers.append(MoELayer(16, 4, 256, 256, w, S=1, Fs=128, ep=D, rank=r, max_tokens=4, norm_topk=0,
+                                   local_group=group, a2a_p2p=p2p))
+        ys, errs = [None] * D, []
+
+        def worker(r):
+            try:
+                torch.cuda.set_device(0)
+                s = torch.cuda.Stream()
+                with torch.cuda.stream(s):
+                    x = dev_bf16(x_all[start[r]:start[r + 1]]) if start[r + 1] > start[r] else \
+                        torch.empty(0, 256, dtype=torch.bfloat16, device="cuda")
+                    ys[r] = layers[r].forward(x, plan=make_plan(2, MOE_GEMM_GROUPED), stream=s)
+                    s.synchronize()
+            except Exception as e:  # pragma: no cover
+                errs.append(repr(e))
+
+        th = [threading.Thread(target=worker, args=(r,), daemon=True) for r in range(D)]
+        for t in th:
+            t.start()
+        for t in th:
+            t.join(timeout=120)
+        assert not errs, errs
+        y = torch.cat(ys).float().cpu().numpy()
+        assert y.shape == (T, 256)
+        if T:
+            ref = oracle.moe_layer(x_all, inp.w_router, inp.w_gate, inp.w_up, inp.w_down, k=4, norm_topk=0,
+                                   ws_gate_bits=inp.ws_gate, ws_up_bits=inp.ws_up, ws_down_bits=inp.ws_down, D=D)
+            assert_close(y, ref["y"], f"T={T} p2p={p2p}")
+        for L in layers:
+            L.close()
