@@ -312,7 +312,8 @@ def ours(args, cfg):
         dist.broadcast_object_list(ids, src=0)
         uid_d, uid_c = ids
     opts = feature_opts(args)
-    layer = MoELayer(E, k, H, F, w, S=S, Fs=Fs, ep=D, rank=rank, max_tokens=T_loc, norm_topk=cfg["norm_topk"],
+    layer = MoELayer(E, k, H, F, w, S=S, Fs=Fs, ep=D, rank=rank, max_tokens=int(np.diff(starts).max()),
+                     norm_topk=cfg["norm_topk"],
                      uid_dispatch=uid_d, uid_combine=uid_c, device=dev, **layer_opts(args))
     if args.calibrate == "on" or (args.calibrate == "auto" and D > 1):
         layer.calibrate()        # collective at ep > 1; every rank ends with rank 0's model

@@ -65,7 +65,10 @@ typedef struct {
   int32_t shared_ffn;   /* width of each shared expert                        */
   int32_t ep;           /* ep: expert-parallel degree = ranks */
   int32_t rank;         /* this rank, 0 <= rank < ep                          */
-  int64_t max_tokens;   /* capacity: largest T_loc per forward (sizes workspace) */
+  int64_t max_tokens;   /* capacity: the largest T_loc of ANY rank in any forward
+                           (identical on every rank; sizes the workspace: a
+                           rank receives up to ep * max_tokens * min(topk,
+                           E_loc) rows)                                      */
   int32_t norm_topk;    /* 1: renormalise the top-k weights (Mixtral); 0: raw
                            softmax probabilities (DeepSeek)             (R1)  */
   float routed_scale;   /* multiplies routed weights (1.0)                    */

@@ -563,20 +563,20 @@ static moe_status_t create_impl(const moe_config_t* cfg, const moe_weights_t* w,
         return fail(MOE_ERR_NCCL);
       }
       // every rank must agree on the shape (MOE_ERR_MISMATCH)
-      int32_t sig[8] = {cfg->num_experts, cfg->top_k, cfg->hidden, cfg->ffn, cfg->num_shared, cfg->shared_ffn,
+      int32_t sig[9] = {cfg->num_experts, cfg->top_k, cfg->hidden, cfg->ffn, cfg->num_shared, cfg->shared_ffn,
                         cfg->norm_topk | (cfg->dispatch_fp8 << 1) | (cfg->local_reduce << 2) |
                             (cfg->route_groups << 3) | (cfg->route_topk_groups << 9) | (cfg->a2a_p2p << 15),
-                        (int32_t)(cfg->routed_scale * 1e6f)};
+                        (int32_t)(cfg->routed_scale * 1e6f), (int32_t)cfg->max_tokens};
       int32_t* d_sig = nullptr;
       if (cudaMalloc(&d_sig, sizeof(sig) * (cfg->ep + 1)) != cudaSuccess) return fail(MOE_ERR_CUDA);
       cudaMemcpy(d_sig, sig, sizeof(sig), cudaMemcpyHostToDevice);
-      int r3 = L->tr->allgather_i32(d_sig, d_sig + 8, 8, 0);
-      std::vector<int32_t> all(8 * cfg->ep);
-      cudaMemcpy(all.data(), d_sig + 8, sizeof(int32_t) * 8 * cfg->ep, cudaMemcpyDeviceToHost);
+      int r3 = L->tr->allgather_i32(d_sig, d_sig + 9, 9, 0);
+      std::vector<int32_t> all(9 * cfg->ep);
+      cudaMemcpy(all.data(), d_sig + 9, sizeof(int32_t) * 9 * cfg->ep, cudaMemcpyDeviceToHost);
       cudaFree(d_sig);
       if (r3) return fail((moe_status_t)r3);
       for (int r = 0; r < cfg->ep; ++r)
-        if (std::memcmp(all.data() + 8 * r, sig, sizeof(sig)) != 0) {
+        if (std::memcmp(all.data() + 9 * r, sig, sizeof(sig)) != 0) {
           set_error("config mismatch across ranks");
           return fail(MOE_ERR_MISMATCH);
         }

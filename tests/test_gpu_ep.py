@@ -37,7 +37,8 @@ def _ep_forward(inp, k, norm, D, plan=None, skew_bias=None, fp8=False, lr=False,
         if skew_bias is not None:
             w["router_bias"] = torch.from_numpy(skew_bias).cuda()
         T_loc = int(start[r + 1] - start[r])
-        layers.append(MoELayer(E, k, H, F, w, S=inp.S, Fs=inp.Fs, ep=D, rank=r, max_tokens=max(T_loc, 1),
+        T_max = int(np.diff(start).max())   # capacity: the largest T_loc of any rank
+        layers.append(MoELayer(E, k, H, F, w, S=inp.S, Fs=inp.Fs, ep=D, rank=r, max_tokens=max(T_max, 1),
                                norm_topk=norm, local_group=group, dispatch_fp8=fp8, local_reduce=lr,
                                a2a_p2p=p2p))
         xs.append(dev_bf16(inp.x[start[r]:start[r + 1]]))

@@ -134,7 +134,7 @@ def test_full_size_ep8_on_one_gpu(name, skew, fp8):
             wr = {n: t for n, t in w.items() if n not in ("w_gate", "w_up", "w_down")}
             for n in ("w_gate", "w_up", "w_down"):
                 wr[n] = w[n][r * E_loc:(r + 1) * E_loc]
-            layers.append(MoELayer(E, k, H, F, wr, S=S, Fs=Fs, ep=D, rank=r, max_tokens=int(start[r + 1] - start[r]),
+            layers.append(MoELayer(E, k, H, F, wr, S=S, Fs=Fs, ep=D, rank=r, max_tokens=int(np.diff(start).max()),
                                    norm_topk=norm, local_group=group, a2a_p2p=p2p, dispatch_fp8=fp8))
         ys, plans, errs = [None] * D, [None] * D, []
 
