@@ -91,3 +91,65 @@ def test_fuzz_layer_vs_oracle(seed):
     assert_close(y, ref["y"], f"seed {seed}: D{D} E{E} k{k} H{H} F{F} S{S} T{T} {o}")
     for L in layers:
         L.close()
+
+
+@pytest.mark.parametrize("seed", list(range(30)))
+def test_fuzz_plans_vs_oracle(seed):
+    """Random explicit plans on random configurations: expert-group chunk
+    counts, token slices (ep > 1, not with LocalReduce), GEMM kind, tile rows;
+    y vs the oracle simulating the same (D, N, slices)."""
+    D, E, k, H, F, S, T, o = _case(5000 + seed)
+    rng = np.random.default_rng(9000 + seed)
+    E_loc = E // D
+    NG = int(rng.integers(1, E_loc + 1))
+    SL = int(rng.integers(1, 4)) if (D > 1 and not o["lr"] and NG * 3 <= 64) else 1
+    kind = int(rng.choice([1, 2]))
+    tile_m = int(rng.choice([0, 128, 256]))
+    inp = Inputs(E=E, k=k, H=H, F=F, S=min(S, 1), Fs=128 * S if S else 0, T=T, seed=seed + 77, grid=True)
+    bias = router_skew_bias(E, o["skew"]) if o["skew"] else None
+    rg = dict(route_groups=o.get("route_groups", 0), route_topk_groups=o.get("route_topk_groups", 0))
+    ref = oracle.moe_layer(inp.x, inp.w_router, inp.w_gate, inp.w_up, inp.w_down, k=k, norm_topk=o["norm"],
+                           ws_gate_bits=inp.ws_gate if inp.S else None, ws_up_bits=inp.ws_up if inp.S else None,
+                           ws_down_bits=inp.ws_down if inp.S else None, router_bias=bias, D=D, N=NG,
+                           token_slices=SL, dispatch_fp8=o["fp8"], local_reduce=o["lr"], **rg)
+    start = oracle.token_shards(T, D)
+    T_max = max(int(np.diff(start).max()), 1)
+    group = LocalGroup(D) if D > 1 else None
+    layers, xs = [], []
+    for r in range(D):
+        w = dict(w_router=dev_bf16(inp.w_router), w_gate=dev_bf16(inp.w_gate[r * E_loc:(r + 1) * E_loc]),
+                 w_up=dev_bf16(inp.w_up[r * E_loc:(r + 1) * E_loc]),
+                 w_down=dev_bf16(inp.w_down[r * E_loc:(r + 1) * E_loc]))
+        if inp.S:
+            w.update(ws_gate=dev_bf16(inp.ws_gate), ws_up=dev_bf16(inp.ws_up), ws_down=dev_bf16(inp.ws_down))
+        if bias is not None:
+            w["router_bias"] = torch.from_numpy(bias).cuda()
+        layers.append(MoELayer(E, k, H, F, w, S=inp.S, Fs=inp.Fs, ep=D, rank=r, max_tokens=T_max,
+                               norm_topk=o["norm"], dispatch_fp8=o["fp8"], local_reduce=o["lr"], local_group=group,
+                               a2a_p2p=o["p2p"], **rg))
+        T_loc = int(start[r + 1] - start[r])
+        xs.append(dev_bf16(inp.x[start[r]:start[r + 1]]) if T_loc else
+                  torch.empty(0, H, dtype=torch.bfloat16, device="cuda"))
+    ys, errs = [None] * D, []
+    plan = make_plan(NG * SL, kind, tile_m=tile_m, token_slices=SL)
+
+    def worker(r):
+        try:
+            torch.cuda.set_device(0)
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                ys[r] = layers[r].forward(xs[r], plan=plan, stream=s)
+                s.synchronize()
+        except Exception as e:  # pragma: no cover
+            errs.append(repr(e))
+
+    th = [threading.Thread(target=worker, args=(r,), daemon=True) for r in range(D)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=120)
+    desc = f"seed {seed}: D{D} E{E} k{k} H{H} F{F} S{S} T{T} NG{NG} SL{SL} kind{kind} tile{tile_m} {o}"
+    assert not errs, (errs, desc)
+    assert_close(torch.cat(ys).float().cpu().numpy(), ref["y"], desc)
+    for L in layers:
+        L.close()
