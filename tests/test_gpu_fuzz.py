@@ -153,3 +153,48 @@ def test_fuzz_plans_vs_oracle(seed):
     assert_close(torch.cat(ys).float().cpu().numpy(), ref["y"], desc)
     for L in layers:
         L.close()
+
+
+@pytest.mark.parametrize("p2p", [False, True])
+def test_worst_case_concentration(p2p):
+    """Every token of every rank routes to the same k experts on one rank (the
+    capacity bound D * max_tokens * min(k, E_loc) is met exactly there)."""
+    D, E, k, H, F, T = 4, 16, 4, 128, 128, 803
+    inp = Inputs(E=E, k=k, H=H, F=F, T=T, seed=3, grid=True)
+    bias = np.full(E, -1000.0, np.float32)
+    bias[4:8] = 0.0                                   # experts 4..7 = all of rank 1's experts
+    ref = oracle.moe_layer(inp.x, inp.w_router, inp.w_gate, inp.w_up, inp.w_down, k=k, norm_topk=1,
+                           router_bias=bias, D=D)
+    assert (np.sort(ref["idx"], axis=1) == np.arange(4, 8)).all()
+    start = oracle.token_shards(T, D)
+    T_max = int(np.diff(start).max())
+    group = LocalGroup(D)
+    layers, xs = [], []
+    for r in range(D):
+        w = dict(w_router=dev_bf16(inp.w_router), w_gate=dev_bf16(inp.w_gate[r * 4:(r + 1) * 4]),
+                 w_up=dev_bf16(inp.w_up[r * 4:(r + 1) * 4]), w_down=dev_bf16(inp.w_down[r * 4:(r + 1) * 4]),
+                 router_bias=torch.from_numpy(bias).cuda())
+        layers.append(MoELayer(E, k, H, F, w, ep=D, rank=r, max_tokens=T_max, norm_topk=1, local_group=group,
+                               a2a_p2p=p2p))
+        xs.append(dev_bf16(inp.x[start[r]:start[r + 1]]))
+    ys, errs = [None] * D, []
+
+    def worker(r):
+        try:
+            torch.cuda.set_device(0)
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                ys[r] = layers[r].forward(xs[r], stream=s)
+                s.synchronize()
+        except Exception as e:  # pragma: no cover
+            errs.append(repr(e))
+
+    th = [threading.Thread(target=worker, args=(r,), daemon=True) for r in range(D)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=120)
+    assert not errs, errs
+    assert_close(torch.cat(ys).float().cpu().numpy(), ref["y"], f"concentrated p2p={p2p}")
+    for L in layers:
+        L.close()
