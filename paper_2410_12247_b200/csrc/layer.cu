@@ -79,6 +79,11 @@ struct moe_layer {
   int32_t* gslice_host = nullptr;  // pinned [ep * E * 64]
   cudaStream_t s_disp = nullptr, s_comb = nullptr;
   cudaStream_t s_side = nullptr;  // shared experts, concurrent with routing / dispatch
+  // odd chunks' ComputeMoE runs here: chunk c+1's persistent GEMMs fill the SMs
+  // chunk c's last tile wave leaves idle (EPSMOE_CHUNK_STREAMS=1: all on the caller's stream)
+  cudaStream_t s_comp2 = nullptr;
+  cudaEvent_t ev_routed = nullptr, ev_comp2 = nullptr;
+  int chunk_streams = 2;
   cudaStream_t s_h2d = nullptr, s_d2h = nullptr;  // forward_host copy streams
   static constexpr int MAX_HOST_SLICES = 8;
   cudaEvent_t ev_in[MAX_HOST_SLICES] = {}, ev_out[MAX_HOST_SLICES] = {};
@@ -218,7 +223,7 @@ size_t carve(moe_layer* L, char* base) {
   L->topk_w = cv.take<float>(T * k);
   L->pos = cv.take<int32_t>(T * k);
   L->row_token = cv.take<int32_t>(T * k);
-  L->tickets = cv.take<int32_t>(4);
+  L->tickets = cv.take<int32_t>(6);  // tile-ticket pairs: caller stream, s_side, s_comp2
   L->range_hist = cv.take<int32_t>(E * R);
   L->range_off = cv.take<int32_t>(E * R);
   L->hist = cv.take<int32_t>(MOE_MAX_EXPERTS + 1);
@@ -322,7 +327,7 @@ int compute_moe(moe_layer* L, const void* A, int64_t a_rows, const int32_t* row_
   g1a.cta_pair = cta_pair;
   g1a.A = A;
   g1a.a_row_index = a_row_index;
-  g1a.tile_counter = L->tickets;
+  g1a.tile_counter = (st == L->s_comp2) ? L->tickets + 4 : L->tickets;
   g1a.a_rows = a_rows;
   g1a.B0 = L->w.w_gate;
   g1a.B1 = L->w.w_up;
@@ -341,7 +346,7 @@ int compute_moe(moe_layer* L, const void* A, int64_t a_rows, const int32_t* row_
   g2a.nsig = down_nsig;
   g2a.sig_epoch = down_epoch;
   g2a.cta_pair = cta_pair;
-  g2a.tile_counter = L->tickets;
+  g2a.tile_counter = g1a.tile_counter;
   g2a.A = L->h;
   g2a.a_rows = L->gemm_rows_cap;
   g2a.B0 = L->w.w_down;
@@ -460,7 +465,7 @@ static moe_status_t create_impl(const moe_config_t* cfg, const moe_weights_t* w,
   char* base = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(workspace) + ALIGN - 1) & ~(uintptr_t)(ALIGN - 1));
   carve(L, base);
   L->ws_base = base;
-  if (cudaMemset(L->tickets, 0, 4 * sizeof(int32_t)) != cudaSuccess ||
+  if (cudaMemset(L->tickets, 0, 6 * sizeof(int32_t)) != cudaSuccess ||
       (L->p2p_flags && (cudaMemset(L->p2p_flags, 0, sizeof(uint32_t) * 2 * MOE_MAX_CHUNKS * cfg->ep) != cudaSuccess ||
                         cudaMemset(L->p2p_done, 0, sizeof(uint32_t) * 2 * MOE_MAX_CHUNKS) != cudaSuccess))) {
     set_error("workspace memset failed");
@@ -518,6 +523,13 @@ static moe_status_t create_impl(const moe_config_t* cfg, const moe_weights_t* w,
       set_error("event creation failed");
       return fail(MOE_ERR_CUDA);
     }
+  if (const char* cs = std::getenv("EPSMOE_CHUNK_STREAMS")) L->chunk_streams = std::max(1, std::min(2, std::atoi(cs)));
+  if (cudaStreamCreateWithFlags(&L->s_comp2, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&L->ev_routed, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&L->ev_comp2, cudaEventDisableTiming) != cudaSuccess) {
+    set_error("stream creation failed");
+    return fail(MOE_ERR_CUDA);
+  }
   if (cudaStreamCreateWithFlags(&L->s_side, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreateWithFlags(&L->ev_router, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&L->ev_shared, cudaEventDisableTiming) != cudaSuccess) {
@@ -607,6 +619,9 @@ moe_status_t moe_layer_destroy(moe_layer_t* L) {
   delete L->tr;
   if (L->s_disp) cudaStreamDestroy(L->s_disp);
   if (L->s_side) cudaStreamDestroy(L->s_side);
+  if (L->s_comp2) cudaStreamDestroy(L->s_comp2);
+  for (cudaEvent_t e : {L->ev_routed, L->ev_comp2})
+    if (e) cudaEventDestroy(e);
   if (L->s_h2d) cudaStreamDestroy(L->s_h2d);
   if (L->s_d2h) cudaStreamDestroy(L->s_d2h);
   for (int i = 0; i < moe_layer::MAX_HOST_SLICES; ++i) {
@@ -904,8 +919,14 @@ moe_status_t fwd_local(Fwd& F) {
   // ---- EP = 1: no all2all; every chunk is local (C = 0 => PN = 1 is optimal)
   if (!plan_in) plan_compute(c, L->cost, T, nullptr, &plan);
   if (side) CUDA_TRY(cudaStreamWaitEvent(st, L->ev_shared, 0));
+  const bool two = L->chunk_streams > 1 && plan.num_chunks > 1 && T > 0;
+  if (two) {  // odd chunks on s_comp2 (after the routing on st)
+    CUDA_TRY(cudaEventRecord(L->ev_routed, st));
+    CUDA_TRY(cudaStreamWaitEvent(L->s_comp2, L->ev_routed, 0));
+  }
   for (int ch = 0; T > 0 && ch < plan.num_chunks; ++ch) {
     int g0 = plan.group_begin[ch], g1 = plan.group_begin[ch + 1];
+    cudaStream_t cs = (two && (ch & 1)) ? L->s_comp2 : st;
     // maximal runs of equal kind inside the chunk
     int a = g0;
     while (a < g1) {
@@ -913,10 +934,14 @@ moe_status_t fwd_local(Fwd& F) {
       while (b < g1 && plan.expert_kind[b] == plan.expert_kind[a]) ++b;
       int err = compute_moe(L, gather ? x : L->send, gather ? T : L->send_cap, L->seg_start, L->hist, a, b,
                             plan.expert_kind[a], num_ctas, pick_cta_pair(plan, (double)T * k / E),
-                            (double)T * k / E, st, gather ? L->row_token : nullptr);
+                            (double)T * k / E, cs, gather ? L->row_token : nullptr);
       if (err) { set_error(std::string("ComputeMoE: ") + cudaGetErrorString((cudaError_t)err)); return MOE_ERR_CUDA; }
       a = b;
     }
+  }
+  if (two) {
+    CUDA_TRY(cudaEventRecord(L->ev_comp2, L->s_comp2));
+    CUDA_TRY(cudaStreamWaitEvent(st, L->ev_comp2, 0));
   }
   int c0 = prof_rec(L, st);
   if (fuse == 2) {
@@ -1344,17 +1369,22 @@ moe_status_t fwd_ep(Fwd& F) {
     prof_mark(L, MOE_STAGE_COMB_A2A, b0, prof_rec(L, L->s_comb));
     return MOE_OK;
   };
+  // odd chunks compute on s_comp2, so a chunk's GEMMs fill the SMs the previous
+  // chunk's last tile wave leaves idle (ordering comes from the dispatch event;
+  // the final combine waits for every chunk through the combine stream)
+  const bool two = L->chunk_streams > 1 && plan.num_chunks > 1;
   auto compute = [&](int ch) -> moe_status_t {
     const int sl = ch % S, g0 = plan.group_begin[ch / S], g1 = plan.group_begin[ch / S + 1];
-    CUDA_TRY(cudaStreamWaitEvent(st, L->ev_disp[ch], 0));  // (p2p: my puts read `send`)
+    cudaStream_t cs = (two && (ch & 1)) ? L->s_comp2 : st;
+    CUDA_TRY(cudaStreamWaitEvent(cs, L->ev_disp[ch], 0));  // (p2p: my puts read `send`)
     if (p2p) {  // every source's rows
-      TR_TRY(L->tr->p2p_before_wait(ch, 1, st));
-      KERNEL_TRY(launch_p2p_wait(L->p2p_flags + (size_t)ch * D, D, epoch, st));
+      TR_TRY(L->tr->p2p_before_wait(ch, 1, cs));
+      KERNEL_TRY(launch_p2p_wait(L->p2p_flags + (size_t)ch * D, D, epoch, cs));
     }
     const int64_t u0 = urecv[(size_t)ch * D], u1 = urecv[(size_t)(ch + 1) * D];
     if (lr_ep) {  // unique rows -> expert-major GEMM rows (R6 order, so the GEMMs are unchanged)
       KERNEL_TRY(launch_lr_expand(L->recvu, fp8 ? L->recvq : nullptr, L->qpitch, u0, u1, H, k, D, ch, L->lr_usrc_d,
-                                  L->lr_recv_off_d, L->meta_recv, L->recv, st));
+                                  L->lr_recv_off_d, L->meta_recv, L->recv, cs));
     } else if (fp8) {  // the chunk's rows: one range per expert, merged where contiguous (all, if S == 1)
       int el = g0;
       while (el < g1) {
@@ -1362,7 +1392,7 @@ moe_status_t fwd_ep(Fwd& F) {
         int64_t r1 = rpos(el, sl, D - 1) + cnt(D - 1, me * E_loc + el, sl);
         while (++el < g1 && rpos(el, sl, 0) == r1) r1 = rpos(el, sl, D - 1) + cnt(D - 1, me * E_loc + el, sl);
         KERNEL_TRY(launch_dequant_rows(drecv + r0 * drow, r1 - r0, H, L->qpitch, (char*)L->recv + r0 * row_bytes,
-                                       st));
+                                       cs));
       }
     }
     int a = g0;
@@ -1375,7 +1405,7 @@ moe_status_t fwd_ep(Fwd& F) {
       const size_t cslot = (size_t)MOE_MAX_CHUNKS + ch;
       int err = compute_moe(
           L, L->recv, L->recv_cap, L->recv_start_d + ch * E_loc, L->recv_count_d + ch * E_loc, a, b,
-          plan.expert_kind[a], num_ctas, pick_cta_pair(plan, rows / (b - a)), rows / (b - a), st, nullptr,
+          plan.expert_kind[a], num_ctas, pick_cta_pair(plan, rows / (b - a)), rows / (b - a), cs, nullptr,
           fz ? reinterpret_cast<const GemmRowSeg*>(L->p2p_tab + P2P_SEGS_BYTES + P2P_PRE_BYTES + p2p_fptr_bytes(D)) +
                    (size_t)ch * moe_layer::P2P_MAXS
              : nullptr,
@@ -1386,9 +1416,9 @@ moe_status_t fwd_ep(Fwd& F) {
       a = b;
     }
     // LocalReduce: the chunk's partial per unique row, in place of its x row
-    if (lr_ep) KERNEL_TRY(launch_lr_reduce(L->o, L->meta_recv, u0, u1, H, k, L->recvu, st));
-    if (p2p && fuse_comb[ch]) TR_TRY(L->tr->p2p_after_put(MOE_MAX_CHUNKS + ch, st));  // combine rows are out
-    CUDA_TRY(cudaEventRecord(L->ev_gemm[ch], st));
+    if (lr_ep) KERNEL_TRY(launch_lr_reduce(L->o, L->meta_recv, u0, u1, H, k, L->recvu, cs));
+    if (p2p && fuse_comb[ch]) TR_TRY(L->tr->p2p_after_put(MOE_MAX_CHUNKS + ch, cs));  // combine rows are out
+    CUDA_TRY(cudaEventRecord(L->ev_gemm[ch], cs));
     return MOE_OK;
   };
   // Algorithm 1 issue order
