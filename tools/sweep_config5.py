@@ -36,6 +36,7 @@ def main():
     ap.add_argument("--chunks", default="1,2,3,4,5,6,7,8")
     ap.add_argument("--kinds", default="grouped,dense,auto")
     ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--rounds", type=int, default=3, help="interleaved repetitions (median reported)")
     ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r01_config5_sweep.md"))
     ap.add_argument("--sm-sweep", action="store_true",
                     help="Table IV analog (P:467-490): layer ms vs GEMM SM budget for several token counts")
@@ -75,10 +76,15 @@ def main():
         hist = b["hist"].cpu().numpy()
         skew_stats = dict(max_over_mean=float(hist.max() / hist.mean()), zero_experts=int((hist == 0).sum()))
         auto_plan = L.plan(T, hist[None, :])
-        for kind in a.kinds.split(","):
-            for n in [int(v) for v in a.chunks.split(",")]:
-                if kind == "auto" and n != 1:
-                    continue
+        points = [(kind, n) for kind in a.kinds.split(",") for n in [int(v) for v in a.chunks.split(",")]
+                  if not (kind == "auto" and n != 1)]
+        # interleaved rounds in a shuffled order, median per point: a sequential sweep
+        # on a power-capped GPU drifts (later points run hotter) and biases the ranking
+        times = {p: [] for p in points}
+        rng = np.random.default_rng(0)
+        for rnd in range(a.rounds):
+            for i in rng.permutation(len(points)):
+                kind, n = points[i]
                 plan = None if kind == "auto" else make_plan(n, KINDS[kind])
                 for _ in range(2):
                     L.forward(x, plan=plan)
@@ -89,14 +95,18 @@ def main():
                     L.forward(x, plan=plan)
                 e1.record()
                 torch.cuda.synchronize()
-                ms = e0.elapsed_time(e1) / a.steps
-                r = dict(config=a.config, skew=s, kind=kind, chunks=n, ms=ms, tokens_per_s=T / ms * 1e3,
-                         launches=L.last_launches(), **skew_stats)
-                if kind == "auto":
-                    r["auto_kinds"] = {"grouped": int(sum(1 for e in range(E) if auto_plan.expert_kind[e] == 1)),
-                                       "dense": int(sum(1 for e in range(E) if auto_plan.expert_kind[e] == 2))}
-                rows.append(r)
-                print(json.dumps(r), flush=True)
+                times[(kind, n)].append(e0.elapsed_time(e1) / a.steps)
+        for kind, n in points:
+            plan = None if kind == "auto" else make_plan(n, KINDS[kind])
+            L.forward(x, plan=plan)
+            ms = float(np.median(times[(kind, n)]))
+            r = dict(config=a.config, skew=s, kind=kind, chunks=n, ms=ms, ms_rounds=times[(kind, n)],
+                     tokens_per_s=T / ms * 1e3, launches=L.last_launches(), **skew_stats)
+            if kind == "auto":
+                r["auto_kinds"] = {"grouped": int(sum(1 for e in range(E) if auto_plan.expert_kind[e] == 1)),
+                                   "dense": int(sum(1 for e in range(E) if auto_plan.expert_kind[e] == 2))}
+            rows.append(r)
+            print(json.dumps(r), flush=True)
         L.close()
     with open(a.out, "w") as f:
         f.write(f"# Config-5 sweep ({a.config}, EP=1, B200) — generated by tools/sweep_config5.py\n\n")
@@ -104,7 +114,7 @@ def main():
         f.write("| rows/expert | grouped ms | dense ms |\n|---|---|---|\n")
         for mp, g, dn in zip(calib["m_points"], calib["grouped_ms"], calib["dense_ms"]):
             f.write(f"| {mp:.0f} | {g:.4f} | {dn:.4f} |\n")
-        f.write("\n| skew s | max/mean expert load | zero-load experts | kind | chunks | ms/layer | tokens/s | launches |\n")
+        f.write("\n| skew s | max/mean expert load | zero-load experts | kind | chunks | ms/layer (median of rounds) | tokens/s | launches |\n")
         f.write("|---|---|---|---|---|---|---|---|\n")
         for r in rows:
             f.write(f"| {r['skew']} | {r['max_over_mean']:.2f} | {r['zero_experts']} | {r['kind']} | {r['chunks']} | "
