@@ -1,8 +1,10 @@
 # Round evidence refresh: GPU tests, bench lines, ncu launch list, ncu full of the expert GEMMs.
 set -x
-mkdir -p gpurun_out/r01b
-O=gpurun_out/r01b
+TAG=${1:-r01b}
+O=gpurun_out/$TAG
+mkdir -p $O
 python -m pytest tests -m gpu -q 2>&1 | tail -3 > $O/pytest_gpu.txt
+python -c 'import __graft_entry__ as g; g.smoke()' > $O/smoke.txt 2>&1
 python bench.py > $O/bench_dsv2.json 2> $O/bench_dsv2.err
 python bench.py --config mixtral > $O/bench_mixtral.json 2> $O/bench_mixtral.err
 python bench.py --config dsv2_lite > $O/bench_dsv2_lite.json 2> $O/bench_dsv2_lite.err
