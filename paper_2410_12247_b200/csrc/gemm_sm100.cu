@@ -71,7 +71,8 @@ struct KParams {
   int raster_gm;  // tile order inside a group: blocks of raster_gm m-tiles, m fastest inside a block
   int dynamic;    // 1: dynamic tile tickets (tile_counter), 0: static round robin
   int row_mode;   // 0 all rows, 1 bulk (multiple of 256), 2 remainder (see GemmArgs)
-  int diag;       // diagnostics only (EPSMOE_GEMM_DIAG): 1 skip output stores, 2 skip TMEM loads + stores
+  int diag;       // diagnostics only (EPSMOE_GEMM_DIAG): 1 skip output stores, 2 skip TMEM loads + stores,
+                  // 3 bulk stores into a 256-row window (L2-resident: same store traffic, no DRAM writes)
   int tma_store;  // bf16 outputs: full 32-row warp slices leave through TMA bulk-tensor stores (tmO)
   int64_t ldo;
   void* out;
@@ -544,7 +545,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
             pk[i] = pack_bf16(silu_f32(g0) * u0, silu_f32(g1) * u1);
           }
           store_chunk(pk, stg, out0 + c * 32, p.ldo, vr, lane, p.tma_store ? &tmO : nullptr, nt * 128 + c * 32,
-                      (int)(grow - lane));
+                      (p.diag == 3 ? (int)((grow - lane) & 255) : (int)(grow - lane)));
         }
       } else if (EPI == EPI_BF16 && p.rseg) {
         // DownGemm fused with the combine all2all: each row is stored straight
@@ -592,7 +593,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
 #pragma unroll
           for (int i = 0; i < 16; ++i) pk[i] = pack_bf16(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1]));
           store_chunk(pk, stg, out0 + c * 32, p.ldo, vr, lane, p.tma_store ? &tmO : nullptr, nt * BN + c * 32,
-                      (int)(grow - lane));
+                      (p.diag == 3 ? (int)((grow - lane) & 255) : (int)(grow - lane)));
         }
       } else if (EPI == EPI_COMBINE) {
         // s = bf16(acc) is staged row-major in smem; the weighted unpermute then
@@ -662,7 +663,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
             *sp = make_uint4(pack_bf16(a[0], a[1]), pack_bf16(a[2], a[3]), pack_bf16(a[4], a[5]),
                              pack_bf16(a[6], a[7]));
           }
-          stage_flush(stg, out0 + c * 32, p.ldo, vr, lane, p.tma_store ? &tmO : nullptr, col0, (int)(grow - lane));
+          stage_flush(stg, out0 + c * 32, p.ldo, vr, lane, p.tma_store ? &tmO : nullptr, col0, (p.diag == 3 ? (int)((grow - lane) & 255) : (int)(grow - lane)));
         }
       } else {
         float* out = reinterpret_cast<float*>(p.out) + grow * p.ldo;
