@@ -497,6 +497,36 @@ def ours(args, cfg):
            "api": "moe_layer_forward_host_async x steps + moe_layer_host_sync (pinned host x/y; calls overlap)"}
 
     stages = {n: round(v / args.steps, 4) for n, v in stage_sum.items()}
+    # ---- all2all alone: the same chunked dispatch / combine with ComputeMoE and the
+    # shared experts skipped (moe_layer_set_comm_only); hidden = 1 - exposed / alone, max over ranks
+    a2a_alone = None
+    if D > 1:
+        layer.set_comm_only(True)
+        for _ in range(2):
+            layer.forward(x, y, plan=plan)
+        torch.cuda.synchronize()
+        dist.barrier()
+        k_alone = max(3, min(args.steps, 10))
+        c_ev0, c_ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        c_ev0.record(stream)
+        for i in range(k_alone):
+            if i == k_alone - 1:
+                layer.set_profiling(True)
+            layer.forward(x, y, plan=plan)
+        c_ev1.record(stream)
+        torch.cuda.synchronize()
+        st_alone = layer.stage_ms()
+        layer.set_profiling(False)
+        layer.set_comm_only(False)
+        tc = torch.tensor([c_ev0.elapsed_time(c_ev1) / k_alone, st_alone["exposed_a2a"][0],
+                           stages.get("exposed_a2a", 0.0)], dtype=torch.float64, device=dev)
+        dist.all_reduce(tc, op=dist.ReduceOp.MAX)
+        alone_ms, exposed_max = float(tc[1].item()), float(tc[2].item())
+        a2a_alone = {"a2a_ms": alone_ms, "comm_only_ms_per_step": float(tc[0].item()), "steps": k_alone,
+                     "exposed_a2a_ms_max_rank": exposed_max,
+                     "hidden_frac": (1.0 - exposed_max / alone_ms) if alone_ms > 0 else None,
+                     "how": "moe_layer_set_comm_only: routing, plan, every chunk's dispatch/combine and the "
+                            "unpermute, no ComputeMoE / shared experts; comm intervals of the last forward"}
     cpu = None
     if rank == 0 and D == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(cfg, seed, args.skew, args.cpu_sample, opts)
@@ -511,7 +541,8 @@ def ours(args, cfg):
                            **opts, "a2a": args.a2a if D > 1 else None, "cuda_graph": bool(use_graph),
                            "plan": plan_used},
                 "roofline": roofline, "layer_roofline": layer_roofline,
-                "exposed_a2a_ms": stages.get("exposed_a2a", 0.0), "stages_ms": stages, "stages_source": stages_src,
+                "exposed_a2a_ms": stages.get("exposed_a2a", 0.0), "a2a_alone": a2a_alone,
+                "stages_ms": stages, "stages_source": stages_src,
                 "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk}
         print(json.dumps(line), flush=True)
     layer.close()

@@ -308,6 +308,18 @@ enum {
   MOE_NUM_STAGES = 10
 };
 moe_status_t moe_layer_set_profiling(moe_layer_t* layer, int32_t enable);
+/* Measurement hook for the exposed-all2all figure ("the same
+ * chunked dispatch/combine with the GEMMs replaced by no-ops"; the paper's
+ * overlap claim).  enable != 0: later forwards run routing, the
+ * count exchange, the plan, every chunk's dispatch and combine all2all (same
+ * plan, streams, events and data plane; the fused DownGemm combine becomes the
+ * put kernel) and the weighted unpermute, but skip ComputeMoE (expert GEMMs,
+ * SwiGLU, LocalReduce partials, FP8 dequantisation) and the shared experts, so
+ * y is UNDEFINED while it is set.  Collective: every rank of the EP group sets
+ * the same value between forwards.  Ignored at ep == 1 (no all2all).  Errors:
+ * MOE_ERR_INVALID for a NULL layer. */
+moe_status_t moe_layer_set_comm_only(moe_layer_t* layer, int32_t enable);
+
 /* Waits for the last forward's events; ms[MOE_NUM_STAGES] (host) in ms;
  * counts[MOE_NUM_STAGES] (host, may be NULL) = launches timed per stage. */
 moe_status_t moe_layer_stage_ms(const moe_layer_t* layer, float* ms, int32_t* counts);

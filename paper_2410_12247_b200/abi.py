@@ -97,6 +97,7 @@ _SIGS = {
     "moe_layer_host_sync": (C.c_int, [C.c_void_p, C.c_void_p]),
     "moe_layer_last_launches": (C.c_int32, [C.c_void_p]),
     "moe_layer_set_profiling": (C.c_int, [C.c_void_p, C.c_int32]),
+    "moe_layer_set_comm_only": (C.c_int, [C.c_void_p, C.c_int32]),
     "moe_layer_stage_ms": (C.c_int, [C.c_void_p, C.POINTER(C.c_float), C.POINTER(C.c_int32)]),
     "moe_last_error": (C.c_char_p, []),
     "moe_gemm_grouped": (C.c_int, [C.c_int32, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_int64,

@@ -111,6 +111,9 @@ struct moe_layer {
   epsmoe::Transport* tr = nullptr;  // all2all transport (NCCL, or in-process for tests), ep > 1
   moe_cost_model_t cost;
   int last_launches = 0;
+  // ep > 1 measurement hook (moe_layer_set_comm_only): forwards skip ComputeMoE
+  // and the shared experts, so the same chunked all2all runs alone
+  bool comm_only = false;
   // per-stage device timing (moe_layer_set_profiling)
   bool prof = false;
   std::vector<cudaEvent_t> pev;
@@ -703,6 +706,12 @@ moe_status_t moe_layer_set_profiling(moe_layer_t* L, int32_t enable) {
   return MOE_OK;
 }
 
+moe_status_t moe_layer_set_comm_only(moe_layer_t* L, int32_t enable) {
+  if (!L) return MOE_ERR_INVALID;
+  L->comm_only = enable != 0 && L->cfg.ep > 1;
+  return MOE_OK;
+}
+
 moe_status_t moe_layer_stage_ms(const moe_layer_t* L, float* ms, int32_t* counts) {
   if (!L || !ms) return MOE_ERR_INVALID;
   for (int i = 0; i < MOE_NUM_STAGES; ++i) {
@@ -854,7 +863,7 @@ moe_status_t fwd_routing(Fwd& F) {
   };
   // ep == 1: the routing kernels stream with L2 evict-first hints, so they
   // co-run with the shared GEMMs (measured ~1% faster per layer than in order).
-  const bool has_shared = L->SF && T > 0;
+  const bool has_shared = L->SF && T > 0 && !(L->comm_only && D > 1);
   // (small decode batches: the routing kernels are latency-bound and a concurrent
   // persistent GEMM only delays them, so they stay in order below 8K tokens)
   const bool side = has_shared && (D > 1 || (L->overlap_shared && T >= 8192));
@@ -1249,7 +1258,7 @@ moe_status_t fwd_ep(Fwd& F) {
         }
         p2p_nseg[dir][ch] = n;
         p2p_total[dir][ch] = pr[n];
-        if (dir == 1 && L->p2p_fuse && !lr_ep && !L->split_rem) {
+        if (dir == 1 && L->p2p_fuse && !lr_ep && !L->split_rem && !L->comm_only) {
           bool one_kind = true;
           for (int el = g0 + 1; el < g1; ++el) one_kind &= plan.expert_kind[el] == plan.expert_kind[g0];
           if (one_kind) {
@@ -1380,6 +1389,10 @@ moe_status_t fwd_ep(Fwd& F) {
     if (p2p) {  // every source's rows
       TR_TRY(L->tr->p2p_before_wait(ch, 1, cs));
       KERNEL_TRY(launch_p2p_wait(L->p2p_flags + (size_t)ch * D, D, epoch, cs));
+    }
+    if (L->comm_only) {  // measurement: the chunk's all2all without its ComputeMoE
+      CUDA_TRY(cudaEventRecord(L->ev_gemm[ch], cs));
+      return MOE_OK;
     }
     const int64_t u0 = urecv[(size_t)ch * D], u1 = urecv[(size_t)(ch + 1) * D];
     if (lr_ep) {  // unique rows -> expert-major GEMM rows (R6 order, so the GEMMs are unchanged)

@@ -140,6 +140,11 @@ class MoELayer:
         st = stream if stream is not None else torch.cuda.current_stream(self.device)
         abi.check(self.lib.moe_layer_host_sync(self.handle, C.c_void_p(st.cuda_stream)), "moe_layer_host_sync")
 
+    def set_comm_only(self, on: bool = True) -> None:
+        """ep > 1 measurement hook: later forwards skip ComputeMoE and the shared
+        experts (y undefined), so the chunked all2all is timed alone."""
+        abi.check(self.lib.moe_layer_set_comm_only(self.handle, 1 if on else 0), "moe_layer_set_comm_only")
+
     def set_profiling(self, on: bool = True) -> None:
         abi.check(self.lib.moe_layer_set_profiling(self.handle, 1 if on else 0), "moe_layer_set_profiling")
 

@@ -546,3 +546,63 @@ def test_ep_ranks_with_no_tokens(p2p):
             assert_close(y, ref["y"], f"T={T} p2p={p2p}")
         for L in layers:
             L.close()
+
+
+@pytest.mark.parametrize("p2p", [False, True])
+def test_comm_only_measurement_mode(p2p):
+    """moe_layer_set_comm_only (the bench's all2all-alone figure):
+    with it set, forwards run every chunk's dispatch and combine but no GEMM
+    (no gateup / down / shared stage is timed, the all2all stages still are,
+    one per chunk); cleared again, the next forward's y is the normal layer's
+    bit for bit (nothing the mode skipped leaks into later forwards)."""
+    D, N = 2, 3
+    inp = Inputs(E=12, k=2, H=256, F=256, S=1, Fs=128, T=1200, seed=7)
+    E_loc = 6
+    start = oracle.token_shards(1200, D)
+    group = LocalGroup(D)
+    layers, xs = [], []
+    for r in range(D):
+        w = dict(w_router=dev_bf16(inp.w_router), w_gate=dev_bf16(inp.w_gate[r * E_loc:(r + 1) * E_loc]),
+                 w_up=dev_bf16(inp.w_up[r * E_loc:(r + 1) * E_loc]),
+                 w_down=dev_bf16(inp.w_down[r * E_loc:(r + 1) * E_loc]),
+                 ws_gate=dev_bf16(inp.ws_gate), ws_up=dev_bf16(inp.ws_up), ws_down=dev_bf16(inp.ws_down))
+        layers.append(MoELayer(12, 2, 256, 256, w, S=1, Fs=128, ep=D, rank=r, max_tokens=600, norm_topk=1,
+                               local_group=group, a2a_p2p=p2p))
+        xs.append(dev_bf16(inp.x[start[r]:start[r + 1]]))
+    out = {}
+    errs = []
+
+    def worker(r):
+        try:
+            torch.cuda.set_device(0)
+            s = torch.cuda.Stream()
+            plan = make_plan(N, MOE_GEMM_GROUPED)
+            with torch.cuda.stream(s):
+                y0 = layers[r].forward(xs[r], plan=plan, stream=s).clone()
+                layers[r].set_comm_only(True)
+                layers[r].set_profiling(True)
+                layers[r].forward(xs[r], plan=plan, stream=s)
+                s.synchronize()
+                st = layers[r].stage_ms()
+                layers[r].set_profiling(False)
+                layers[r].set_comm_only(False)
+                y1 = layers[r].forward(xs[r], plan=plan, stream=s)
+                s.synchronize()
+                out[r] = (y0, y1, st)
+        except Exception as e:  # pragma: no cover
+            errs.append(repr(e))
+
+    th = [threading.Thread(target=worker, args=(r,), daemon=True) for r in range(D)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=120)
+    assert not errs, errs
+    for r in range(D):
+        y0, y1, st = out[r]
+        assert torch.equal(y0, y1)
+        assert st["gateup"][1] == 0 and st["down"][1] == 0 and st["shared"][1] == 0
+        assert st["dispatch_a2a"][1] == N and st["combine_a2a"][1] == N
+        assert st["exposed_a2a"][0] > 0.0
+    for L in layers:
+        L.close()
