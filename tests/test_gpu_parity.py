@@ -68,6 +68,39 @@ def test_grouped_gemm_swiglu_and_down(counts, tile_m):
         assert_close(o_np[a:b], ref_o, f"o group {g}")
 
 
+def test_tile_shape_does_not_change_bits():
+    """R14 picks the tile shape by load (128-row tiles on one CTA, cta_group::1,
+    or 256-row tiles on a CTA pair, cta_group::2).  Every output element is the
+    same k-ordered chain of K = 16 tensor-core steps either way, so the choice
+    must not change a bit (the EP = D == EP = 1 and chunked == unchunked claims
+    rely on it when shapes differ): all three epilogues, ragged groups."""
+    H, F = 512, 384
+    counts = [700, 0, 129, 1, 300]
+    G, rows = len(counts), sum(counts)
+    A = dev_bf16(fill_bf16(rows * H, 2, 1, 0, MODE_UNIF, 1.7).reshape(rows, H))
+    Wg = dev_bf16(fill_bf16(G * F * H, 2, 3, 0, MODE_UNIF, 0.1).reshape(G * F, H))
+    Wu = dev_bf16(fill_bf16(G * F * H, 2, 4, 0, MODE_UNIF, 0.1).reshape(G * F, H))
+    Wd = dev_bf16(fill_bf16(G * H * F, 2, 5, 0, MODE_UNIF, 0.08).reshape(G * H, F))
+    starts = np.concatenate([[0], np.cumsum(counts)[:-1]]).astype(np.int32)
+    rs = torch.from_numpy(starts).cuda()
+    rc = torch.from_numpy(np.array(counts, np.int32)).cuda()
+    out = {}
+    for tm in (128, 256):
+        h = torch.zeros(rows, F, dtype=torch.bfloat16, device="cuda")
+        gemm_grouped(0, A, Wg, Wu, F, h, rs, rc, F, tile_m=tm)
+        o = torch.zeros(rows, H, dtype=torch.bfloat16, device="cuda")
+        gemm_grouped(1, h, Wd, None, H, o, rs, rc, H, tile_m=tm)
+        lg = torch.zeros(rows, 160, dtype=torch.float32, device="cuda")   # router: fp32 epilogue, N = E padded
+        Wr = dev_bf16(fill_bf16(256 * H, 2, 2, 0, MODE_UNIF, 0.05).reshape(256, H))
+        one_s = torch.zeros(1, dtype=torch.int32, device="cuda")
+        one_c = torch.full((1,), rows, dtype=torch.int32, device="cuda")
+        gemm_grouped(2, A, Wr, None, 160, lg, one_s, one_c, 0, tile_m=tm)
+        torch.cuda.synchronize()
+        out[tm] = (h, o, lg)
+    for a, b, name in zip(out[128], out[256], ("h", "o", "logits")):
+        assert torch.equal(a, b), name
+
+
 @pytest.mark.parametrize("tile_m", [128, 256])
 def test_router_gemm_exact_on_grid(tile_m):
     T, H, E = 333, 512, 160
