@@ -62,8 +62,9 @@ def parse():
                         "launch gaps matter)")
     p.add_argument("--calibrate", default="auto", choices=["auto", "on", "off"],
                    help="measure the planner's cost model first (auto: ep > 1, where NVLink costs matter)")
-    p.add_argument("--a2a", default="nccl", choices=["nccl", "p2p"],
-                   help="ep > 1 all2all: NCCL send/recv, or the layer's put kernels over NVLink peer memory")
+    p.add_argument("--a2a", default="nccl", choices=["nccl", "p2p", "ce"],
+                   help="ep > 1 all2all: NCCL send/recv, the layer's put kernels over NVLink peer memory, or "
+                        "copy-engine peer copies (no SM moves a row)")
     return p.parse_args()
 
 
@@ -212,7 +213,7 @@ def feature_opts(args):
 
 def layer_opts(args):
     """feature_opts + the all2all data plane (no effect on the arithmetic)."""
-    return dict(feature_opts(args), a2a_p2p=args.a2a == "p2p")
+    return dict(feature_opts(args), a2a_p2p={"nccl": 0, "p2p": 1, "ce": 2}[args.a2a])
 
 
 def cpu_baseline(cfg, seed, skew, sample=0, opts=None):

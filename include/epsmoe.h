@@ -95,7 +95,11 @@ typedef struct {
                            workspace must be a cudaMalloc allocation) and
                            raise per-(chunk, source) flags there; NCCL only
                            allgathers counts (and, once, the buffer offsets
-                           of every rank's workspace).                       */
+                           of every rank's workspace).  2: as 1, but the
+                           rows move as cudaMemcpyAsync peer copies on the
+                           copy engines (no SM moves a row; NEXT-1's
+                           zero-CTA transfer) and one thread raises the
+                           flags after them.  Other values: MOE_ERR_INVALID. */
 } moe_config_t;
 
 /* Caller-owned device weights (bf16, K-major), valid for the layer's life.

@@ -199,7 +199,7 @@ int validate(const moe_config_t* c) {
   else if (c->dispatch_fp8 && c->hidden % 128) why = "dispatch_fp8 needs hidden % 128 == 0";
   else if (c->max_tokens < 1) why = "max_tokens must be >= 1";
   else if (c->local_reduce != 0 && c->local_reduce != 1) why = "local_reduce must be 0 or 1";
-  else if (c->a2a_p2p != 0 && c->a2a_p2p != 1) why = "a2a_p2p must be 0 or 1";
+  else if (c->a2a_p2p < 0 || c->a2a_p2p > 2) why = "a2a_p2p must be 0, 1 or 2";
   else if (c->route_groups > 1 &&
            (c->route_groups > 32 || c->num_experts % c->route_groups || c->route_topk_groups < 1 ||
             c->route_topk_groups > c->route_groups ||
@@ -1289,11 +1289,23 @@ moe_status_t fwd_ep(Fwd& F) {
       }
     CUDA_TRY(cudaMemcpyAsync(L->p2p_tab, L->p2p_host, p2p_table_bytes(D), cudaMemcpyHostToDevice, st));
   }
+  const bool copy_engine = c.a2a_p2p == 2;
   auto p2p_put = [&](int dir, int ch, cudaStream_t ps) -> moe_status_t {
     const size_t slot = (size_t)dir * MOE_MAX_CHUNKS + ch;
     auto* dsegs = reinterpret_cast<epsmoe::P2PSeg*>(L->p2p_tab) + slot * moe_layer::P2P_MAXS;
     auto* dpre = reinterpret_cast<int64_t*>(L->p2p_tab + P2P_SEGS_BYTES) + slot * (moe_layer::P2P_MAXS + 1);
     auto* dfp = reinterpret_cast<uint32_t**>(L->p2p_tab + P2P_SEGS_BYTES + P2P_PRE_BYTES) + slot * D;
+    if (copy_engine) {
+      // the same segments as cudaMemcpyAsync peer copies (copy engines: no SM
+      // moves a row), then one thread raises the chunk's flags after them
+      const auto* hs = reinterpret_cast<const epsmoe::P2PSeg*>(L->p2p_host) + slot * moe_layer::P2P_MAXS;
+      const auto* hp = reinterpret_cast<const int64_t*>(L->p2p_host + P2P_SEGS_BYTES) + slot * (moe_layer::P2P_MAXS + 1);
+      for (int i = 0; i < p2p_nseg[dir][ch]; ++i)
+        CUDA_TRY(cudaMemcpyAsync(hs[i].dst, hs[i].src, (size_t)(hp[i + 1] - hp[i]) * 16, cudaMemcpyDeviceToDevice, ps));
+      KERNEL_TRY(launch_p2p_signal(dfp, D, epoch, ps));
+      TR_TRY(L->tr->p2p_after_put((int)slot, ps));
+      return MOE_OK;
+    }
     KERNEL_TRY(launch_p2p_put(dsegs, dpre, p2p_nseg[dir][ch], p2p_total[dir][ch], 2 * L->comm_ctas,
                               L->p2p_done + slot, dfp, D, epoch, ps));
     TR_TRY(L->tr->p2p_after_put((int)slot, ps));

@@ -1,4 +1,5 @@
-// The layer's own all2all data plane over NVLink peer memory (a2a_p2p = 1):
+// The layer's own all2all data plane over NVLink peer memory (a2a_p2p = 1, or
+// 2 with the copies on the copy engines):
 // every rank's workspace is mapped into every other rank (cudaIpc, or plain
 // pointers for the in-process test group), so a chunk's dispatch / combine is
 // one put kernel per rank that stores its rows straight into the peers'
@@ -97,7 +98,20 @@ __global__ void p2p_wait_kernel(const uint32_t* __restrict__ flags, int n, uint3
   __syncwarp();
 }
 
+// Copy-engine plane (a2a_p2p = 2): the chunk's rows were moved by
+// cudaMemcpyAsync peer copies earlier on this stream (no SM involved); this
+// one-thread kernel runs after they completed and raises the flags.
+__global__ void p2p_signal_kernel(uint32_t* const* __restrict__ flags, int nflags, uint32_t epoch) {
+  __threadfence_system();
+  for (int i = 0; i < nflags; ++i) st_release_sys(flags[i], epoch);
+}
+
 }  // namespace
+
+int launch_p2p_signal(uint32_t* const* flags, int nflags, uint32_t epoch, cudaStream_t st) {
+  p2p_signal_kernel<<<1, 1, 0, st>>>(flags, nflags, epoch);
+  return (int)cudaGetLastError();
+}
 
 int launch_p2p_put(const P2PSeg* segs, const int64_t* pre, int nseg, int64_t total_vec, int ctas,
                    uint32_t* done_ctas, uint32_t* const* flags, int nflags, uint32_t epoch, cudaStream_t st) {

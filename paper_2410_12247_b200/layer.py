@@ -41,13 +41,13 @@ class MoELayer:
 
     def __init__(self, E, k, H, F, weights, S=0, Fs=0, ep=1, rank=0, max_tokens=1, norm_topk=0,
                  routed_scale=1.0, dispatch_fp8: bool = False, local_reduce: bool = False,
-                 route_groups: int = 0, route_topk_groups: int = 0, a2a_p2p: bool = False,
+                 route_groups: int = 0, route_topk_groups: int = 0, a2a_p2p: int = 0,
                  uid_dispatch: bytes | None = None, uid_combine: bytes | None = None,
                  device=None, local_group: "LocalGroup | None" = None):
         self.lib = abi.lib()
         self.cfg = abi.make_config(E, k, H, F, S, Fs, ep, rank, max_tokens, norm_topk, routed_scale,
                                    1 if dispatch_fp8 else 0, 1 if local_reduce else 0, route_groups,
-                                   route_topk_groups, 1 if a2a_p2p else 0)
+                                   route_topk_groups, int(a2a_p2p))
         self.E, self.k, self.H, self.F, self.S, self.Fs, self.ep, self.rank = E, k, H, F, S, Fs, ep, rank
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         nbytes = self.lib.moe_layer_workspace_bytes(C.byref(self.cfg))

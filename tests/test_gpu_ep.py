@@ -330,14 +330,16 @@ def test_ep_stage_profiling_and_exposed_a2a():
 
 # ---------------------------------------------------------------- own put-kernel all2all (a2a_p2p)
 
+@pytest.mark.parametrize("plane", [1, 2])
 @pytest.mark.parametrize("fuse", ["1", "0"])
 @pytest.mark.parametrize("D,N,S,fp8,lr", [(2, 2, 1, False, False), (4, 3, 1, False, False), (8, 2, 1, False, False),
                                           (2, 1, 3, False, False), (4, 2, 1, True, False), (2, 2, 1, False, True),
                                           (4, 1, 1, True, True)])
-def test_p2p_put_all2all(D, N, S, fp8, lr, fuse, monkeypatch):
-    """a2a_p2p: each rank's put kernel stores its rows straight into the peers'
-    workspaces (here: the other ranks' workspaces on the same GPU) and raises
-    per-(chunk, source) flags; consumers wait on them.  fuse = 1: the combine is
+def test_p2p_put_all2all(D, N, S, fp8, lr, fuse, plane, monkeypatch):
+    """a2a_p2p: each rank's put kernel (plane 1) or copy-engine peer copies
+    (plane 2) store its rows straight into the peers' workspaces (here: the
+    other ranks' workspaces on the same GPU), then per-(chunk, source) flags are
+    raised; consumers wait on them.  fuse = 1: the combine is
     the DownGemm's own epilogue scattering rows into the home ranks' buffers
     (flags raised by its last CTA).  y == the NCCL-path layout's result: EP = 1
     bit for bit (per-pair path) or the oracle's R16."""
@@ -345,7 +347,7 @@ def test_p2p_put_all2all(D, N, S, fp8, lr, fuse, monkeypatch):
     E = 16
     inp = Inputs(E=E, k=4, H=256, F=256, S=1, Fs=128, T=919, seed=100 + D + N, grid=True)
     plan = make_plan(N * S, MOE_GEMM_GROUPED, token_slices=S)
-    y, bufs = _ep_forward(inp, 4, 1, D, plan, fp8=fp8, lr=lr, p2p=True)
+    y, bufs = _ep_forward(inp, 4, 1, D, plan, fp8=fp8, lr=lr, p2p=plane)
     # second forward on fresh layers again (flags / epochs start over) and a
     # repeated forward on the same layers are covered by the layer reuse below
     if lr:
@@ -500,7 +502,7 @@ def test_ep_calibration_collective_and_shared():
         L.close()
 
 
-@pytest.mark.parametrize("p2p", [False, True])
+@pytest.mark.parametrize("p2p", [0, 1, 2])
 def test_ep_ranks_with_no_tokens(p2p):
     """Ragged extreme: T = 3 over 4 ranks (one rank has no tokens, the others one
     each) and T = 0 everywhere; both all2all planes; y == EP 1 bit for bit."""
@@ -548,7 +550,7 @@ def test_ep_ranks_with_no_tokens(p2p):
             L.close()
 
 
-@pytest.mark.parametrize("p2p", [False, True])
+@pytest.mark.parametrize("p2p", [0, 1, 2])
 def test_comm_only_measurement_mode(p2p):
     """moe_layer_set_comm_only (the bench's all2all-alone figure):
     with it set, forwards run every chunk's dispatch and combine but no GEMM

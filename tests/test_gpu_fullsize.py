@@ -127,7 +127,7 @@ def test_full_size_ep8_on_one_gpu(name, skew, fp8):
     ref_layer.close()
     del ref_layer
     start = oracle.token_shards(T, D)
-    for p2p in (False, True):
+    for p2p in (0, 1, 2):   # NCCL-path layout (in-process transport), put kernels, copy engines
         group = LocalGroup(D)
         layers = []
         for r in range(D):
