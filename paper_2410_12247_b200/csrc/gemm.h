@@ -47,7 +47,7 @@ struct GemmArgs {
   int num_ctas;            // persistent grid size (SM budget)
   int cta_pair;            // 1: 256-row tiles on CTA pairs (cta_group::2); 0: 128-row tiles
   const int32_t* a_row_index;  // optional gather: logical A row r is physical row a_row_index[r] of A
-                               // (TMA tile::gather4; EPI_SWIGLU only).  nullptr = contiguous A.
+                               // (16-B cp.async into the swizzled stage; EPI_SWIGLU only).  nullptr = contiguous A.
   int32_t* tile_counter;       // device int32[2], zero-initialised, for dynamic tile tickets; launches
                                // that may run concurrently need distinct counters (nullptr = shared)
   int row_mode;                // 0: all rows of each group; 1: only the first floor(n/256)*256 rows

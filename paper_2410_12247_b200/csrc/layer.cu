@@ -103,9 +103,9 @@ struct moe_layer {
                                   // single CTAs; measured 1-3% slower than padding (DSv2, Mixtral), so off
   int comm_ctas = 0;              // ep > 1: NCCL maxCTAs per communicator (EPSMOE_COMM_CTAS, default 8);
                                   // the persistent GEMM grid leaves 2*comm_ctas SMs free for them
-  bool gather_a = false;          // EPSMOE_GATHER=1: GateUp gathers x rows (tile::gather4) at ep == 1
-                                  // instead of reading a materialised send buffer; measured 3.5x
-                                  // slower GateUp on B200 (32 gather4 per stage), so off by default
+  bool gather_a = false;          // EPSMOE_GATHER=1: GateUp gathers x rows itself at ep == 1 (16-B cp.async
+                                  // into the swizzled stage) instead of reading a materialised send buffer;
+                                  // measured 1.9x slower GateUp on B200 (request-bound), so off by default
   cudaEvent_t ev_hist = nullptr, ev_ready = nullptr, ev_comb_done = nullptr;
   std::vector<cudaEvent_t> ev_disp, ev_gemm;
   epsmoe::Transport* tr = nullptr;  // all2all transport (NCCL, or in-process for tests), ep > 1
@@ -822,9 +822,10 @@ moe_status_t fwd_routing(Fwd& F) {
   // Shared experts depend only on x: they run on s_side, concurrently
   // with topKGating / split (HBM-bound kernels that co-reside with the GEMM's
   // CTAs) and, for ep > 1, with the count exchange, host wait and dispatch(0).
-  // ep == 1: the shared DownGemm is deferred and fused with the combine
-  // (EPI_COMBINE), so only GateUp runs here.
-  // (a debug request for s materialises it: unfused path)
+  // ep == 1 with EPSMOE_FUSE_COMBINE=1/2 (off by default, measured no faster):
+  // the shared DownGemm is deferred and meets the combine (EPI_COMBINE epilogue,
+  // or token pieces), so only GateUp runs here.  (A debug request for s
+  // materialises it: unfused path.)
   const int fuse =
       ((D == 1) && L->SF && T > 0 && !c.local_reduce && !(dbg && dbg->shared_out)) ? L->fuse_combine : 0;
   auto shared_experts = [&](cudaStream_t ss) -> int {
@@ -887,8 +888,8 @@ moe_status_t fwd_routing(Fwd& F) {
   KERNEL_TRY(launch_range_scan(L->range_hist, (int)T, E, L->range_off, L->hist, L->seg_start, st));
   ++L->last_launches;  // range scan + expert scan
   // ---- split (K3): x -> send rows, expert-major (R6).  At ep == 1 the send
-  // buffer is only the GateUp GEMM's A operand, so by default the split is
-  // index-only and the GEMM gathers x's rows with TMA tile::gather4.
+  // buffer is only the GateUp GEMM's A operand; with EPSMOE_GATHER=1 the split
+  // is index-only and the GEMM gathers x's rows itself (measured slower, off).
   const bool fp8 = c.dispatch_fp8 != 0;
   const bool gather = (D == 1) && L->gather_a && T > 0 && !fp8;
   // ep > 1 with local_reduce: index-only here (pos feeds the dedup rows' codes);
