@@ -74,6 +74,7 @@ struct KParams {
   int diag;       // diagnostics only (EPSMOE_GEMM_DIAG): 1 skip output stores, 2 skip TMEM loads + stores,
                   // 3 bulk stores into a 256-row window (L2-resident: same store traffic, no DRAM writes)
   int tma_store;  // bf16 outputs: full 32-row warp slices leave through TMA bulk-tensor stores (tmO)
+  int half_tiles;  // CTA pairs: a group's last m-tile with <= 128 rows runs as an M = 128 2-CTA MMA (see kernel)
   int64_t ldo;
   void* out;
   const float* bias;
@@ -282,8 +283,19 @@ struct Tickets {
 template <int EPI, int CG, bool GATHER>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
 gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB0,
-            const __grid_constant__ CUtensorMap tmB1, const __grid_constant__ CUtensorMap tmO, const KParams p) {
+            const __grid_constant__ CUtensorMap tmB1, const __grid_constant__ CUtensorMap tmO,
+            const __grid_constant__ CUtensorMap tmB0h, const __grid_constant__ CUtensorMap tmB1h, const KParams p) {
   using C = Cfg<CG>;
+  // Half tiles (CTA pairs, GateUp / Down): a group's last m-tile holding <= 128
+  // valid rows is issued as one M = 128 cta_group::2 MMA (64 rows per CTA)
+  // instead of M = 256, halving its tensor work (the M padding is ~128 rows per
+  // expert on average).  Accumulator layout of that shape (per CTA, 64 rows):
+  // TMEM lanes 0-63 hold columns [0, 128) of the pair's 256, lanes 64-127
+  // columns [128, 256), both at TMEM columns 0-127.  So epilogue warps 0/1 own
+  // rows 0-63 x the low column half and warps 2/3 the same rows x the high
+  // half.  For SwiGLU each CTA then loads 64 gate + 64 up rows (64-row boxes
+  // tmB0h / tmB1h) so that a warp sees matching gate and up columns.
+  constexpr bool HALF_OK = (CG == 2) && !GATHER && (EPI == EPI_SWIGLU || EPI == EPI_BF16);
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
@@ -384,7 +396,8 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
       if (t < 0) break;
       int g, mt, nt;
       decode_tile(st, G, n_tiles, p.raster_gm, t, g, mt, nt);
-      const int a_row = st.gstart[g] + mt * C::TILE_M + (int)rank * BM;
+      const bool half = HALF_OK && p.half_tiles && st.gcount[g] - mt * C::TILE_M <= BM;
+      const int a_row = st.gstart[g] + mt * C::TILE_M + (int)rank * (half ? BM / 2 : BM);
       const int b_row0 = (p.b_base + g) * p.b_group_rows + nt * n_out_tile;
       if constexpr (GATHER) {
         // this lane's rows of the tile: chunk (lane & 7) of rows (lane >> 3) + 4 i;
@@ -434,6 +447,10 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
             } else {
               ptx::tma_load_2d(b_dst, &tmB0, fb, kb * BK, b_row0);
             }
+          } else if (HALF_OK && EPI == EPI_SWIGLU && half) {
+            // half tile: this CTA's B = gate rows [64r, 64r+64) then up rows [64r, 64r+64)
+            ptx::tma_load_2d_pair(b_dst, &tmB0h, fb, kb * BK, b_row0 + (int)rank * 64);
+            ptx::tma_load_2d_pair(b_dst + C::B_BYTES / 2, &tmB1h, fb, kb * BK, b_row0 + (int)rank * 64);
           } else {
             // SwiGLU: CTA0 gate rows -> acc cols [0,128); CTA1 up rows -> [128,256)
             const void* tb = (EPI == EPI_SWIGLU && rank == 1) ? (const void*)&tmB1 : (const void*)&tmB0;
@@ -447,11 +464,18 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
   } else if (warp == 1) {
     // ===================== MMA issuer (one thread of the leader CTA) =====================
     if (lane == 0 && rank == 0) {
-      constexpr uint32_t idesc = ptx::idesc_bf16_f32(C::TILE_M, BN);
+      constexpr uint32_t idesc_full = ptx::idesc_bf16_f32(C::TILE_M, BN);
+      constexpr uint32_t idesc_half = ptx::idesc_bf16_f32(C::TILE_M / 2, BN);
       uint32_t stage = 0, phase = 0, iter = 0;
       while (true) {
         const int t = tk.consume(true);
         if (t < 0) break;
+        uint32_t idesc = idesc_full;
+        if (HALF_OK && p.half_tiles) {
+          int g, mt, nt;
+          decode_tile(st, G, n_tiles, p.raster_gm, t, g, mt, nt);
+          if (st.gcount[g] - mt * C::TILE_M <= BM) idesc = idesc_half;
+        }
         const uint32_t acc = iter & 1, accph = (iter >> 1) & 1;
         ptx::mbar_wait(ptx::smem_u32(&st.tempty[acc]), accph ^ 1);
         ptx::tc_fence_after();
@@ -513,7 +537,10 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
       const uint32_t acc = iter & 1, accph = (iter >> 1) & 1;
       ptx::mbar_wait(ptx::smem_u32(&st.tfull[acc]), accph);
       ptx::tc_fence_after();
-      const int local_row = mt * C::TILE_M + (int)rank * BM + q * 32 + lane;
+      const bool half = HALF_OK && p.half_tiles && st.gcount[g] - mt * C::TILE_M <= BM;
+      const int hq = half ? (q >> 1) : 0;  // half tile: which 128 (Down) / 64 (SwiGLU) column half
+      const int local_row = half ? mt * C::TILE_M + (int)rank * (BM / 2) + (q & 1) * 32 + lane
+                                 : mt * C::TILE_M + (int)rank * BM + q * 32 + lane;
       const bool valid = local_row < st.gcount[g];
       const int64_t grow = (int64_t)st.gstart[g] + local_row;
       const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
@@ -531,12 +558,16 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
       }
       uint8_t* stg = st.stage_out[q];
       if (EPI == EPI_SWIGLU) {
-        __nv_bfloat16* out0 = reinterpret_cast<__nv_bfloat16*>(p.out) + (grow - lane) * p.ldo + nt * 128;
+        // full tile: 4 x 32 output columns, gate at TMEM column c*32, up at 128 + c*32;
+        // half tile: this warp's 64 output columns nt*128 + 64*hq + [0, 64), gate at c*32, up at 64 + c*32
+        const int ocol = nt * 128 + hq * 64;
+        const int nchunk = half ? 2 : 4, up_off = half ? 64 : 128;
+        __nv_bfloat16* out0 = reinterpret_cast<__nv_bfloat16*>(p.out) + (grow - lane) * p.ldo + ocol;
 #pragma unroll 1
-        for (int c = 0; c < 4; ++c) {  // 4 x 32 output columns
+        for (int c = 0; c < nchunk; ++c) {
           uint32_t gr[32], ur[32], pk[16];
           ptx::tmem_ld32(taddr + c * 32, gr);
-          ptx::tmem_ld32(taddr + 128 + c * 32, ur);
+          ptx::tmem_ld32(taddr + up_off + c * 32, ur);
           ptx::tmem_wait_ld();
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
@@ -544,7 +575,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
             float u0 = __uint_as_float(ur[2 * i]), u1 = __uint_as_float(ur[2 * i + 1]);
             pk[i] = pack_bf16(silu_f32(g0) * u0, silu_f32(g1) * u1);
           }
-          store_chunk(pk, stg, out0 + c * 32, p.ldo, vr, lane, p.tma_store ? &tmO : nullptr, nt * 128 + c * 32,
+          store_chunk(pk, stg, out0 + c * 32, p.ldo, vr, lane, p.tma_store ? &tmO : nullptr, ocol + c * 32,
                       (p.diag == 3 ? (int)((grow - lane) & 255) : (int)(grow - lane)));
         }
       } else if (EPI == EPI_BF16 && p.rseg) {
@@ -562,8 +593,8 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
         }
         const int jq = lane & 3;
 #pragma unroll 1
-        for (int c = 0; c < BN / 32; ++c) {
-          const int col0 = nt * BN + c * 32;
+        for (int c = 0; c < (half ? BN / 64 : BN / 32); ++c) {  // half tile: this warp's 128 columns
+          const int col0 = nt * BN + hq * 128 + c * 32;
           if (col0 >= p.N) break;
           uint32_t r[32], pk[16];
           ptx::tmem_ld32(taddr + c * 32, r);
@@ -583,16 +614,17 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
           __syncwarp();
         }
       } else if (EPI == EPI_BF16) {
-        __nv_bfloat16* out0 = reinterpret_cast<__nv_bfloat16*>(p.out) + (grow - lane) * p.ldo + nt * BN;
+        const int ocol = nt * BN + hq * 128;  // half tile: this warp's 128 of the 256 columns
+        __nv_bfloat16* out0 = reinterpret_cast<__nv_bfloat16*>(p.out) + (grow - lane) * p.ldo + ocol;
 #pragma unroll 1
-        for (int c = 0; c < BN / 32; ++c) {
-          if (nt * BN + c * 32 >= p.N) break;  // N is a multiple of 32 (warp-uniform)
+        for (int c = 0; c < (half ? BN / 64 : BN / 32); ++c) {
+          if (ocol + c * 32 >= p.N) break;  // N is a multiple of 32 (warp-uniform)
           uint32_t r[32], pk[16];
           ptx::tmem_ld32(taddr + c * 32, r);
           ptx::tmem_wait_ld();
 #pragma unroll
           for (int i = 0; i < 16; ++i) pk[i] = pack_bf16(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1]));
-          store_chunk(pk, stg, out0 + c * 32, p.ldo, vr, lane, p.tma_store ? &tmO : nullptr, nt * BN + c * 32,
+          store_chunk(pk, stg, out0 + c * 32, p.ldo, vr, lane, p.tma_store ? &tmO : nullptr, ocol + c * 32,
                       (p.diag == 3 ? (int)((grow - lane) & 255) : (int)(grow - lane)));
         }
       } else if (EPI == EPI_COMBINE) {
@@ -814,7 +846,7 @@ int launch_epi(const GemmArgs& a, cudaStream_t stream) {
     if (e != cudaSuccess) return (int)e;
     attr_set = true;
   }
-  CUtensorMap tA, tB0, tB1;
+  CUtensorMap tA, tB0, tB1, tB0h, tB1h;
   const int b_box = (EPI == EPI_SWIGLU || CG == 2) ? 128 : 256;
   if (!make_tmap(&tA, a.A, a.a_rows, a.K, GATHER ? 1 : BM)) return (int)cudaErrorInvalidValue;
   if (!make_tmap(&tB0, a.B0, a.b_rows, a.K, b_box)) return (int)cudaErrorInvalidValue;
@@ -822,6 +854,14 @@ int launch_epi(const GemmArgs& a, cudaStream_t stream) {
     if (!make_tmap(&tB1, a.B1, a.b_rows, a.K, b_box)) return (int)cudaErrorInvalidValue;
   } else {
     tB1 = tB0;
+  }
+  // half tiles (CTA pairs): 64-row boxes of W_gate / W_up for SwiGLU
+  const int half_env = env_int("EPSMOE_HALF_TILES", 1);
+  tB0h = tB0;
+  tB1h = tB1;
+  if (EPI == EPI_SWIGLU && CG == 2 && !GATHER && half_env) {
+    if (!make_tmap(&tB0h, a.B0, a.b_rows, a.K, 64) || !make_tmap(&tB1h, a.B1, a.b_rows, a.K, 64))
+      return (int)cudaErrorInvalidValue;
   }
   KParams p;
   p.K = a.K;
@@ -849,6 +889,7 @@ int launch_epi(const GemmArgs& a, cudaStream_t stream) {
   p.comb_w = a.comb_w;
   p.comb_k = a.comb_k;
   p.diag = env_int("EPSMOE_GEMM_DIAG", 0);
+  p.half_tiles = (CG == 2 && !GATHER && (EPI == EPI_SWIGLU || EPI == EPI_BF16) && a.row_mode == 0) ? half_env : 0;
   CUtensorMap tO;
   std::memset(&tO, 0, sizeof(tO));
   p.tma_store = 0;
@@ -873,7 +914,7 @@ int launch_epi(const GemmArgs& a, cudaStream_t stream) {
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, tA, tB0, tB1, tO, p);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, tA, tB0, tB1, tO, tB0h, tB1h, p);
   return (int)e;
 }
 
