@@ -284,7 +284,8 @@ template <int EPI, int CG, bool GATHER>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
 gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB0,
             const __grid_constant__ CUtensorMap tmB1, const __grid_constant__ CUtensorMap tmO,
-            const __grid_constant__ CUtensorMap tmB0h, const __grid_constant__ CUtensorMap tmB1h, const KParams p) {
+            const __grid_constant__ CUtensorMap tmB0h, const __grid_constant__ CUtensorMap tmB1h,
+            const __grid_constant__ CUtensorMap tmAh, const KParams p) {
   using C = Cfg<CG>;
   // Half tiles (CTA pairs, GateUp / Down): a group's last m-tile holding <= 128
   // valid rows is issued as one M = 128 cta_group::2 MMA (64 rows per CTA)
@@ -294,7 +295,8 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
   // columns [128, 256), both at TMEM columns 0-127.  So epilogue warps 0/1 own
   // rows 0-63 x the low column half and warps 2/3 the same rows x the high
   // half.  For SwiGLU each CTA then loads 64 gate + 64 up rows (64-row boxes
-  // tmB0h / tmB1h) so that a warp sees matching gate and up columns.
+  // tmB0h / tmB1h) so that a warp sees matching gate and up columns; A comes
+  // as 64-row boxes (tmAh), so a half tile also moves 25% fewer bytes.
   constexpr bool HALF_OK = (CG == 2) && !GATHER && (EPI == EPI_SWIGLU || EPI == EPI_BF16);
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -417,7 +419,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
           const uint32_t a_dst = ptx::smem_u32(sA + stage * C::A_BYTES);
           const uint32_t b_dst = ptx::smem_u32(sB + stage * C::B_BYTES);
           if ((CG == 1 || rank == 0) && lane == 0)
-            ptx::mbar_arrive_expect_tx(fb, CG * ((GATHER ? 0 : C::A_BYTES) + C::B_BYTES));
+            ptx::mbar_arrive_expect_tx(fb, CG * ((GATHER ? 0 : (half ? C::A_BYTES / 2 : C::A_BYTES)) + C::B_BYTES));
           if constexpr (GATHER) {
             // A by 16-B cp.async straight into the 128-B swizzle (chunk c of row r at
             // c ^ (r & 7)): 4 rows x 128 B per warp instruction, no TMA descriptor per row
@@ -438,7 +440,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
           } else if constexpr (CG == 1) {
             ptx::tma_load_2d(a_dst, &tmA, fb, kb * BK, a_row);
           } else {
-            ptx::tma_load_2d_pair(a_dst, &tmA, fb, kb * BK, a_row);
+            ptx::tma_load_2d_pair(a_dst, half ? &tmAh : &tmA, fb, kb * BK, a_row);
           }
           if constexpr (CG == 1) {
             if (EPI == EPI_SWIGLU) {
@@ -846,7 +848,7 @@ int launch_epi(const GemmArgs& a, cudaStream_t stream) {
     if (e != cudaSuccess) return (int)e;
     attr_set = true;
   }
-  CUtensorMap tA, tB0, tB1, tB0h, tB1h;
+  CUtensorMap tA, tB0, tB1, tB0h, tB1h, tAh;
   const int b_box = (EPI == EPI_SWIGLU || CG == 2) ? 128 : 256;
   if (!make_tmap(&tA, a.A, a.a_rows, a.K, GATHER ? 1 : BM)) return (int)cudaErrorInvalidValue;
   if (!make_tmap(&tB0, a.B0, a.b_rows, a.K, b_box)) return (int)cudaErrorInvalidValue;
@@ -859,6 +861,10 @@ int launch_epi(const GemmArgs& a, cudaStream_t stream) {
   const int half_env = env_int("EPSMOE_HALF_TILES", 1);
   tB0h = tB0;
   tB1h = tB1;
+  tAh = tA;
+  if (CG == 2 && !GATHER && (EPI == EPI_SWIGLU || EPI == EPI_BF16) && half_env &&
+      !make_tmap(&tAh, a.A, a.a_rows, a.K, BM / 2))
+    return (int)cudaErrorInvalidValue;
   if (EPI == EPI_SWIGLU && CG == 2 && !GATHER && half_env) {
     if (!make_tmap(&tB0h, a.B0, a.b_rows, a.K, 64) || !make_tmap(&tB1h, a.B1, a.b_rows, a.K, 64))
       return (int)cudaErrorInvalidValue;
@@ -914,7 +920,7 @@ int launch_epi(const GemmArgs& a, cudaStream_t stream) {
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, tA, tB0, tB1, tO, tB0h, tB1h, p);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, tA, tB0, tB1, tO, tB0h, tB1h, tAh, p);
   return (int)e;
 }
 
