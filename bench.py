@@ -218,9 +218,9 @@ def layer_opts(args):
 
 def cpu_baseline(cfg, seed, skew, sample=0, opts=None):
     # sized for ~10 s of oracle work on a 16-core host (the contract's bounded sample; measured
-    # oracle rates there at these sizes: dsv2 ~12, mixtral ~19, dsv2_lite ~800 tokens/s)
-    n = sample or {"tiny": 256, "dsv2_lite": 8192, "mixtral": 192, "dsv2": 128, "dsv2_decode": 128,
-                   "mixtral_decode": 192}.get(cfg["name"], 32)
+    # oracle rates there at these sizes: dsv2 ~19, mixtral ~50, dsv2_lite ~1150 tokens/s)
+    n = sample or {"tiny": 256, "dsv2_lite": 12288, "mixtral": 512, "dsv2": 192, "dsv2_decode": 192,
+                   "mixtral_decode": 512}.get(cfg["name"], 32)
     inp, ew, cache = oracle_sample(cfg, seed, n, 0, skew, device_gen=True)
     dt = run_oracle_timed(cfg, inp, ew, cache, opts)
     return {"value": n / dt, "unit": UNIT, "cores": host_cores(), "kind": "oracle",
