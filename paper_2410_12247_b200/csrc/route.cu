@@ -30,6 +30,100 @@ __device__ __forceinline__ bool better(float av, int ae, float bv, int be) {
   return av > bv || (av == bv && ae < be);
 }
 
+// U consecutive tokens of a routing range, unrestricted routing (see the
+// kernel below for the per-token definition; this is the same arithmetic).
+constexpr int GATE_U = 4;
+template <int U>
+__device__ __forceinline__ void gate_tokens(const float* __restrict__ logits, int t0, int E, int k, int norm_topk,
+                                            float scale, int32_t* __restrict__ topk_idx, float* __restrict__ topk_w,
+                                            int32_t* hist, int lane) {
+  float v[U][MAX_EPL];
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const float* row = logits + (int64_t)(t0 + u) * E;
+#pragma unroll
+    for (int i = 0; i < MAX_EPL; ++i) {
+      const int e = lane + 32 * i;
+      v[u][i] = (e < E) ? row[e] : -INFINITY;
+    }
+  }
+  uint32_t taken[U];
+  float top_v[U][MAX_K];
+  int top_e[U][MAX_K];
+#pragma unroll
+  for (int u = 0; u < U; ++u) taken[u] = 0;
+#pragma unroll
+  for (int j = 0; j < MAX_K; ++j) {
+    if (j < k) {
+      float bv[U];
+      int be[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        bv[u] = -INFINITY;
+        be[u] = 0x7fffffff;
+#pragma unroll
+        for (int i = 0; i < MAX_EPL; ++i) {
+          const int e = lane + 32 * i;
+          if (e < E && !((taken[u] >> i) & 1u) && better(v[u][i], e, bv[u], be[u])) { bv[u] = v[u][i]; be[u] = e; }
+        }
+      }
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const float ov = __shfl_xor_sync(0xffffffffu, bv[u], off);
+          const int oe = __shfl_xor_sync(0xffffffffu, be[u], off);
+          if (better(ov, oe, bv[u], be[u])) { bv[u] = ov; be[u] = oe; }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        top_v[u][j] = bv[u];
+        top_e[u][j] = be[u];
+        if ((be[u] & 31) == lane) taken[u] |= 1u << (be[u] >> 5);
+      }
+    }
+  }
+  float sm[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const float m = top_v[u][0];
+    float s = 0.f;
+#pragma unroll
+    for (int i = 0; i < MAX_EPL; ++i) s += expf(v[u][i] - m);
+    sm[u] = s;
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1)
+#pragma unroll
+    for (int u = 0; u < U; ++u) sm[u] += __shfl_xor_sync(0xffffffffu, sm[u], off);
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const float m = top_v[u][0];
+    float psel = 0.f, pj = 0.f;
+    int ej = 0;
+#pragma unroll
+    for (int j = 0; j < MAX_K; ++j) {
+      if (j < k) {
+        const float pv = expf(top_v[u][j] - m) / sm[u];
+        psel += pv;
+        if (j == lane) { pj = pv; ej = top_e[u][j]; }
+      }
+    }
+    const int64_t t = t0 + u;
+    if (lane < k) {
+      const float w = norm_topk ? pj / psel : pj;
+      topk_idx[t * k + lane] = ej;
+      topk_w[t * k + lane] = w * scale;
+    }
+    if (lane == 0)
+#pragma unroll
+      for (int j = 0; j < MAX_K; ++j)
+        if (j < k) hist[top_e[u][j]] += 1;
+  }
+  __syncwarp();
+}
+
 // K2 topKGating.  One warp per range of range_len(T) tokens, tokens
 // in order.  idx = k largest logits (ties -> lower expert id, R2); p = softmax
 // over all E in fp32; w_j = p_{idx_j} (/ sum_j p_{idx_j} if norm_topk) * scale.
@@ -37,7 +131,7 @@ __device__ __forceinline__ bool better(float av, int ae, float bv, int be) {
 __global__ void __launch_bounds__(WARPS_R * 32)
 gate_topk_kernel(const float* __restrict__ logits, int T, int E, int k, int norm_topk, float scale,
                  int override_routing, int route_groups, int route_topk_groups, int32_t* __restrict__ topk_idx,
-                 float* __restrict__ topk_w, int32_t* __restrict__ range_hist, int R, int rt) {
+                 float* __restrict__ topk_w, int32_t* __restrict__ range_hist, int R, int rt, int interleave) {
   __shared__ int32_t hist_s[WARPS_R][256];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int r = blockIdx.x * WARPS_R + warp;
@@ -45,7 +139,16 @@ gate_topk_kernel(const float* __restrict__ logits, int T, int E, int k, int norm
   __syncwarp();
   if (r < R) {
     const int t_end = min(T, (r + 1) * rt);
-    for (int t = r * rt; t < t_end; ++t) {
+    int t = r * rt;
+    if (interleave && !override_routing && !route_groups) {
+      // GATE_U tokens at a time: the same per-token operations (lane-strided
+      // logits, local argmax in i order, the same xor-shuffle trees, the same
+      // softmax sum order), interleaved so their shuffle / expf latencies overlap:
+      // bit-identical to the one-token loop below, which takes the remainder
+      for (; t + GATE_U <= t_end; t += GATE_U) gate_tokens<GATE_U>(logits, t, E, k, norm_topk, scale, topk_idx, topk_w,
+                                                                  hist_s[warp], lane);
+    }
+    for (; t < t_end; ++t) {
       if (override_routing) {
         if (lane < k) {
           int e = topk_idx[(int64_t)t * k + lane];
@@ -432,6 +535,14 @@ int max_ranges(int64_t T_max) {
   return (int)std::max<int64_t>(std::min<int64_t>(T_max, ranges_target()), num_ranges(T_max));
 }
 
+static int gate_interleave() {  // EPSMOE_GATE_U=0: one token at a time (bit-identical, slower)
+  static const int v = [] {
+    const char* e = std::getenv("EPSMOE_GATE_U");
+    return e ? std::atoi(e) : 1;
+  }();
+  return v;
+}
+
 int launch_gate_topk(const float* logits, int T, int E, int k, int norm_topk, float scale, int override_routing,
                      int route_groups, int route_topk_groups, int32_t* topk_idx, float* topk_w,
                      int32_t* range_hist, cudaStream_t st) {
@@ -441,7 +552,8 @@ int launch_gate_topk(const float* logits, int T, int E, int k, int norm_topk, fl
   gate_topk_kernel<<<(R + WARPS_R - 1) / WARPS_R, WARPS_R * 32, 0, st>>>(logits, T, E, k, norm_topk, scale,
                                                                          override_routing, route_groups,
                                                                          route_topk_groups, topk_idx, topk_w,
-                                                                         range_hist, R, range_len(T));
+                                                                         range_hist, R, range_len(T),
+                                                                         gate_interleave());
   return (int)cudaGetLastError();
 }
 

@@ -117,6 +117,43 @@ def test_router_gemm_exact_on_grid(tile_m):
     assert np.array_equal(out.cpu().numpy(), ref)
 
 
+def test_gate_interleaved_tokens_bit_identical():
+    """The gate kernel takes 4 tokens of a routing range at a time with the same
+    per-token operations (EPSMOE_GATE_U=1, default) as the one-token loop: indices
+    and weights bit-identical, at range lengths 1 (T = 1000, remainder path
+    only), 8 and 32 (16 000 and 40 000 tokens), in a subprocess per setting (the
+    switch is read once per process)."""
+    import subprocess
+    import sys
+    code = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, %r)
+from gen import Inputs
+from tests.gpu_util import layer_from_inputs, dev_bf16
+out = []
+for T in (1000, 16000, 40000):
+    inp = Inputs(E=160, k=6, H=256, F=128, T=T, seed=9)
+    L = layer_from_inputs(inp, 6, 0)
+    d, b = L.debug_buffers(T)
+    L.forward(dev_bf16(inp.x), debug=d)
+    torch.cuda.synchronize()
+    out += [b["topk_idx"].cpu().numpy(), b["topk_w"].cpu().numpy().view(np.uint32), b["pos"].cpu().numpy()]
+    L.close()
+np.savez(sys.argv[1], *out)
+""" % os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    import tempfile
+    res = []
+    with tempfile.TemporaryDirectory() as td:
+        for u in ("1", "0"):
+            f = os.path.join(td, f"g{u}.npz")
+            env = dict(os.environ, EPSMOE_GATE_U=u)
+            subprocess.run([sys.executable, "-c", code, f], check=True, env=env, timeout=300)
+            z = np.load(f)
+            res.append([z[n] for n in z.files])
+    for a, b in zip(*res):
+        assert np.array_equal(a, b)
+
+
 # ---------------------------------------------------------------- full layer (EP = 1)
 
 CASES = {
