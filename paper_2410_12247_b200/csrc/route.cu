@@ -33,16 +33,16 @@ __device__ __forceinline__ bool better(float av, int ae, float bv, int be) {
 // U consecutive tokens of a routing range, unrestricted routing (see the
 // kernel below for the per-token definition; this is the same arithmetic).
 constexpr int GATE_U = 4;
-template <int U>
+template <int U, int EPL>
 __device__ __forceinline__ void gate_tokens(const float* __restrict__ logits, int t0, int E, int k, int norm_topk,
                                             float scale, int32_t* __restrict__ topk_idx, float* __restrict__ topk_w,
                                             int32_t* hist, int lane) {
-  float v[U][MAX_EPL];
+  float v[U][EPL];
 #pragma unroll
   for (int u = 0; u < U; ++u) {
     const float* row = logits + (int64_t)(t0 + u) * E;
 #pragma unroll
-    for (int i = 0; i < MAX_EPL; ++i) {
+    for (int i = 0; i < EPL; ++i) {
       const int e = lane + 32 * i;
       v[u][i] = (e < E) ? row[e] : -INFINITY;
     }
@@ -62,7 +62,7 @@ __device__ __forceinline__ void gate_tokens(const float* __restrict__ logits, in
         bv[u] = -INFINITY;
         be[u] = 0x7fffffff;
 #pragma unroll
-        for (int i = 0; i < MAX_EPL; ++i) {
+        for (int i = 0; i < EPL; ++i) {
           const int e = lane + 32 * i;
           if (e < E && !((taken[u] >> i) & 1u) && better(v[u][i], e, bv[u], be[u])) { bv[u] = v[u][i]; be[u] = e; }
         }
@@ -90,7 +90,7 @@ __device__ __forceinline__ void gate_tokens(const float* __restrict__ logits, in
     const float m = top_v[u][0];
     float s = 0.f;
 #pragma unroll
-    for (int i = 0; i < MAX_EPL; ++i) s += expf(v[u][i] - m);
+    for (int i = 0; i < EPL; ++i) s += expf(v[u][i] - m);
     sm[u] = s;
   }
 #pragma unroll
@@ -128,6 +128,9 @@ __device__ __forceinline__ void gate_tokens(const float* __restrict__ logits, in
 // in order.  idx = k largest logits (ties -> lower expert id, R2); p = softmax
 // over all E in fp32; w_j = p_{idx_j} (/ sum_j p_{idx_j} if norm_topk) * scale.
 // Also writes the range's expert histogram range_hist[e * R + r].
+// EPL = ceil(E / 32) logits per lane (a loop over MAX_EPL with the e < E guard
+// would add only -inf candidates and +0 softmax terms: the same bits, more work).
+template <int EPL>
 __global__ void __launch_bounds__(WARPS_R * 32)
 gate_topk_kernel(const float* __restrict__ logits, int T, int E, int k, int norm_topk, float scale,
                  int override_routing, int route_groups, int route_topk_groups, int32_t* __restrict__ topk_idx,
@@ -145,7 +148,7 @@ gate_topk_kernel(const float* __restrict__ logits, int T, int E, int k, int norm
       // logits, local argmax in i order, the same xor-shuffle trees, the same
       // softmax sum order), interleaved so their shuffle / expf latencies overlap:
       // bit-identical to the one-token loop below, which takes the remainder
-      for (; t + GATE_U <= t_end; t += GATE_U) gate_tokens<GATE_U>(logits, t, E, k, norm_topk, scale, topk_idx, topk_w,
+      for (; t + GATE_U <= t_end; t += GATE_U) gate_tokens<GATE_U, EPL>(logits, t, E, k, norm_topk, scale, topk_idx, topk_w,
                                                                   hist_s[warp], lane);
     }
     for (; t < t_end; ++t) {
@@ -156,10 +159,10 @@ gate_topk_kernel(const float* __restrict__ logits, int T, int E, int k, int norm
         }
         continue;
       }
-      float v[MAX_EPL];
+      float v[EPL];
       const float* row = logits + (int64_t)t * E;
 #pragma unroll
-      for (int i = 0; i < MAX_EPL; ++i) {
+      for (int i = 0; i < EPL; ++i) {
         int e = lane + 32 * i;
         v[i] = (e < E) ? row[e] : -INFINITY;
       }
@@ -173,7 +176,7 @@ gate_topk_kernel(const float* __restrict__ logits, int T, int E, int k, int norm
         for (int q = 0; q < route_groups; ++q) {
           float m = -INFINITY;
 #pragma unroll
-          for (int i = 0; i < MAX_EPL; ++i) {
+          for (int i = 0; i < EPL; ++i) {
             const int e = lane + 32 * i;
             if (e < E && e / gsz == q) m = fmaxf(m, v[i]);
           }
@@ -196,7 +199,7 @@ gate_topk_kernel(const float* __restrict__ logits, int T, int E, int k, int norm
           if (lane == bg) used = true;
         }
 #pragma unroll
-        for (int i = 0; i < MAX_EPL; ++i) {
+        for (int i = 0; i < EPL; ++i) {
           const int e = lane + 32 * i;
           if (e < E && !((keep >> (e / gsz)) & 1u)) taken |= 1u << i;
         }
@@ -207,7 +210,7 @@ gate_topk_kernel(const float* __restrict__ logits, int T, int E, int k, int norm
         float bv = -INFINITY;
         int be = 0x7fffffff;
 #pragma unroll
-        for (int i = 0; i < MAX_EPL; ++i) {
+        for (int i = 0; i < EPL; ++i) {
           int e = lane + 32 * i;
           if (e < E && !((taken >> i) & 1u) && better(v[i], e, bv, be)) { bv = v[i]; be = e; }
         }
@@ -225,7 +228,7 @@ gate_topk_kernel(const float* __restrict__ logits, int T, int E, int k, int norm
       const float m = top_v[0];
       float s = 0.f;
 #pragma unroll
-      for (int i = 0; i < MAX_EPL; ++i) s += expf(v[i] - m);   // -inf lanes add 0
+      for (int i = 0; i < EPL; ++i) s += expf(v[i] - m);   // -inf lanes add 0
 #pragma unroll
       for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
       float psel = 0.f;
@@ -549,11 +552,20 @@ int launch_gate_topk(const float* logits, int T, int E, int k, int norm_topk, fl
   int R = num_ranges(T);
   if (R == 0) return 0;
   if (route_groups <= 1 || route_topk_groups >= route_groups) route_groups = 0;  // unrestricted
-  gate_topk_kernel<<<(R + WARPS_R - 1) / WARPS_R, WARPS_R * 32, 0, st>>>(logits, T, E, k, norm_topk, scale,
-                                                                         override_routing, route_groups,
-                                                                         route_topk_groups, topk_idx, topk_w,
-                                                                         range_hist, R, range_len(T),
-                                                                         gate_interleave());
+  const dim3 grid((R + WARPS_R - 1) / WARPS_R), block(WARPS_R * 32);
+  const int rt = range_len(T), il = gate_interleave();
+#define EPSMOE_GATE_CASE(n)                                                                                \
+  case n:                                                                                                  \
+    gate_topk_kernel<n><<<grid, block, 0, st>>>(logits, T, E, k, norm_topk, scale, override_routing,        \
+                                                route_groups, route_topk_groups, topk_idx, topk_w,         \
+                                                range_hist, R, rt, il);                                    \
+    break;
+  switch ((E + 31) / 32) {
+    EPSMOE_GATE_CASE(1) EPSMOE_GATE_CASE(2) EPSMOE_GATE_CASE(3) EPSMOE_GATE_CASE(4)
+    EPSMOE_GATE_CASE(5) EPSMOE_GATE_CASE(6) EPSMOE_GATE_CASE(7) EPSMOE_GATE_CASE(8)
+    default: return (int)cudaErrorInvalidValue;
+  }
+#undef EPSMOE_GATE_CASE
   return (int)cudaGetLastError();
 }
 
