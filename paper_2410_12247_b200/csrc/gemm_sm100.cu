@@ -74,7 +74,8 @@ struct KParams {
   int diag;       // diagnostics only (EPSMOE_GEMM_DIAG): 1 skip output stores, 2 skip TMEM loads + stores,
                   // 3 bulk stores into a 256-row window (L2-resident: same store traffic, no DRAM writes)
   int tma_store;  // bf16 outputs: full 32-row warp slices leave through TMA bulk-tensor stores (tmO)
-  int half_tiles;  // CTA pairs: a group's last m-tile with <= 128 rows runs as an M = 128 2-CTA MMA (see kernel)
+  int half_tiles;
+  int n_mma;       // MMA N: BN, or for EPI_F32 (the router, N = E) E rounded up to 16 - no 256-column padding  // CTA pairs: a group's last m-tile with <= 128 rows runs as an M = 128 2-CTA MMA (see kernel)
   int64_t ldo;
   void* out;
   const float* bias;
@@ -419,7 +420,8 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
           const uint32_t a_dst = ptx::smem_u32(sA + stage * C::A_BYTES);
           const uint32_t b_dst = ptx::smem_u32(sB + stage * C::B_BYTES);
           if ((CG == 1 || rank == 0) && lane == 0)
-            ptx::mbar_arrive_expect_tx(fb, CG * ((GATHER ? 0 : (half ? C::A_BYTES / 2 : C::A_BYTES)) + C::B_BYTES));
+            ptx::mbar_arrive_expect_tx(fb, CG * ((GATHER ? 0 : (half ? C::A_BYTES / 2 : C::A_BYTES)) +
+                                                 (EPI == EPI_F32 ? (p.n_mma / CG) * BK * 2 : C::B_BYTES)));
           if constexpr (GATHER) {
             // A by 16-B cp.async straight into the 128-B swizzle (chunk c of row r at
             // c ^ (r & 7)): 4 rows x 128 B per warp instruction, no TMA descriptor per row
@@ -456,7 +458,8 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
           } else {
             // SwiGLU: CTA0 gate rows -> acc cols [0,128); CTA1 up rows -> [128,256)
             const void* tb = (EPI == EPI_SWIGLU && rank == 1) ? (const void*)&tmB1 : (const void*)&tmB0;
-            const int brow = (EPI == EPI_SWIGLU) ? b_row0 : b_row0 + (int)rank * C::B_ROWS;
+            const int brow = (EPI == EPI_SWIGLU) ? b_row0
+                             : b_row0 + (int)rank * (EPI == EPI_F32 ? p.n_mma / 2 : C::B_ROWS);
             ptx::tma_load_2d_pair(b_dst, tb, fb, kb * BK, brow);
           }
           if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
@@ -472,7 +475,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
       while (true) {
         const int t = tk.consume(true);
         if (t < 0) break;
-        uint32_t idesc = idesc_full;
+        uint32_t idesc = (EPI == EPI_F32) ? ptx::idesc_bf16_f32(C::TILE_M, p.n_mma) : idesc_full;
         if (HALF_OK && p.half_tiles) {
           int g, mt, nt;
           decode_tile(st, G, n_tiles, p.raster_gm, t, g, mt, nt);
@@ -703,10 +706,11 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
         float* out = reinterpret_cast<float*>(p.out) + grow * p.ldo;
 #pragma unroll 1
         for (int c = 0; c < BN / 32; ++c) {
+          const int col0 = nt * BN + c * 32;
+          if (col0 >= p.N) break;  // warp-uniform; columns past n_mma were never computed
           uint32_t r[32];
           ptx::tmem_ld32(taddr + c * 32, r);
           ptx::tmem_wait_ld();
-          const int col0 = nt * BN + c * 32;
           if (valid) {
 #pragma unroll
             for (int i = 0; i < 32; ++i) {
@@ -849,7 +853,9 @@ int launch_epi(const GemmArgs& a, cudaStream_t stream) {
     attr_set = true;
   }
   CUtensorMap tA, tB0, tB1, tB0h, tB1h, tAh;
-  const int b_box = (EPI == EPI_SWIGLU || CG == 2) ? 128 : 256;
+  // router (EPI_F32, N = E in one n-tile): the MMA covers E rounded up to 16 columns
+  const int n_mma = (EPI == EPI_F32 && a.N <= BN && !env_int("EPSMOE_ROUTER_NFULL", 0)) ? ((a.N + 15) & ~15) : BN;
+  const int b_box = (EPI == EPI_F32) ? n_mma / CG : (EPI == EPI_SWIGLU || CG == 2) ? 128 : 256;
   if (!make_tmap(&tA, a.A, a.a_rows, a.K, GATHER ? 1 : BM)) return (int)cudaErrorInvalidValue;
   if (!make_tmap(&tB0, a.B0, a.b_rows, a.K, b_box)) return (int)cudaErrorInvalidValue;
   if (EPI == EPI_SWIGLU) {
@@ -895,6 +901,7 @@ int launch_epi(const GemmArgs& a, cudaStream_t stream) {
   p.comb_w = a.comb_w;
   p.comb_k = a.comb_k;
   p.diag = env_int("EPSMOE_GEMM_DIAG", 0);
+  p.n_mma = n_mma;
   p.half_tiles = (CG == 2 && !GATHER && (EPI == EPI_SWIGLU || EPI == EPI_BF16) && a.row_mode == 0) ? half_env : 0;
   CUtensorMap tO;
   std::memset(&tO, 0, sizeof(tO));
