@@ -17,7 +17,7 @@ import oracle
 from gen import Inputs
 from paper_2410_12247_b200 import MOE_GEMM_DENSE, MOE_GEMM_GROUPED, LocalGroup, MoELayer, make_plan
 
-from .gpu_util import assert_close, dev_bf16, to_f32
+from .gpu_util import assert_close, dev_bf16
 
 pytestmark = pytest.mark.gpu
 

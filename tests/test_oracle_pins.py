@@ -11,7 +11,7 @@ import pytest
 import torch
 
 import oracle
-from gen import Inputs, f32_to_bf16_bits
+from gen import Inputs
 
 GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
 
