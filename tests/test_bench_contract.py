@@ -6,6 +6,8 @@ import os
 import subprocess
 import sys
 
+import pytest
+
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
@@ -35,3 +37,24 @@ def test_reference_arm_non_zero_rank_is_silent():
     lines = _run(["--impl", "reference", "--steps", "1", "--warmup", "0", "--config", "tiny", "--gpus", "2"],
                  env={"RANK": "1", "WORLD_SIZE": "2", "LOCAL_RANK": "1"})
     assert lines == []
+
+
+@pytest.mark.gpu
+def test_our_arm_json_line_tiny():
+    """Our arm at the tiny config on one GPU: the driver contract's keys, the
+    roofline / cpu_baseline / e2e / clocks objects, and a positive launch count."""
+    lines = _run(["--config", "tiny", "--steps", "5", "--warmup", "3", "--e2e-steps", "2"])
+    assert len(lines) == 1
+    d = lines[0]
+    for key in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+                "scaling", "vs_baseline", "dtype", "data", "config", "roofline", "cpu_baseline", "e2e",
+                "gpu_launches", "clocks"):
+        assert key in d, key
+    assert d["n_gpus"] == 1 and d["steps"] == 5 and d["warmup"] == 3 and d["value"] > 0
+    assert d["config"]["workload"] == "tiny"
+    r = d["roofline"]
+    for key in ("bound", "achieved", "peak", "unit", "frac", "traffic"):
+        assert key in r, key
+    assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["value"] > 0
+    assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
+    assert d["gpu_launches"] > 0
