@@ -683,13 +683,21 @@ moe_status_t moe_exchange_layout(const moe_config_t* cfg, const moe_plan_t* plan
   return MOE_OK;
 }
 
+// Persistent GEMM grid of a forward (the SM partition, NEXT-1): all SMs
+// at ep == 1 and on the copy-engine plane; else 2 * comm_ctas SMs are left to
+// the all2all's kernels (NCCL's two communicators, or the put kernels).
+static int gemm_sm_budget(const moe_layer* L) {
+  if (L->cfg.ep == 1 || L->cfg.a2a_p2p == 2) return L->num_sms;
+  return L->num_sms - 2 * L->comm_ctas;
+}
+
 moe_status_t moe_plan_pipeline(const moe_layer_t* L, int64_t global_tokens, const int32_t* global_hist,
                                moe_plan_t* out) {
   if (!L || !out) return MOE_ERR_INVALID;
   int r = plan_compute(L->cfg, L->cost, global_tokens, global_hist, out);
   if (r == MOE_OK && L->cfg.ep > 1) {  // SM partition of this layer (NEXT-1)
     out->comm_ctas = L->comm_ctas;
-    out->sm_gemm = L->num_sms - 2 * L->comm_ctas;
+    out->sm_gemm = gemm_sm_budget(L);
   }
   return (moe_status_t)r;
 }
@@ -1576,8 +1584,10 @@ moe_status_t moe_layer_forward(moe_layer_t* L, const void* x, int64_t T, void* y
   }
   // GEMM SM budget (A15, Table IV): a persistent GEMM owns every SM
   // it runs on (~220 KB smem), so at ep > 1 it must leave SMs for the two
-  // communicators' kernels or the all2all could not overlap it at all.
-  const int default_ctas = (D > 1) ? L->num_sms - 2 * L->comm_ctas : L->num_sms;
+  // communicators' kernels or the all2all could not overlap it at all.  The
+  // copy-engine plane moves rows without SMs (its flag / wait kernels are one
+  // warp and co-reside), so there the GEMMs keep every SM.
+  const int default_ctas = gemm_sm_budget(L);
   int num_ctas = (plan_in && plan.sm_gemm > 0) ? std::min(plan.sm_gemm, L->num_sms) : default_ctas;
 
   Fwd F{L, x, T, y, plan_in, st, dbg, plan};
