@@ -98,6 +98,7 @@ struct moe_layer {
   int fuse_combine = 0;
   static constexpr int COMB_PIECES = 4;
   cudaEvent_t ev_piece[COMB_PIECES] = {};
+  bool ce_batch = true;           // copy-engine plane: cudaMemcpyBatchAsync per chunk (cleared if unsupported)
   bool overlap_shared = true;     // shared experts on s_side, concurrent with routing (EPSMOE_OVERLAP_SHARED=0: in order)
   bool split_rem = false;         // EPSMOE_SPLIT_REM=1: expert GEMMs as bulk on CTA pairs + remainder rows on
                                   // single CTAs; measured 1-3% slower than padding (DSv2, Mixtral), so off
@@ -1309,8 +1310,30 @@ moe_status_t fwd_ep(Fwd& F) {
       // moves a row), then one thread raises the chunk's flags after them
       const auto* hs = reinterpret_cast<const epsmoe::P2PSeg*>(L->p2p_host) + slot * moe_layer::P2P_MAXS;
       const auto* hp = reinterpret_cast<const int64_t*>(L->p2p_host + P2P_SEGS_BYTES) + slot * (moe_layer::P2P_MAXS + 1);
-      for (int i = 0; i < p2p_nseg[dir][ch]; ++i)
-        CUDA_TRY(cudaMemcpyAsync(hs[i].dst, hs[i].src, (size_t)(hp[i + 1] - hp[i]) * 16, cudaMemcpyDeviceToDevice, ps));
+      // one batched call for the chunk's segments (cudaMemcpyBatchAsync, CUDA 12.8+),
+      // else one cudaMemcpyAsync per segment
+      const int n = p2p_nseg[dir][ch];
+      if (n > 0) {
+        std::vector<void*> dsts(n), srcs(n);
+        std::vector<size_t> sizes(n);
+        for (int i = 0; i < n; ++i) {
+          dsts[i] = hs[i].dst;
+          srcs[i] = const_cast<uint4*>(hs[i].src);
+          sizes[i] = (size_t)(hp[i + 1] - hp[i]) * 16;
+        }
+        cudaMemcpyAttributes attr;
+        std::memset(&attr, 0, sizeof(attr));
+        attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
+        size_t attr_idx = 0, fail_idx = 0;
+        if (L->ce_batch && cudaMemcpyBatchAsync(dsts.data(), srcs.data(), sizes.data(), (size_t)n, &attr, &attr_idx, 1,
+                                                &fail_idx, ps) != cudaSuccess) {
+          (void)cudaGetLastError();
+          L->ce_batch = false;  // not supported here: per-segment copies from now on
+          for (int i = 0; i < n; ++i) CUDA_TRY(cudaMemcpyAsync(dsts[i], srcs[i], sizes[i], cudaMemcpyDeviceToDevice, ps));
+        } else if (!L->ce_batch) {
+          for (int i = 0; i < n; ++i) CUDA_TRY(cudaMemcpyAsync(dsts[i], srcs[i], sizes[i], cudaMemcpyDeviceToDevice, ps));
+        }
+      }
       KERNEL_TRY(launch_p2p_signal(dfp, D, epoch, ps));
       TR_TRY(L->tr->p2p_after_put((int)slot, ps));
       return MOE_OK;
