@@ -50,7 +50,9 @@ def parse():
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-sample", type=int, default=0, help="oracle sample tokens (0 = auto)")
-    p.add_argument("--e2e-steps", type=int, default=10)
+    p.add_argument("--e2e-steps", type=int, default=30,
+                   help="host-buffer steps timed for e2e (the first step's H2D cannot overlap earlier compute; "
+                        "more steps amortise that pipeline fill)")
     p.add_argument("--seed", type=int, default=20241016)
     p.add_argument("--dispatch-fp8", action="store_true", help="FP8 e4m3 dispatch payload (NEXT-2, R15)")
     p.add_argument("--local-reduce", action="store_true", help="expert-side LocalReduce + dedup (NEXT-3, R16)")
@@ -496,6 +498,7 @@ def ours(args, cfg):
     e2e_ms = float(te.item()) / args.e2e_steps
     e2e = {"value": T / (e2e_ms / 1e3), "unit": UNIT, "ms_per_step": e2e_ms,
            "h2d_bytes_per_step": int(T_loc * H * 2), "d2h_bytes_per_step": int(T_loc * H * 2),
+           "steps": args.e2e_steps,
            "api": "moe_layer_forward_host_async x steps + moe_layer_host_sync (pinned host x/y; calls overlap)"}
 
     stages = {n: round(v / args.steps, 4) for n, v in stage_sum.items()}
