@@ -135,8 +135,12 @@ typedef struct {
                            slice c % S); the forward then exchanges the
                            (expert, slice) counts once more                    */
   int32_t gemm_kind;    /* moe_gemm_kind_t applied to all experts (AUTO: see below) */
-  int32_t sm_gemm;      /* persistent GEMM grid (0 = all SMs)           P:492, A15 */
-  int32_t comm_ctas;    /* NCCL maxCTAs per communicator (0 = default) */
+  int32_t sm_gemm;      /* persistent GEMM grid (0 = all SMs); at ep > 1 every
+                           persistent GEMM grid of the forward together stays
+                           within it (one grid resident at a time when it is
+                           below the SM count)              P:492, A15, NEXT-1 */
+  int32_t comm_ctas;    /* NCCL maxCTAs per communicator / put-kernel CTAs per
+                           direction / 2 (0 = the layer's default) */
   int32_t group_begin[MOE_MAX_CHUNKS + 1]; /* local-expert group bounds (R8),
                                               [0 .. PN / token_slices]        */
   uint8_t expert_kind[MOE_MAX_EXPERTS];    /* resolved kind per local expert      */
@@ -152,9 +156,16 @@ typedef struct {
 
 /* Measured cost model behind moe_plan_pipeline (calibrated on B200 by
  * moe_layer_calibrate, or supplied by the caller).  GEMM time of one expert
- * with m rows is linear-interpolated in m from `m_points`; all2all time is
- * a2a_fixed_ms + bytes / a2a_gbps; per-chunk overhead R(N) = k*N + b. */
+ * with m rows is linear-interpolated in m from `m_points` (all SMs); all2all
+ * time is a2a_fixed_ms + wire bytes / GB/s; per-chunk overhead R(N) = k*N + b.
+ * The SM partition (Table IV; NEXT-1): candidate
+ * comm budgets comm_ctas[i] (CTAs per communicator / put direction), each with
+ * its measured all2all rate a2a_gbps_at[i] and the factor gemm_scale_at[i] by
+ * which the expert GEMMs slow down on the num_sms - 2 * comm_ctas[i] SMs left
+ * to them.  n_comm = 0: one candidate, the layer's default budget, at a2a_gbps
+ * with proportional GEMM scaling. */
 #define MOE_COST_POINTS 12
+#define MOE_COMM_POINTS 4
 typedef struct {
   int32_t n_points;
   float m_points[MOE_COST_POINTS];          /* rows per expert, ascending       */
@@ -164,6 +175,11 @@ typedef struct {
   float a2a_gbps;                           /* effective per-rank GB/s         */
   float k_ms;                               /* R(N) slope         */
   float b_ms;                               /* R(N) intercept         */
+  int32_t num_sms;                          /* SMs of the measured device (0 = 148) */
+  int32_t n_comm;                           /* comm-budget candidates (<= 4)   */
+  int32_t comm_ctas[MOE_COMM_POINTS];       /* CTAs per communicator           */
+  float a2a_gbps_at[MOE_COMM_POINTS];       /* all2all GB/s at that budget     */
+  float gemm_scale_at[MOE_COMM_POINTS];     /* GEMM time factor on the SMs left */
 } moe_cost_model_t;
 
 /* Debug / test hooks (NULL in benchmarks).  All array pointers are DEVICE
@@ -191,6 +207,14 @@ typedef struct {
                                sends to [0][c] / receives from [1][c] each
                                peer in chunk c < PN (dedup rows under
                                local_reduce)                                 */
+  void* combine_in;         /* out [T_loc * topk, H] bf16 (local_reduce = 0):
+                               the expert outputs o the weighted unpermute
+                               reads, at the send rows (row pos[t][j] holds
+                               o_{t,j}), for the stage-wise combine check     */
+  int32_t* gemm_resident;   /* out [2] int32 (zeroed by the caller): the
+                               persistent GEMM CTAs of this forward count
+                               themselves in [0] while resident and record
+                               the maximum in [1] (SM-partition probe)       */
 } moe_debug_t;
 
 /* ---------------------------------------------------------------- lifecycle */
@@ -216,6 +240,19 @@ moe_status_t moe_layer_create(const moe_config_t* cfg, const moe_weights_t* w,
 
 moe_status_t moe_layer_destroy(moe_layer_t* layer);
 
+/* Create the layer with the caller's blocking HOST allgather in place of
+ * NCCL: allgather(ctx, send, recv, bytes) must write rank r's `bytes` bytes at
+ * recv + r * bytes on every rank (collective, same call order; 0 = success).
+ * It carries the count exchange and the one-time cudaIpc mapping of the
+ * workspaces; routed rows move only on the layer's peer-memory planes, so
+ * cfg->a2a_p2p must be 1 or 2 (else MOE_ERR_INVALID).  One process per rank
+ * (ranks may share a GPU: separate contexts, real mappings and device flags).
+ * `workspace` must be a cudaMalloc allocation (or inside one). */
+typedef int (*moe_host_allgather_fn)(void* ctx, const void* send, void* recv, size_t bytes);
+moe_status_t moe_layer_create_hostcoll(const moe_config_t* cfg, const moe_weights_t* w,
+                                       moe_host_allgather_fn allgather, void* ctx, void* workspace,
+                                       size_t workspace_bytes, moe_layer_t** out);
+
 /* In-process EP group for tests on ONE GPU: the ep ranks are ep layer objects
  * of one process, each driven by its own host thread; the all2all becomes
  * host-rendezvous + device-to-device copies (same forward code as NCCL).
@@ -230,7 +267,12 @@ moe_status_t moe_layer_create_local(const moe_config_t* cfg, const moe_weights_t
 /* Pure, host-only, deterministic: the expert pipeline scheduler.
  *   N = argmax_{1<=N<=E_loc} min(T_comm, T_comp)(N-1)/N - (kN + b)  (P:408-415,
  *       ties -> smaller N), T_comm / T_comp from the cost model for the
- *       max-loaded rank;
+ *       max-loaded rank; T_comm prices the wire bytes: FP8 dispatch rows
+ *       (H + H/128, padded to 16 B, R15), bf16 combine rows, and under
+ *       local_reduce the expected dedup rows of N chunks (R16);
+ *   ep > 1: (sm_gemm, comm_ctas) = the comm-budget candidate minimising the
+ *       modelled pipelined layer time T_comp + T_comm - G(N) (NEXT-1; the
+ *       copy-engine plane reserves no SMs);
  *   kind_e = argmin over {GROUPED, DENSE} of the modelled expert time (A8);
  *   group_begin = balanced contiguous expert groups (R8).
  * `global_hist` is HOST [ep, e] (pairs per rank and expert) or NULL for

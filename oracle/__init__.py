@@ -11,6 +11,6 @@ Pinned by tests/test_oracle_pins.py (no function is "parity unpinned").
 """
 from .moe import (bf16_bits_to_f64, bf16_value_to_bits, chunk_groups, chunk_send_counts,  # noqa: F401
                   combine, dispatch_layout, expert_ffn, fmaf, fp8_block_exponent, fp8_dispatch_roundtrip,
-                  local_reduce_combine, lr_group_ids, lr_layout, moe_layer, moe_tokens, round_bf16,
+                  local_reduce_combine, lr_group_ids, lr_layout, moe_layer, moe_tokens, round_bf16, slice_ranges,
                   router_logits, silu_f32, token_shards, topk_gating)
 from .planner import activated_experts, pn_gain, pn_optimum_closed_form, pn_optimum_grid  # noqa: F401

@@ -37,7 +37,10 @@ chunked == unchunked, EP=D == EP=1; FP8 codec vs the e4m3 format definition;
 LocalReduce (R16): the worked example's dedup counts by hand, exact-mode
 regrouping identity, single-group special case, the hypergeometric
 distinct-rank closed form; device-limited routing (R17): a hand fixture, the
-M = groups special case; the P:265 all2all volume bounds.
+M = groups special case; the P:265 all2all volume bounds; chunk groups vs the
+SURVEY §8(c) table, token slices / shards / sliced send counts vs hand tables
+(tests/golden/chunk_rules.json); the contract combine vs an exact-rational
+fmaf chain with crafted tokens that expose s-last and mul+add.
 """
 from __future__ import annotations
 
@@ -177,6 +180,10 @@ def topk_gating(logits, k, norm_topk, routed_scale=1.0, mode="contract", route_g
     largest logit; only the experts of the route_topk_groups best groups
     (score desc, group id asc) are eligible for the top-k above.  The softmax
     still runs over all E.
+
+    A NaN logit (from NaN / Inf inputs only) ranks as -inf: never selected
+    ahead of a number, 0 in the softmax (R18).  A row of NaNs selects experts
+    0..k-1 and gets NaN weights (its max is -inf).
     """
     logits = np.asarray(logits)
     T, E = logits.shape
@@ -189,6 +196,7 @@ def topk_gating(logits, k, norm_topk, routed_scale=1.0, mode="contract", route_g
         groups = np.arange(route_groups)
     for t in range(T):
         row = logits[t].astype(np.float64)
+        row = np.where(np.isnan(row), -np.inf, row)  # a NaN logit ranks as -inf (R18)
         order = np.lexsort((experts, -row))          # primary: -logit, secondary: e
         if limited:
             score = row.reshape(route_groups, gsz).max(axis=1)

@@ -16,6 +16,7 @@ MOE_MAX_EXPERTS = 256
 MOE_MAX_TOPK = 8
 MOE_MAX_CHUNKS = 64
 MOE_COST_POINTS = 12
+MOE_COMM_POINTS = 4
 
 MOE_GEMM_AUTO, MOE_GEMM_GROUPED, MOE_GEMM_DENSE = 0, 1, 2
 STAGES = ["router", "route", "shared", "gateup", "down", "combine", "dispatch_a2a", "combine_a2a", "total",
@@ -60,7 +61,9 @@ class moe_plan_t(C.Structure):
 class moe_cost_model_t(C.Structure):
     _fields_ = [("n_points", C.c_int32), ("m_points", C.c_float * MOE_COST_POINTS),
                 ("gemm_ms", (C.c_float * MOE_COST_POINTS) * 2), ("a2a_fixed_ms", C.c_float),
-                ("a2a_gbps", C.c_float), ("k_ms", C.c_float), ("b_ms", C.c_float)]
+                ("a2a_gbps", C.c_float), ("k_ms", C.c_float), ("b_ms", C.c_float),
+                ("num_sms", C.c_int32), ("n_comm", C.c_int32), ("comm_ctas", C.c_int32 * MOE_COMM_POINTS),
+                ("a2a_gbps_at", C.c_float * MOE_COMM_POINTS), ("gemm_scale_at", C.c_float * MOE_COMM_POINTS)]
 
 
 class moe_debug_t(C.Structure):
@@ -68,7 +71,8 @@ class moe_debug_t(C.Structure):
                 ("topk_w", C.c_void_p), ("pos", C.c_void_p), ("hist", C.c_void_p),
                 ("seg_start", C.c_void_p), ("shared_out", C.c_void_p),
                 ("global_hist_host", C.c_void_p), ("plan_used", C.POINTER(moe_plan_t)),
-                ("lr_pos", C.c_void_p), ("lr_hist", C.c_void_p), ("chunk_rows_host", C.c_void_p)]
+                ("lr_pos", C.c_void_p), ("lr_hist", C.c_void_p), ("chunk_rows_host", C.c_void_p),
+                ("combine_in", C.c_void_p), ("gemm_resident", C.c_void_p)]
 
 
 _SIGS = {
@@ -77,6 +81,8 @@ _SIGS = {
     "moe_layer_create": (C.c_int, [C.POINTER(moe_config_t), C.POINTER(moe_weights_t), C.c_void_p, C.c_void_p,
                                    C.c_void_p, C.c_size_t, C.POINTER(C.c_void_p)]),
     "moe_layer_destroy": (C.c_int, [C.c_void_p]),
+    "moe_layer_create_hostcoll": (C.c_int, [C.POINTER(moe_config_t), C.POINTER(moe_weights_t), C.c_void_p,
+                                            C.c_void_p, C.c_void_p, C.c_size_t, C.POINTER(C.c_void_p)]),
     "moe_local_group_create": (C.c_int, [C.c_int32, C.POINTER(C.c_void_p)]),
     "moe_local_group_destroy": (C.c_int, [C.c_void_p]),
     "moe_layer_create_local": (C.c_int, [C.POINTER(moe_config_t), C.POINTER(moe_weights_t), C.c_void_p,
@@ -122,6 +128,10 @@ def lib():
             f.argtypes = args
         _LIB = L
     return _LIB
+
+
+# int allgather(void* ctx, const void* send, void* recv, size_t bytes)
+HOST_ALLGATHER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t)
 
 
 class EpsMoeError(RuntimeError):

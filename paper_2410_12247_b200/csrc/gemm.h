@@ -67,6 +67,9 @@ struct GemmArgs {
   uint32_t* const* sig_flags;
   int nsig;
   uint32_t sig_epoch;
+  // optional SM-partition probe (device int32[2]): each CTA adds itself to [0]
+  // while resident and records the running maximum in [1]
+  int32_t* resident;
 };
 
 // Launch on `stream`.  Returns a cudaError_t-compatible code (0 = success).

@@ -93,6 +93,7 @@ struct KParams {
   const int32_t* comb_pos;
   const float* comb_w;
   int comb_k;
+  int32_t* resident;  // SM-partition probe (GemmArgs::resident) or nullptr
 };
 
 constexpr int COMB_MAX_K = 8;
@@ -299,6 +300,8 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
   // tmB0h / tmB1h) so that a warp sees matching gate and up columns; A comes
   // as 64-row boxes (tmAh), so a half tile also moves 25% fewer bytes.
   constexpr bool HALF_OK = (CG == 2) && !GATHER && (EPI == EPI_SWIGLU || EPI == EPI_BF16);
+  // SM-partition probe: this CTA is resident from here to the end of the kernel
+  if (p.resident && threadIdx.x == 0) atomicMax(p.resident + 1, atomicAdd(p.resident, 1) + 1);
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
@@ -736,7 +739,9 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
     }
   }
 
-  if (p.nsig) __threadfence_system();  // scattered rows visible to the peers before the flags
+  // scattered rows visible to the peers before this launch ends (flags raised by
+  // this launch's last CTA, or by a later stream-ordered launch: DENSE chunks)
+  if (p.nsig || p.rseg) __threadfence_system();
   ptx::tc_fence_before();
   __syncthreads();
   if constexpr (CG == 2) ptx::cluster_sync();  // no CTA leaves while its peer may still signal it
@@ -758,6 +763,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
       __threadfence();
     }
   }
+  if (p.resident && threadIdx.x == 0) atomicSub(p.resident, 1);
 }
 
 // ------------------------------------------------------------------ host side
@@ -900,6 +906,7 @@ int launch_epi(const GemmArgs& a, cudaStream_t stream) {
   p.comb_pos = a.comb_pos;
   p.comb_w = a.comb_w;
   p.comb_k = a.comb_k;
+  p.resident = a.resident;
   p.diag = env_int("EPSMOE_GEMM_DIAG", 0);
   p.n_mma = n_mma;
   p.half_tiles = (CG == 2 && !GATHER && (EPI == EPI_SWIGLU || EPI == EPI_BF16) && a.row_mode == 0) ? half_env : 0;

@@ -9,6 +9,7 @@
 //                    into S token slices (N = E_loc * S, R8 extension)
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -58,6 +59,34 @@ void default_cost_model(const moe_config_t& cfg, moe_cost_model_t* c) {
   c->a2a_gbps = 700.0f;   // measured peer copy ~770 GB/s per direction (B200_PROFILING.md)
   c->k_ms = 0.015f;       // per-chunk fixed overhead (two NCCL groups + events)
   c->b_ms = 0.0f;
+  // one comm budget (the layer's default; EPSMOE_COMM_CTAS) at a2a_gbps, the
+  // GEMMs slowed in proportion to the SMs they give up
+  c->num_sms = 148;
+  c->n_comm = 1;
+  c->comm_ctas[0] = default_comm_ctas();
+  c->a2a_gbps_at[0] = c->a2a_gbps;
+  c->gemm_scale_at[0] = (float)(148.0 / (148.0 - 2.0 * c->comm_ctas[0]));
+}
+
+int default_comm_ctas() {
+  const char* cv = std::getenv("EPSMOE_COMM_CTAS");
+  return std::max(1, std::min(32, cv ? std::atoi(cv) : 8));
+}
+
+// Expected all2all rows per routed pair under expert-side LocalReduce (R16)
+// with N chunks: a token sends one row per distinct (rank, chunk) group among
+// its k experts.  With G = N * D groups of E / G experts and k distinct experts
+// drawn uniformly, a group is missed with probability
+// q = C(E - E/G, k) / C(E, k), so the token's remote groups number
+// (G - N)(1 - q) on average (its own rank's N groups need no transfer), against
+// k (D - 1) / D remote pairs.  (N = 1: D(1 - q) rows, the closed form of R16.)
+double lr_rows_per_pair(int E, int D, int k, int N) {
+  if (D <= 1) return 1.0;
+  const double G = (double)N * D, s = (double)E / G;
+  double q = 1.0;
+  for (int i = 0; i < k; ++i) q *= std::max(0.0, (E - s - i) / (double)(E - i));
+  const double remote_pairs = k * (D - 1.0) / D;
+  return (G - N) * (1.0 - q) / remote_pairs;
 }
 
 static void balanced_groups(int e_loc, int n, int32_t* begin) {
@@ -103,9 +132,9 @@ int plan_compute(const moe_config_t& cfg, const moe_cost_model_t& cost, int64_t 
     for (int r = 0; r < D; ++r) { send_rows[r] = cross; recv_rows[r] = cross; }
   }
 
-  // per-expert kind (A8) and per-rank modelled compute; the plan follows the
-  // max-loaded rank so every rank derives the same plan from the same input.
-  double t_comp = 0.0;
+  // per-expert kind (A8) and per-rank modelled compute on all SMs; the plan
+  // follows the max-loaded rank so every rank derives the same plan.
+  double t_comp_all = 0.0;
   for (int d = 0; d < D; ++d) {
     double t = 0.0;
     for (int el = 0; el < E_loc; ++el) {
@@ -115,41 +144,73 @@ int plan_compute(const moe_config_t& cfg, const moe_cost_model_t& cost, int64_t 
       t += std::min(tg, td);
       if (d == cfg.rank) out->expert_kind[el] = (uint8_t)(td < tg ? MOE_GEMM_DENSE : MOE_GEMM_GROUPED);
     }
-    t_comp = std::max(t_comp, t);
+    t_comp_all = std::max(t_comp_all, t);
   }
-  double t_comm = 0.0;
-  if (D > 1) {
-    double bytes = 0.0;
-    for (int d = 0; d < D; ++d) bytes = std::max(bytes, std::max(send_rows[d], recv_rows[d]));
-    bytes *= 2.0 * cfg.hidden;                           // bf16 rows, one direction
-    double one = cost.a2a_fixed_ms + bytes / (cost.a2a_gbps * 1e9) * 1e3;
-    t_comm = 2.0 * one;                                   // dispatch + combine
-  }
-
+  // wire rows of the max-loaded rank in one direction, and the bytes per row:
+  // dispatch FP8 rows (H + H/128 e4m3 + exponents, padded to 16 B; R15) or bf16,
+  // combine always bf16 rows
+  double pairs = 0.0;
+  for (int d = 0; d < D; ++d) pairs = std::max(pairs, std::max(send_rows[d], recv_rows[d]));
+  const double disp_row = cfg.dispatch_fp8 ? (double)(((cfg.hidden + cfg.hidden / 128) + 15) & ~15)
+                                           : 2.0 * cfg.hidden;
+  const double comb_row = 2.0 * cfg.hidden;
+  // comm budgets: NCCL / put planes give up 2 * comm_ctas SMs; the copy-engine
+  // plane none (its rows move without SMs)
+  const int nsm = cost.num_sms > 0 ? cost.num_sms : 148;
+  int ncand = (D > 1) ? std::max(1, std::min(cost.n_comm, (int)MOE_COMM_POINTS)) : 1;
+  const bool ce = cfg.a2a_p2p == 2;
+  if (ce) ncand = 1;
   // pipeline number over N = 1..E_loc, then N = E_loc * S token-
-  // sliced chunks (S = 2..slice_max, R8 extension); ties -> smaller N
-  const double C = std::min(t_comm, t_comp);
+  // sliced chunks (S = 2..slice_max, R8 extension), for every comm budget;
+  // the pair with the smallest modelled layer time T_comp + T_comm - G(N)
+  // wins (ties -> smaller N, then the first budget).  For one budget and a
+  // wire size independent of N this is the paper's argmax of G(N).
   const int n_max = std::min(E_loc, MOE_MAX_CHUNKS);
-  int best_n = 1;
-  double best_v = -(cost.k_ms * 1 + cost.b_ms);
-  auto consider = [&](int n) {
-    double v = C / n * (n - 1) - (cost.k_ms * n + cost.b_ms);
-    if (v > best_v) { best_v = v; best_n = n; }
-  };
-  for (int n = 2; n <= n_max; ++n) consider(n);
   const int s_max = (D > 1 && !cfg.local_reduce) ? plan_slice_max(E_loc, global_tokens / D) : 1;
-  for (int s = 2; s <= s_max; ++s) consider(E_loc * s);
+  std::vector<int> cands;
+  for (int n = 1; n <= n_max; ++n) cands.push_back(n);
+  for (int s = 2; s <= s_max; ++s) cands.push_back(E_loc * s);
+  int best_n = 1, best_i = 0;
+  double best_t = 1e300, best_comm = 0.0, best_comp = t_comp_all, best_g = 0.0;
+  for (int i = 0; i < ncand; ++i) {
+    const bool have = cost.n_comm > 0 && i < cost.n_comm;
+    const int cc = (D > 1 && !ce) ? (have ? cost.comm_ctas[i] : default_comm_ctas()) : 0;
+    const double gbps = have && cost.a2a_gbps_at[i] > 0 ? cost.a2a_gbps_at[i] : cost.a2a_gbps;
+    double scale = 1.0;
+    if (cc > 0) scale = (have && cost.gemm_scale_at[i] > 0) ? cost.gemm_scale_at[i] : nsm / (double)(nsm - 2 * cc);
+    const double t_comp = t_comp_all * scale;
+    for (int n : cands) {
+      double t_comm = 0.0;
+      if (D > 1) {
+        const double f = cfg.local_reduce ? lr_rows_per_pair(E, D, k, n) : 1.0;
+        const double bytes = pairs * f * (disp_row + comb_row);
+        t_comm = 2.0 * cost.a2a_fixed_ms + bytes / (gbps * 1e9) * 1e3;  // dispatch + combine
+      }
+      const double C = std::min(t_comm, t_comp);
+      const double g = C / n * (n - 1) - (cost.k_ms * n + cost.b_ms);   // L(theta;N) - R(N)
+      const double t = t_comp + t_comm - g;
+      if (t < best_t - 1e-12) {
+        best_t = t; best_n = n; best_i = i; best_comm = t_comm; best_comp = t_comp; best_g = g;
+      }
+    }
+  }
   out->num_chunks = best_n;
   out->token_slices = best_n > E_loc ? best_n / E_loc : 1;
   balanced_groups(E_loc, best_n / out->token_slices, out->group_begin);
   out->gemm_kind = MOE_GEMM_AUTO;
-  out->sm_gemm = 0;
-  out->comm_ctas = 0;
-  out->pred_comm_ms = (float)t_comm;
-  out->pred_comp_ms = (float)t_comp;
+  if (D > 1 && !ce) {
+    const bool have = cost.n_comm > 0 && best_i < cost.n_comm;
+    out->comm_ctas = have ? cost.comm_ctas[best_i] : default_comm_ctas();
+    out->sm_gemm = nsm - 2 * out->comm_ctas;
+  } else {
+    out->comm_ctas = 0;
+    out->sm_gemm = (D > 1) ? nsm : 0;
+  }
+  out->pred_comm_ms = (float)best_comm;
+  out->pred_comp_ms = (float)best_comp;
   out->pred_k_ms = cost.k_ms;
   out->pred_b_ms = cost.b_ms;
-  out->pred_gain_ms = (float)(C - cost.b_ms - (C / best_n + cost.k_ms * best_n));
+  out->pred_gain_ms = (float)best_g;
   return MOE_OK;
 }
 

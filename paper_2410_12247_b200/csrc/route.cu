@@ -29,6 +29,11 @@ constexpr int MAX_K = 8;    // top_k <= 8
 __device__ __forceinline__ bool better(float av, int ae, float bv, int be) {
   return av > bv || (av == bv && ae < be);
 }
+// A NaN logit (only NaN / Inf inputs make one) ranks as -inf (R18): never ahead of
+// a number, 0 in the softmax sum.  An all-NaN row then still selects k valid
+// experts (the lowest ids: -inf ties) and its weights are NaN (max = -inf), so
+// the token's y is NaN instead of an out-of-range expert index.
+__device__ __forceinline__ float logit_or_neg_inf(float v) { return v != v ? -INFINITY : v; }
 
 // U consecutive tokens of a routing range, unrestricted routing (see the
 // kernel below for the per-token definition; this is the same arithmetic).
@@ -44,7 +49,7 @@ __device__ __forceinline__ void gate_tokens(const float* __restrict__ logits, in
 #pragma unroll
     for (int i = 0; i < EPL; ++i) {
       const int e = lane + 32 * i;
-      v[u][i] = (e < E) ? row[e] : -INFINITY;
+      v[u][i] = (e < E) ? logit_or_neg_inf(row[e]) : -INFINITY;
     }
   }
   uint32_t taken[U];
@@ -164,7 +169,7 @@ gate_topk_kernel(const float* __restrict__ logits, int T, int E, int k, int norm
 #pragma unroll
       for (int i = 0; i < EPL; ++i) {
         int e = lane + 32 * i;
-        v[i] = (e < E) ? row[e] : -INFINITY;
+        v[i] = (e < E) ? logit_or_neg_inf(row[e]) : -INFINITY;
       }
       uint32_t taken = 0;
       if (route_groups) {

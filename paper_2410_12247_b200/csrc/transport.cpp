@@ -4,7 +4,10 @@
 
 #include <cuda.h>
 
+#include <algorithm>
+#include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <string>
 
 #include "../../include/epsmoe.h"
@@ -21,14 +24,19 @@ static int nccl_err(ncclResult_t r, const char* what) {
 
 NcclTransport::~NcclTransport() {
   for (void* p : opened_) cudaIpcCloseMemHandle(p);
-  for (auto c : comm_)
+  for (const Split& s : splits_)
+    for (ncclComm_t c : s.c)
+      if (c) ncclCommDestroy(c);
+  for (auto c : base_)
     if (c) ncclCommDestroy(c);
 }
 
-int NcclTransport::map_peers(void* mine, std::vector<char*>& out) {
-  int nranks = 0, me = 0;
-  if (int e = nccl_err(ncclCommCount(comm_[0], &nranks), "ncclCommCount")) return e;
-  if (int e = nccl_err(ncclCommUserRank(comm_[0], &me), "ncclCommUserRank")) return e;
+// cudaIpc mapping of every rank's `mine` (+ its offset inside its cudaMalloc
+// allocation); `gather(send, recv, bytes)` is a blocking host allgather of
+// `bytes` per rank.  opened: handles to close on teardown.
+static int ipc_map_peers(void* mine, int nranks, int me,
+                         const std::function<int(const void*, void*, size_t)>& gather,
+                         std::vector<void*>& opened, std::vector<char*>& out) {
   // handle of the whole allocation + this pointer's offset inside it
   CUdeviceptr base = 0;
   size_t size = 0;
@@ -50,14 +58,8 @@ int NcclTransport::map_peers(void* mine, std::vector<char*>& out) {
   std::memcpy(rec, &h, sizeof(h));
   const int64_t off = (int64_t)((CUdeviceptr)mine - base);
   std::memcpy(rec + W - 2, &off, sizeof(off));
-  int32_t* dev = nullptr;
-  if (cudaMalloc(&dev, sizeof(int32_t) * W * (nranks + 1)) != cudaSuccess) return MOE_ERR_CUDA;
-  cudaMemcpy(dev, rec, sizeof(rec), cudaMemcpyHostToDevice);
-  int e = allgather_i32(dev, dev + W, W, 0);
   std::vector<int32_t> all((size_t)W * nranks);
-  if (!e) e = cudaMemcpy(all.data(), dev + W, sizeof(int32_t) * W * nranks, cudaMemcpyDeviceToHost) ? MOE_ERR_CUDA : 0;
-  cudaFree(dev);
-  if (e) return e;
+  if (int e = gather(rec, all.data(), sizeof(rec))) return e;
   out.assign(nranks, nullptr);
   for (int r = 0; r < nranks; ++r) {
     if (r == me) { out[r] = (char*)mine; continue; }
@@ -70,10 +72,110 @@ int NcclTransport::map_peers(void* mine, std::vector<char*>& out) {
       set_error("map_peers: cudaIpcOpenMemHandle failed for rank " + std::to_string(r));
       return MOE_ERR_CUDA;
     }
-    opened_.push_back(p);
+    opened.push_back(p);
     out[r] = (char*)p + offr;
   }
   return 0;
+}
+
+int NcclTransport::map_peers(void* mine, std::vector<char*>& out) {
+  int nranks = 0, me = 0;
+  if (int e = nccl_err(ncclCommCount(comm_[0], &nranks), "ncclCommCount")) return e;
+  if (int e = nccl_err(ncclCommUserRank(comm_[0], &me), "ncclCommUserRank")) return e;
+  // the handles travel through a device buffer and one allgather on communicator 0
+  auto gather = [&](const void* send, void* recv, size_t bytes) -> int {
+    char* dev = nullptr;
+    if (cudaMalloc(&dev, bytes * (nranks + 1)) != cudaSuccess) return MOE_ERR_CUDA;
+    cudaMemcpy(dev, send, bytes, cudaMemcpyHostToDevice);
+    int e = nccl_err(ncclAllGather(dev, dev + bytes, bytes, ncclUint8, comm_[0], 0), "ncclAllGather");
+    if (!e) e = cudaMemcpy(recv, dev + bytes, bytes * nranks, cudaMemcpyDeviceToHost) ? MOE_ERR_CUDA : 0;
+    cudaFree(dev);
+    return e;
+  };
+  return ipc_map_peers(mine, nranks, me, gather, opened_, out);
+}
+
+// NEXT-1: the communicators' CTA budget.  ncclCommSplit (color 0, key = rank:
+// same ranks, same order) with maxCTAs = ctas gives communicators with the new
+// SM budget without a new bootstrap; they are kept for reuse.
+int NcclTransport::set_comm_ctas(int ctas) {
+  if (ctas <= 0 || ctas == ctas_) return 0;
+  for (const Split& s : splits_)
+    if (s.ctas == ctas) {
+      comm_[0] = s.c[0];
+      comm_[1] = s.c[1];
+      ctas_ = ctas;
+      return 0;
+    }
+  Split s{ctas, {nullptr, nullptr}};
+  int me = 0;
+  if (int e = nccl_err(ncclCommUserRank(base_[0], &me), "ncclCommUserRank")) return e;
+  for (int i = 0; i < 2; ++i) {
+    ncclConfig_t cfg = NCCL_CONFIG_INITIALIZER;
+    cfg.blocking = 1;
+    cfg.maxCTAs = ctas;
+    cfg.minCTAs = std::min(ctas, 2);
+    if (int e = nccl_err(ncclCommSplit(base_[i], 0, me, &s.c[i], &cfg), "ncclCommSplit")) return e;
+  }
+  splits_.push_back(s);
+  comm_[0] = s.c[0];
+  comm_[1] = s.c[1];
+  ctas_ = ctas;
+  return 0;
+}
+
+int NcclTransport::poll_async() {
+  for (ncclComm_t c : base_) {
+    ncclResult_t r = ncclSuccess;
+    if (c && ncclCommGetAsyncError(c, &r) == ncclSuccess && r != ncclSuccess && r != ncclInProgress)
+      return nccl_err(r, "ncclCommGetAsyncError");
+  }
+  for (const Split& s : splits_)
+    for (ncclComm_t c : s.c) {
+      ncclResult_t r = ncclSuccess;
+      if (c && ncclCommGetAsyncError(c, &r) == ncclSuccess && r != ncclSuccess && r != ncclInProgress)
+        return nccl_err(r, "ncclCommGetAsyncError");
+    }
+  return 0;
+}
+
+// ------------------------------------------------------------------ host collective
+HostCollTransport::~HostCollTransport() {
+  for (void* p : opened_) cudaIpcCloseMemHandle(p);
+}
+
+int HostCollTransport::unsupported() {
+  set_error("host-collective transport: routed rows move only on a2a_p2p = 1 or 2 (no send / recv)");
+  return MOE_ERR_UNSUPPORTED;
+}
+
+int HostCollTransport::gather_host(const void* send, void* recv, size_t bytes) {
+  if (fn_(ctx_, send, recv, bytes) != 0) {
+    set_error("host allgather callback failed");
+    return MOE_ERR_MISMATCH;
+  }
+  return 0;
+}
+
+int HostCollTransport::allgather_i32(const int32_t* send, int32_t* recv, size_t count, cudaStream_t st) {
+  std::vector<int32_t> mine(count), all(count * ep_);
+  if (cudaMemcpyAsync(mine.data(), send, count * sizeof(int32_t), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+      cudaStreamSynchronize(st) != cudaSuccess) {
+    set_error("host-collective allgather: device->host copy failed");
+    return MOE_ERR_CUDA;
+  }
+  if (int e = gather_host(mine.data(), all.data(), count * sizeof(int32_t))) return e;
+  if (cudaMemcpyAsync(recv, all.data(), all.size() * sizeof(int32_t), cudaMemcpyHostToDevice, st) != cudaSuccess ||
+      cudaStreamSynchronize(st) != cudaSuccess) {
+    set_error("host-collective allgather: host->device copy failed");
+    return MOE_ERR_CUDA;
+  }
+  return 0;
+}
+
+int HostCollTransport::map_peers(void* mine, std::vector<char*>& out) {
+  auto gather = [&](const void* send, void* recv, size_t bytes) { return gather_host(send, recv, bytes); };
+  return ipc_map_peers(mine, ep_, rank_, gather, opened_, out);
 }
 
 
@@ -153,10 +255,17 @@ int LocalTransport::map_peers(void* mine, std::vector<char*>& out) {
   return 0;
 }
 
+LocalTransport::LocalTransport(LocalGroup* g, int rank) : g_(g), rank_(rank) {
+  const char* ev = std::getenv("EPSMOE_LOCAL_P2P_EVENTS");
+  order_puts_ = ev ? std::atoi(ev) != 0 : g->ep > 2;
+}
+
 int LocalTransport::p2p_after_put(int slot, cudaStream_t ps) {
+  if (!order_puts_) return 0;
   return cuda_err(cudaEventRecord(g_->ev_put[rank_][slot], ps), "cudaEventRecord");
 }
 int LocalTransport::p2p_before_wait(int slot0, int nslots, cudaStream_t st) {
+  if (!order_puts_) return 0;  // the device flags alone order the rows
   LocalGroup& g = *g_;
   g.barrier();  // every rank has issued (recorded) these puts
   for (int p = 0; p < g.ep; ++p)

@@ -1,5 +1,7 @@
 // All2all transport behind the EP layer.
 //
+//   HostCollTransport — counts over a caller-supplied host allgather, rows
+//                    over the layer's own peer-memory planes only.
 //   NcclTransport  — production: two NCCL communicators over NVLink (channel 0 =
 //                    dispatch, channel 1 = combine) so both phases can be in
 //                    flight; grouped ncclSend/ncclRecv; ncclAllGather of counts.
@@ -18,6 +20,8 @@
 #include <cstdint>
 #include <mutex>
 #include <vector>
+
+#include "../../include/epsmoe.h"
 
 namespace epsmoe {
 
@@ -41,12 +45,22 @@ class Transport {
   // waits for; there the put is also ordered by a CUDA event.
   virtual int p2p_after_put(int slot, cudaStream_t) { (void)slot; return 0; }
   virtual int p2p_before_wait(int slot0, int nslots, cudaStream_t) { (void)slot0; (void)nslots; return 0; }
+  // SM budget of the send/recv kernels (NCCL maxCTAs per communicator, the
+  // paper's comm-SM control P:202-209, NEXT-1).  Collective: every rank passes
+  // the same value in the same forward (plans agree).  0 = keep.
+  virtual int set_comm_ctas(int ctas) { (void)ctas; return 0; }
+  // Asynchronous errors of the collectives (ncclCommGetAsyncError); polled
+  // while the host waits for the count exchange.  0 = none.
+  virtual int poll_async() { return 0; }
 };
+
 
 class NcclTransport : public Transport {
  public:
-  NcclTransport(ncclComm_t d, ncclComm_t c) : comm_{d, c} {}
+  NcclTransport(ncclComm_t d, ncclComm_t c, int ctas) : comm_{d, c}, base_{d, c}, ctas_(ctas) {}
   ~NcclTransport() override;
+  int set_comm_ctas(int ctas) override;
+  int poll_async() override;
   int allgather_i32(const int32_t* send, int32_t* recv, size_t count, cudaStream_t st) override;
   int group_start(int channel) override;
   int send(const void* buf, size_t bytes, int peer, int channel, cudaStream_t st) override;
@@ -58,8 +72,40 @@ class NcclTransport : public Transport {
   int map_peers(void* mine, std::vector<char*>& out) override;
 
  private:
-  ncclComm_t comm_[2];
+  ncclComm_t comm_[2];         // in use
+  ncclComm_t base_[2];         // created with the layer's initial maxCTAs
+  int ctas_;                   // maxCTAs of comm_
+  struct Split { int ctas; ncclComm_t c[2]; };
+  std::vector<Split> splits_;  // ncclCommSplit copies with other maxCTAs (NEXT-1), kept for reuse
   std::vector<void*> opened_;  // cudaIpcOpenMemHandle results, closed on destruction
+};
+
+// Host-collective transport (moe_layer_create_hostcoll): the caller's blocking
+// host allgather (e.g. torch.distributed over gloo) carries the count
+// exchange and the one-time peer mapping; routed rows move only on the
+// layer's own peer-memory planes (a2a_p2p = 1 or 2), so send / recv are
+// unsupported.  One process per rank; the ranks may share one GPU (tests:
+// separate contexts, real cudaIpc mappings and device flags, no host
+// ordering of the puts) or be one GPU each.
+class HostCollTransport : public Transport {
+ public:
+  HostCollTransport(moe_host_allgather_fn fn, void* ctx, int ep, int rank) : fn_(fn), ctx_(ctx), ep_(ep), rank_(rank) {}
+  ~HostCollTransport() override;
+  int allgather_i32(const int32_t* send, int32_t* recv, size_t count, cudaStream_t st) override;
+  int group_start(int) override { return unsupported(); }
+  int send(const void*, size_t, int, int, cudaStream_t) override { return unsupported(); }
+  int recv(void*, size_t, int, int, cudaStream_t) override { return unsupported(); }
+  int group_end(int, cudaStream_t) override { return unsupported(); }
+  const char* name() const override { return "hostcoll"; }
+  int map_peers(void* mine, std::vector<char*>& out) override;
+
+ private:
+  int unsupported();
+  int gather_host(const void* send, void* recv, size_t bytes);
+  moe_host_allgather_fn fn_;
+  void* ctx_;
+  int ep_, rank_;
+  std::vector<void*> opened_;
 };
 
 // Shared rendezvous state of the ep local ranks (moe_local_group_create).
@@ -87,7 +133,13 @@ struct LocalGroup {
 
 class LocalTransport : public Transport {
  public:
-  LocalTransport(LocalGroup* g, int rank) : g_(g), rank_(rank) {}
+  // order_puts: p2p_before_wait also orders the peers' puts before the wait by
+  // CUDA events (EPSMOE_LOCAL_P2P_EVENTS=1/0 forces it; default on for ep > 2).
+  // The ranks' streams share one context's hardware queues, and with more
+  // streams than queues (CUDA_DEVICE_MAX_CONNECTIONS) a spinning flag wait can
+  // sit in front of the put it waits for.  Off, the device flags alone order
+  // the data (as across processes).
+  LocalTransport(LocalGroup* g, int rank);
   int allgather_i32(const int32_t* send, int32_t* recv, size_t count, cudaStream_t st) override;
   int group_start(int channel) override;
   int send(const void* buf, size_t bytes, int peer, int channel, cudaStream_t st) override;
@@ -101,6 +153,7 @@ class LocalTransport : public Transport {
  private:
   LocalGroup* g_;
   int rank_;
+  bool order_puts_ = true;
 };
 
 }  // namespace epsmoe

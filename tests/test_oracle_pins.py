@@ -559,3 +559,144 @@ def test_comm_volume_bounds_p265():
         # per token: at most g destination ranks, almost always exactly g
         ng = np.array([len(set((row // (E // D)).tolist())) for row in idx])
         assert ng.max() <= g and (ng == g).mean() > 0.99
+
+
+# --------------------------------------------------------------------------
+# 10. Chunk / slice / shard rules (R8, R12) vs tables written out by hand
+# --------------------------------------------------------------------------
+
+def _rules():
+    return json.load(open(os.path.join(GOLDEN, "chunk_rules.json")))
+
+
+def test_chunk_groups_vs_survey_table():
+    """SURVEY §8(c) table (S:307 rule): the first E_loc mod N groups get one
+    more expert.  Remainder experts going to the LAST groups, or a rounded
+    split, fail here."""
+    for e_loc, per_n in _rules()["chunk_group_sizes"].items():
+        for n, sizes in per_n.items():
+            gb = oracle.chunk_groups(int(e_loc), int(n))
+            assert np.diff(gb).tolist() == sizes, (e_loc, n)
+            assert gb[0] == 0 and gb[-1] == int(e_loc)
+    with pytest.raises(ValueError):
+        oracle.chunk_groups(3, 4)        # N > E_loc is not an expert grouping (P:408)
+
+
+def test_slice_ranges_and_token_shards_vs_hand_tables():
+    for c in _rules()["slice_ranges"]:
+        assert oracle.slice_ranges(c["T_loc"], c["S"]).tolist() == c["begin"], c
+    for c in _rules()["token_shards"]:
+        assert oracle.token_shards(c["T"], c["D"]).tolist() == c["start"], c
+
+
+def test_token_sliced_send_counts_vs_hand_fixture():
+    """fig:eps_overview routing with token slices (R8 extension), counted by hand."""
+    fx = json.load(open(os.path.join(GOLDEN, "fig_eps_overview.json")))
+    idx = np.array(fx["routing"], np.int32)
+    hist = oracle.dispatch_layout(idx, 6, 2)["hist"]
+    for c in _rules()["sliced_send_counts"]:
+        got = oracle.chunk_send_counts(hist, 6, 2, c["N"], token_slices=c["S"], idx=idx)
+        assert got.tolist() == c["send"], c
+        # summed over slices, the sliced counts are the unsliced chunk counts
+        plain = oracle.chunk_send_counts(hist, 6, 2, c["N"])
+        assert np.array_equal(got.reshape(c["N"], c["S"], 2, 2).sum(axis=1), plain)
+
+
+def _round_frac(q, p):
+    """Exact round-to-nearest-even of a Fraction to p significant bits (binary,
+    exponent >= -126, no overflow): fp32 for p = 24, bf16 for p = 8."""
+    if q == 0:
+        return Fraction(0)
+    sgn = -1 if q < 0 else 1
+    a = abs(q)
+    e = a.numerator.bit_length() - a.denominator.bit_length()
+    if Fraction(2) ** e > a:
+        e -= 1                                   # now 2^e <= a < 2^(e+1)
+    e = max(e, -126)
+    ulp = Fraction(2) ** (e - p + 1)
+    m = a / ulp
+    r = m.numerator // m.denominator
+    rem = m - r
+    if rem > Fraction(1, 2) or (rem == Fraction(1, 2) and r % 2 == 1):
+        r += 1
+    return sgn * r * ulp
+
+
+def _fma_sensitive_pair():
+    """(w fp32, o bf16) with q = fp32(w o) = 2^-1 + 2^-8 + 2^-24 exactly and
+    w o - q > 0: from acc = 1, 1 + q is an fp32 tie (1.5 + 2^-8 + 2^-24) whose
+    even side 1.5 + 2^-8 is itself a bf16 tie, so fmaf(w, o, 1) -> bf16 rounds
+    up while fp32(1 + fp32(w o)) -> bf16 rounds down.  Found by scanning bf16
+    mantissas of o with exact rationals."""
+    q = Fraction(1, 2) + Fraction(1, 2 ** 8) + Fraction(1, 2 ** 24)
+    for om in range(128):
+        o = Fraction(128 + om, 128)                     # bf16: 8 significant bits
+        wq = q / o                                      # in [0.25, 0.5]
+        ulp_w = Fraction(1, 2 ** 25) if wq >= Fraction(1, 4) else Fraction(1, 2 ** 26)
+        m = (wq / ulp_w).numerator // (wq / ulp_w).denominator + 1
+        w = m * ulp_w
+        p = w * o
+        if 0 < p - q < Fraction(1, 2 ** 25) and _round_frac(p, 24) == q:
+            fused = _round_frac(_round_frac(1 + p, 24), 8)
+            split = _round_frac(_round_frac(1 + q, 24), 8)
+            if fused != split:
+                return np.float32(float(w)), np.float32(float(o))
+    raise AssertionError("no sensitive pair found")
+
+
+def test_contract_combine_vs_exact_rational_fmaf_chain():
+    """R4 combine: acc = fp32(s); acc = fmaf(w_j, o_j, acc) for j in slot order;
+    y = bf16(acc).  Brute force with exact rationals and an independent
+    rounding.  Two crafted tokens make the plausible mistakes visible in y:
+    token A (s added last instead of first: 1 + 2^-8 then three 2^-25 terms),
+    token B (a separately rounded multiply-add instead of fmaf: an exact product
+    just above an fp32 tie that is also a bf16 tie)."""
+    rng = np.random.default_rng(17)
+    T, k, H = 24, 6, 16
+    s = oracle.round_bf16(rng.standard_normal((T, H)).astype(np.float32))
+    o = oracle.round_bf16((rng.standard_normal((T, k, H)) * 8).astype(np.float32))
+    w = (rng.random((T, k)) / 3).astype(np.float32)
+    # token A: s = 1, products 2^-8, 2^-25 x 3 (0.25 fp32 ulp each), then zeros
+    s[0] = 1.0
+    o[0, :, :] = np.array([2.0 ** -8, 2.0 ** -25, 2.0 ** -25, 2.0 ** -25, 1.0, 1.0], np.float32)[:, None]
+    w[0] = np.array([1, 1, 1, 1, 0, 0], np.float32)
+    # token B: s = 1, one product just above the 1 + 2^-8 + 2^-24 double tie
+    wb, ob = _fma_sensitive_pair()
+    s[1] = 1.0
+    o[1, :, :] = ob
+    w[1] = 0.0
+    w[1, 0] = wb
+    got = oracle.combine(s, o, w)
+    for t in range(T):
+        for h in range(H):
+            acc = Fraction(float(s[t, h]))
+            for j in range(k):
+                acc = _round_frac(Fraction(float(w[t, j])) * Fraction(float(o[t, j, h])) + acc, 24)
+            assert Fraction(float(got[t, h])) == _round_frac(acc, 8), (t, h)
+    # the two crafted tokens separate the contract from the plausible mistakes
+    acc = np.zeros((T, H), np.float32)
+    for j in range(k):
+        acc = oracle.fmaf(np.broadcast_to(w[:, j][:, None], (T, H)), o[:, j, :], acc)
+    s_last = oracle.round_bf16((acc + s).astype(np.float32))
+    acc = s.copy()
+    for j in range(k):
+        acc = (acc + (w[:, j][:, None] * o[:, j, :]).astype(np.float32)).astype(np.float32)
+    mul_add = oracle.round_bf16(acc)
+    assert not np.array_equal(s_last[0], got[0]) and not np.array_equal(mul_add[1], got[1])
+
+
+def test_pn_grid_with_token_slices_vs_hand_candidates():
+    """R8 extension: the candidates are N = 1..E_loc and E_loc*S for
+    S = 2..slice_max (nothing in between).  Objective L - R of P:408-415 with
+    C = min(4, 5) = 4, k = 0.1, b = 0 (N* = sqrt(40) = 6.32 by P:425):
+      E_loc = 1, slice_max = 8: {1..8}            -> 6 (3.3333-0.6 > 3.4286-0.7)
+      E_loc = 3, slice_max = 3: {1,2,3,6,9}       -> 6 (2.7333 > 2.6556 > 2.3667)
+      E_loc = 4, slice_max = 2: {1,2,3,4,8}       -> 8 (2.7 > 2.6; 5 is no candidate)
+      E_loc = 3, slice_max = 1: {1,2,3}           -> 3"""
+    f = lambda n: 4.0 / n * (n - 1) - 0.1 * n
+    for e_loc, smax, cands, want in [(1, 8, [1, 2, 3, 4, 5, 6, 7, 8], 6), (3, 3, [1, 2, 3, 6, 9], 6),
+                                     (4, 2, [1, 2, 3, 4, 8], 8), (3, 1, [1, 2, 3], 3)]:
+        best = max(cands, key=lambda n: (f(n), -n))
+        assert best == want
+        n, v = oracle.pn_optimum_grid(4.0, 5.0, 0.1, 0.0, e_loc, slice_max=smax)
+        assert n == want and abs(v - f(want)) < 1e-12, (e_loc, smax, n)
