@@ -67,6 +67,9 @@ def parse():
     p.add_argument("--a2a", default="nccl", choices=["nccl", "p2p", "ce"],
                    help="ep > 1 all2all: NCCL send/recv, the layer's put kernels over NVLink peer memory, or "
                         "copy-engine peer copies (no SM moves a row)")
+    p.add_argument("--dry-run", action="store_true",
+                   help="run the launch / rank / shard / NCCL-id plumbing on the gloo backend and print what each "
+                        "rank would run, without a GPU (tests/test_bench_contract.py)")
     return p.parse_args()
 
 
@@ -151,14 +154,16 @@ def _isnum(s):
 
 
 # ---------------------------------------------------------------- oracle (cpu_baseline / reference arm)
-def oracle_sample(cfg, seed, n_tokens, token0=0, skew=0.0, device_gen=False):
-    """Inputs for an oracle run on tokens [token0, token0+n).  Expert weights
+def oracle_sample(cfg, seed, n_tokens, token0=0, skew=0.0, device_gen=False, spread=False):
+    """Inputs for an oracle run on tokens [token0, token0+n) (spread: n tokens
+    evenly spaced over the whole global batch, i.e. over every rank's shard).  Expert weights
     come from gen/ (numpy, or its bit-identical device twin when device_gen,
     which only speeds up input generation; tests/test_gpu_parity.py checks the
     twin).  The oracle itself never touches the GPU."""
     from gen import Inputs, TID_WDOWN, TID_WGATE, TID_WUP, MODE_UNIF, fill_bf16, unif_scale
     E, k, H, F = cfg["E"], cfg["k"], cfg["H"], cfg["F"]
-    tok = np.arange(token0, token0 + n_tokens)
+    tok = np.unique(np.linspace(0, cfg["T"] - 1, n_tokens).astype(np.int64)) if spread else \
+        np.arange(token0, token0 + n_tokens)
     inp = Inputs(E=E, k=k, H=H, F=F, S=cfg["S"], Fs=cfg["Fs"], T=cfg["T"], seed=seed, experts=[], tokens=tok,
                  skew=skew)
     cache = {}
@@ -219,15 +224,17 @@ def layer_opts(args):
 
 
 def cpu_baseline(cfg, seed, skew, sample=0, opts=None):
-    # sized for ~10 s of oracle work on a 16-core host (the contract's bounded sample; measured
-    # oracle rates there at these sizes: dsv2 ~19, mixtral ~50, dsv2_lite ~1150 tokens/s)
-    n = sample or {"tiny": 256, "dsv2_lite": 12288, "mixtral": 512, "dsv2": 192, "dsv2_decode": 192,
-                   "mixtral_decode": 512}.get(cfg["name"], 32)
-    inp, ew, cache = oracle_sample(cfg, seed, n, 0, skew, device_gen=True)
+    # sized for ~10-20 s of oracle work on a 16-core host (the contract's bounded sample; measured
+    # oracle rates there: dsv2 ~20-25, mixtral ~50, dsv2_lite ~1150 tokens/s), tokens spread evenly
+    # over the global batch (every rank's shard, every expert the sample routes to)
+    n = sample or {"tiny": 256, "dsv2_lite": 12288, "mixtral": 768, "dsv2": 384, "dsv2_decode": 192,
+                   "mixtral_decode": 256}.get(cfg["name"], 32)
+    inp, ew, cache = oracle_sample(cfg, seed, n, 0, skew, device_gen=True, spread=True)
+    n = len(inp.tokens)
     dt = run_oracle_timed(cfg, inp, ew, cache, opts)
     return {"value": n / dt, "unit": UNIT, "cores": host_cores(), "kind": "oracle",
-            "sample": f"first {n} tokens of the {cfg['name']} workload (all their experts + shared), "
-                      f"contract mode fp64 numpy, {dt:.1f} s"}
+            "sample": f"{n} tokens evenly spaced over the {cfg['name']} global batch (all their experts + "
+                      f"shared), contract mode fp64 numpy, {dt:.1f} s"}
 
 
 def reference_arm(args, cfg):
@@ -263,6 +270,58 @@ def token_shards(T, D):
     return np.concatenate([[0], np.cumsum([base + (1 if r < rem else 0) for r in range(D)])]).astype(np.int64)
 
 
+def dist_setup(args, cfg, backend):
+    """Launch plumbing shared by the run and --dry-run: ranks from the torchrun
+    environment, the process group, DP token shards (R12), EP expert ranges and
+    the two NCCL unique ids rank 0 makes and broadcasts."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2410_12247_b200 import MoELayer
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    dev = None
+    if backend == "nccl":
+        torch.cuda.set_device(local)
+        dev = torch.device("cuda", local)
+    if world > 1:
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
+    E, T, D = cfg["E"], cfg["T"], world
+    if E % D:
+        raise SystemExit(f"E={E} not divisible by {D}")
+    starts = token_shards(T, D)
+    uid_d = uid_c = None
+    if D > 1:
+        ids = [MoELayer.unique_id(), MoELayer.unique_id()] if rank == 0 else [None, None]
+        dist.broadcast_object_list(ids, src=0)
+        uid_d, uid_c = ids
+    return dict(world=world, rank=rank, local=local, dev=dev, D=D, E_loc=E // D, starts=starts,
+                t0=int(starts[rank]), T_loc=int(starts[rank + 1] - starts[rank]), uid_d=uid_d, uid_c=uid_c)
+
+
+def dry_run(args, cfg):
+    import torch.distributed as dist
+    s = dist_setup(args, cfg, "gloo")
+    rec = {"rank": s["rank"], "world": s["world"], "local_rank": s["local"], "tokens": [s["t0"], s["t0"] + s["T_loc"]],
+           "experts": [s["rank"] * s["E_loc"], (s["rank"] + 1) * s["E_loc"]],
+           "uid": None if s["uid_d"] is None else (s["uid_d"][:16] + s["uid_c"][:16]).hex(),
+           "a2a": layer_opts(args)["a2a_p2p"]}
+    recs = [rec]
+    if s["D"] > 1:
+        recs = [None] * s["D"]
+        dist.all_gather_object(recs, rec)
+        dist.destroy_process_group()
+    if s["rank"] == 0:
+        print(json.dumps({"dry_run": True, "metric": METRIC, "n_gpus": s["D"], "config": cfg["name"],
+                          "global_tokens": cfg["T"], "ranks": recs}), flush=True)
+
+
 def ours(args, cfg):
     import torch
     import torch.distributed as dist
@@ -271,23 +330,10 @@ def ours(args, cfg):
                      device_fill_bf16, router_skew_bias, unif_scale)
     from paper_2410_12247_b200 import MOE_GEMM_AUTO, MOE_GEMM_DENSE, MOE_GEMM_GROUPED, MoELayer, make_plan
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world != args.gpus:
-        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
-
+    ds = dist_setup(args, cfg, "nccl")
+    world, rank, local, dev = ds["world"], ds["rank"], ds["local"], ds["dev"]
     E, k, H, F, S, Fs, T = cfg["E"], cfg["k"], cfg["H"], cfg["F"], cfg["S"], cfg["Fs"], cfg["T"]
-    D = world
-    if E % D:
-        raise SystemExit(f"E={E} not divisible by {D}")
-    E_loc = E // D
-    starts = token_shards(T, D)
-    t0, T_loc = int(starts[rank]), int(starts[rank + 1] - starts[rank])
+    D, E_loc, starts, t0, T_loc = world, ds["E_loc"], ds["starts"], ds["t0"], ds["T_loc"]
     seed = args.seed
 
     def gen(shape, tid, base, scale):
@@ -310,11 +356,7 @@ def ours(args, cfg):
     x = gen((T_loc, H), TID_X, t0 * H, unif_scale(1))
     y = torch.empty_like(x)
 
-    uid_d = uid_c = None
-    if D > 1:
-        ids = [MoELayer.unique_id(), MoELayer.unique_id()] if rank == 0 else [None, None]
-        dist.broadcast_object_list(ids, src=0)
-        uid_d, uid_c = ids
+    uid_d, uid_c = ds["uid_d"], ds["uid_c"]
     opts = feature_opts(args)
     layer = MoELayer(E, k, H, F, w, S=S, Fs=Fs, ep=D, rank=rank, max_tokens=int(np.diff(starts).max()),
                      norm_topk=cfg["norm_topk"],
@@ -368,7 +410,6 @@ def ours(args, cfg):
     torch.cuda.synchronize()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
-    stage_sum, stage_cnt = {}, {}
     launches = 0
     t_start = clocks.mark()
     ev0.record(stream)
@@ -377,8 +418,6 @@ def ours(args, cfg):
             graph.replay()
             launches += launches_per_forward
             continue
-        if i == args.steps - 1:
-            layer.set_profiling(True)
         layer.forward(x, y, plan=plan)
         launches += layer.last_launches()
     ev1.record(stream)
@@ -387,20 +426,20 @@ def ours(args, cfg):
     if D > 1:
         dist.barrier()
     clk = clocks.stop(t_start, t_end)
-    stages_src = "last timed forward"
-    if not use_graph:
+    # per-stage CUDA events of PROF_FORWARDS eager forwards right after the timed
+    # region (reading them synchronises the host, so not inside it; a CUDA graph
+    # cannot record them): per-step means, and the GateUp spread across them
+    prof_n = max(5, min(args.steps, 10))
+    stages_src = f"mean of {prof_n} profiled eager forwards right after the timed region"
+    stage_sum, stage_cnt, gateup_each = {}, {}, []
+    layer.set_profiling(True)
+    for _ in range(prof_n):
+        layer.forward(x, y, plan=plan)
         for name, (ms, cnt) in layer.stage_ms().items():
-            stage_sum[name] = ms * args.steps       # per-step averages below divide by steps
-            stage_cnt[name] = cnt * args.steps
-    else:  # events cannot be read inside a graph: profiled eager forwards after the timed region
-        stages_src = "eager forwards after the timed graph replays"
-        layer.set_profiling(True)
-        for _ in range(args.steps):
-            layer.forward(x, y, plan=plan)
-            for name, (ms, cnt) in layer.stage_ms().items():
-                stage_sum[name] = stage_sum.get(name, 0.0) + ms
-                stage_cnt[name] = stage_cnt.get(name, 0) + cnt
-        torch.cuda.synchronize()
+            stage_sum[name] = stage_sum.get(name, 0.0) + ms
+            stage_cnt[name] = stage_cnt.get(name, 0) + cnt
+        gateup_each.append(layer.stage_ms()["gateup"][0])
+    torch.cuda.synchronize()
     layer.set_profiling(False)
     ms_total = ev0.elapsed_time(ev1)
     t = torch.tensor([ms_total], dtype=torch.float64, device=dev)
@@ -421,21 +460,36 @@ def ours(args, cfg):
     # ---- roofline of the dominant kernel: GateUpGemm + SiluAct (tcgen05)
     peaks, peak_src = load_peaks()
     ptf, pkey = peak_tflops(peaks)
-    gu_ms = stage_sum.get("gateup", 0.0) / args.steps
+    gu_ms = stage_sum.get("gateup", 0.0) / prof_n
     gu_flop = 4.0 * H * F * rows_me
     achieved = gu_flop / (gu_ms / 1e3) / 1e12 if gu_ms > 0 else None
-    traffic = None
+    traffic, traffic_src = None, None
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tpath):
         try:
-            traffic = json.load(open(tpath)).get(cfg["name"], {}).get("gateup_dram_bytes_per_launch")
+            tr = json.load(open(tpath)).get(cfg["name"], {})
+            traffic, traffic_src = tr.get("gateup_dram_bytes_per_launch"), tr.get("source")
         except Exception:
             traffic = None
+    # three denominators: the measured sustained peak (a kernel inside a long step),
+    # the measured burst peak, and the clock-normalised tensor peak (8192 dense bf16
+    # FLOP/clk/SM x SMs x the median SM clock sampled during the timed region)
+    burst = float(peaks.get("bf16_tflops", FALLBACK_PEAKS["bf16_tflops"]))
+    nsm = torch.cuda.get_device_properties(dev).multi_processor_count
+    clock_peak = 8192.0 * nsm * clk["sm_mhz"] * 1e6 / 1e12 if clk and clk.get("sm_mhz") else None
     roofline = {"bound": "tensor", "kernel": "gemm_kernel<EPI_SWIGLU> (GateUpGemm+SiluAct)",
                 "achieved": achieved, "peak": ptf, "unit": "TFLOP/s",
                 "frac": (achieved / ptf) if achieved else None, "traffic": traffic,
                 "peak_source": f"{peak_src} {pkey}",
-                "algorithmic": f"4*H*F*rows = {gu_flop:.4g} FLOP per step over {stage_cnt.get('gateup', 0) // args.steps} launch(es)"}
+                "frac_burst": (achieved / burst) if achieved else None, "peak_burst": burst,
+                "frac_clock": (achieved / clock_peak) if achieved and clock_peak else None,
+                "peak_clock": clock_peak,
+                "peak_clock_how": "8192 bf16 FLOP/clk/SM x %d SMs x median SM MHz under load" % nsm,
+                "achieved_spread": [gu_flop / (m / 1e3) / 1e12 for m in (max(gateup_each), min(gateup_each))]
+                if gateup_each and min(gateup_each) > 0 else None,
+                "timing": stages_src,
+                "traffic_source": f"static, {traffic_src}" if traffic_src else None,
+                "algorithmic": f"4*H*F*rows = {gu_flop:.4g} FLOP per step over {stage_cnt.get('gateup', 0) // prof_n} launch(es)"}
 
     # ---- layer roofline: max(expert+shared+router FLOPs / peak, all2all bytes / NVLink), max over ranks
     flops_rank = [6.0 * H * F * rl + 6.0 * H * SF * (starts[r + 1] - starts[r]) + 2.0 * H * E * (starts[r + 1] - starts[r])
@@ -501,7 +555,7 @@ def ours(args, cfg):
            "steps": args.e2e_steps,
            "api": "moe_layer_forward_host_async x steps + moe_layer_host_sync (pinned host x/y; calls overlap)"}
 
-    stages = {n: round(v / args.steps, 4) for n, v in stage_sum.items()}
+    stages = {n: round(v / prof_n, 4) for n, v in stage_sum.items()}
     # ---- all2all alone: the same chunked dispatch / combine with ComputeMoE and the
     # shared experts skipped (moe_layer_set_comm_only); hidden = 1 - exposed / alone, max over ranks
     a2a_alone = None
@@ -563,6 +617,8 @@ def main():
     cfg = dict(CONFIGS[args.config], name=args.config)
     if args.impl == "reference":
         reference_arm(args, cfg)
+    elif args.dry_run:
+        dry_run(args, cfg)
     else:
         ours(args, cfg)
 

@@ -6,4 +6,4 @@ arguments.  It never imports oracle/ and has no CPU fallback.
 """
 from .abi import (MOE_GEMM_AUTO, MOE_GEMM_DENSE, MOE_GEMM_GROUPED, EpsMoeError, lib, make_config,  # noqa: F401
                   make_plan, moe_cost_model_t, moe_plan_t, plan_compute)
-from .layer import LocalGroup, MoELayer, gemm_grouped  # noqa: F401
+from .layer import HostAllgather, LocalGroup, MoELayer, gemm_grouped  # noqa: F401

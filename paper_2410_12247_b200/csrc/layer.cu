@@ -809,7 +809,8 @@ moe_status_t fwd_local(Fwd& F) {
   // ---- EP = 1: no all2all; every chunk is local (C = 0 => PN = 1 is optimal)
   if (!F.plan_in) plan_compute(c, L->cost, T, nullptr, &plan);
   if (side) CUDA_TRY(cudaStreamWaitEvent(st, L->ev_shared, 0));
-  const bool two = L->chunk_streams > 1 && plan.num_chunks > 1 && T > 0;
+  // (a GEMM grid below the SM count is a partition to keep: one grid at a time)
+  const bool two = L->chunk_streams > 1 && plan.num_chunks > 1 && T > 0 && num_ctas >= L->num_sms;
   if (two) {  // odd chunks on s_comp2 (after the routing on st)
     CUDA_TRY(cudaEventRecord(L->ev_routed, st));
     CUDA_TRY(cudaStreamWaitEvent(L->s_comp2, L->ev_routed, 0));

@@ -257,7 +257,7 @@ int LocalTransport::map_peers(void* mine, std::vector<char*>& out) {
 
 LocalTransport::LocalTransport(LocalGroup* g, int rank) : g_(g), rank_(rank) {
   const char* ev = std::getenv("EPSMOE_LOCAL_P2P_EVENTS");
-  order_puts_ = ev ? std::atoi(ev) != 0 : g->ep > 2;
+  order_puts_ = ev ? std::atoi(ev) != 0 : true;
 }
 
 int LocalTransport::p2p_after_put(int slot, cudaStream_t ps) {

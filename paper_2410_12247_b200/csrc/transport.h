@@ -134,11 +134,14 @@ struct LocalGroup {
 class LocalTransport : public Transport {
  public:
   // order_puts: p2p_before_wait also orders the peers' puts before the wait by
-  // CUDA events (EPSMOE_LOCAL_P2P_EVENTS=1/0 forces it; default on for ep > 2).
-  // The ranks' streams share one context's hardware queues, and with more
-  // streams than queues (CUDA_DEVICE_MAX_CONNECTIONS) a spinning flag wait can
-  // sit in front of the put it waits for.  Off, the device flags alone order
-  // the data (as across processes).
+  // CUDA events (default; EPSMOE_LOCAL_P2P_EVENTS=0 turns it off).  The ranks'
+  // streams share one context's hardware queues, and with more streams than
+  // queues (CUDA_DEVICE_MAX_CONNECTIONS, default 8) a spinning flag wait can
+  // sit in front of the put it waits for: measured, a 2-rank copy-engine
+  // forward hung until the wait kernel's 10 s trap.  Off (with <= 32 streams
+  // and CUDA_DEVICE_MAX_CONNECTIONS=32), the device flags alone order the data,
+  // as across processes (moe_layer_create_hostcoll), where contexts never share
+  // a queue.
   LocalTransport(LocalGroup* g, int rank);
   int allgather_i32(const int32_t* send, int32_t* recv, size_t count, cudaStream_t st) override;
   int group_start(int channel) override;

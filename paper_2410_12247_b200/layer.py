@@ -34,6 +34,31 @@ class LocalGroup:
             pass
 
 
+class HostAllgather:
+    """The blocking host allgather moe_layer_create_hostcoll needs, over a
+    torch.distributed process group (e.g. gloo): rank r's `bytes` bytes land at
+    recv + r * bytes on every rank.  Argument marshalling only: the C library
+    decides what to exchange (counts, cudaIpc handles)."""
+
+    def __init__(self, group=None):
+        self.group = group
+        self.fn = abi.HOST_ALLGATHER_FN(self._call)   # keep the C callback alive
+
+    def _call(self, ctx, send, recv, nbytes):
+        try:
+            import torch.distributed as dist
+            ws = dist.get_world_size(self.group)
+            src = torch.empty(nbytes, dtype=torch.uint8)
+            C.memmove(src.data_ptr(), send, nbytes)
+            outs = [torch.empty(nbytes, dtype=torch.uint8) for _ in range(ws)]
+            dist.all_gather(outs, src, group=self.group)
+            for r, t in enumerate(outs):
+                C.memmove(recv + r * nbytes, t.data_ptr(), nbytes)
+            return 0
+        except Exception:  # reported to the library as a failed collective (MOE_ERR_MISMATCH)
+            return 1
+
+
 class MoELayer:
     """weights: dict of DEVICE tensors (bf16): w_router [E,H], w_gate / w_up
     [E_loc,F,H], w_down [E_loc,H,F], optional ws_gate / ws_up [S*Fs,H],
@@ -43,7 +68,8 @@ class MoELayer:
                  routed_scale=1.0, dispatch_fp8: bool = False, local_reduce: bool = False,
                  route_groups: int = 0, route_topk_groups: int = 0, a2a_p2p: int = 0,
                  uid_dispatch: bytes | None = None, uid_combine: bytes | None = None,
-                 device=None, local_group: "LocalGroup | None" = None):
+                 device=None, local_group: "LocalGroup | None" = None,
+                 host_allgather: "HostAllgather | None" = None):
         self.lib = abi.lib()
         self.cfg = abi.make_config(E, k, H, F, S, Fs, ep, rank, max_tokens, norm_topk, routed_scale,
                                    1 if dispatch_fp8 else 0, 1 if local_reduce else 0, route_groups,
@@ -62,7 +88,13 @@ class MoELayer:
         ud = C.create_string_buffer(uid_dispatch, 128) if uid_dispatch is not None else None
         uc = C.create_string_buffer(uid_combine, 128) if uid_combine is not None else None
         with torch.cuda.device(self.device):
-            if local_group is not None:
+            if host_allgather is not None:
+                self.host_allgather = host_allgather  # keep the callback alive
+                abi.check(self.lib.moe_layer_create_hostcoll(C.byref(self.cfg), C.byref(w), host_allgather.fn, None,
+                                                             C.c_void_p(self.workspace.data_ptr()), nbytes,
+                                                             C.byref(h)),
+                          "moe_layer_create_hostcoll")
+            elif local_group is not None:
                 self.local_group = local_group  # keep alive
                 abi.check(self.lib.moe_layer_create_local(C.byref(self.cfg), C.byref(w), local_group.handle,
                                                           C.c_void_p(self.workspace.data_ptr()), nbytes, C.byref(h)),
@@ -158,9 +190,10 @@ class MoELayer:
     def last_launches(self) -> int:
         return int(self.lib.moe_layer_last_launches(self.handle))
 
-    def debug_buffers(self, T: int, override=None):
+    def debug_buffers(self, T: int, override=None, combine_in: bool = False):
         """Allocate a moe_debug_t with device outputs; override=(idx, w) tensors
-        switches routing to explicit (fig:eps_overview fixture)."""
+        switches routing to explicit (fig:eps_overview fixture); combine_in also
+        captures the expert outputs the weighted unpermute reads ([T*k, H])."""
         dev = self.device
         bufs = dict(
             logits=torch.empty(T, self.E, dtype=torch.float32, device=dev),
@@ -172,6 +205,9 @@ class MoELayer:
             shared_out=torch.empty(T, self.H, dtype=torch.bfloat16, device=dev) if self.S else None,
             lr_pos=torch.full((T, self.k), -7, dtype=torch.int32, device=dev) if self.cfg.local_reduce else None,
             lr_hist=torch.full((256,), -7, dtype=torch.int32, device=dev) if self.cfg.local_reduce else None,
+            combine_in=torch.empty(T * self.k, self.H, dtype=torch.bfloat16, device=dev)
+            if combine_in and not self.cfg.local_reduce else None,
+            gemm_resident=torch.zeros(2, dtype=torch.int32, device=dev),
         )
         if override is not None:
             bufs["topk_idx"] = override[0].to(dev, torch.int32).contiguous()
@@ -184,7 +220,8 @@ class MoELayer:
                             *[_ptr(bufs[n]) for n in ("logits", "topk_idx", "topk_w", "pos", "hist",
                                                        "seg_start", "shared_out")],
                             ghist.ctypes.data_as(C.c_void_p), C.pointer(plan_used),
-                            _ptr(bufs["lr_pos"]), _ptr(bufs["lr_hist"]), chunk_rows.ctypes.data_as(C.c_void_p))
+                            _ptr(bufs["lr_pos"]), _ptr(bufs["lr_hist"]), chunk_rows.ctypes.data_as(C.c_void_p),
+                            _ptr(bufs["combine_in"]), _ptr(bufs["gemm_resident"]))
         bufs["chunk_rows"] = chunk_rows
         bufs["global_hist"] = ghist
         bufs["plan_used"] = plan_used

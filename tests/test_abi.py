@@ -178,3 +178,139 @@ def test_planner_token_slices_when_one_expert_per_rank():
     # local_reduce keeps expert-only chunks (R16)
     cfg_lr = abi.make_config(8, 2, 4096, 14336, ep=8, max_tokens=1 << 16, local_reduce=1)
     assert abi.plan_compute(cfg_lr, 16384, hist, c).num_chunks == 1
+
+
+# ---------------------------------------------------------------- planner: wire bytes and SM partition
+
+def _flat_cost(gbps=700.0):
+    """GEMMs cheap enough that the comm side decides nothing about N; per-chunk
+    cost so high that N = 1 (T_comm is then the unsplit all2all)."""
+    c = _cost(k_ms=1e3, b_ms=0.0)
+    c.a2a_fixed_ms, c.a2a_gbps = 0.0, gbps
+    for kind in (0, 1):
+        c.gemm_ms[kind][0], c.gemm_ms[kind][1] = 0.01, 1.0
+    return c
+
+
+def test_planner_prices_fp8_and_dedup_wire_bytes():
+    """T_comm counts the bytes that cross: FP8 dispatch rows of
+    H + H/128 bytes padded to 16 (R15) against bf16 combine rows, and under
+    expert-side LocalReduce (R16) one row per distinct destination rank instead
+    of one per pair, i.e. D (1 - C(E - E_loc, k) / C(E, k)) / k of the rows
+    (DSv2 at EP 8: 4.4586 / 6 = 0.7431)."""
+    E, D, k, H, F = 160, 8, 6, 5120, 1536
+    T = 65536
+    mk = lambda **kw: abi.make_config(E, k, H, F, ep=D, max_tokens=T // D, **kw)  # noqa: E731
+    c = _flat_cost()
+    base = abi.plan_compute(mk(), T, None, c)
+    fp8 = abi.plan_compute(mk(dispatch_fp8=1), T, None, c)
+    lr = abi.plan_compute(mk(local_reduce=1), T, None, c)
+    both = abi.plan_compute(mk(dispatch_fp8=1, local_reduce=1), T, None, c)
+    assert base.num_chunks == fp8.num_chunks == lr.num_chunks == 1
+    q_row = ((H + H // 128) + 15) & ~15
+    f_fp8 = (q_row + 2 * H) / (4 * H)
+    f_lr = D * (1 - math.comb(E - E // D, k) / math.comb(E, k)) / k
+    assert abs(f_lr - 4.4586 / 6) < 1e-4
+    assert fp8.pred_comm_ms / base.pred_comm_ms == pytest.approx(f_fp8, rel=1e-5)
+    assert lr.pred_comm_ms / base.pred_comm_ms == pytest.approx(f_lr, rel=1e-5)
+    assert both.pred_comm_ms / base.pred_comm_ms == pytest.approx(f_fp8 * f_lr, rel=1e-5)
+    # the uniform T_comm itself: 2 directions x cross-rank pairs x row bytes / GB/s
+    pairs = T * k * (D - 1) / D / D
+    assert base.pred_comm_ms == pytest.approx(2 * pairs * 2 * H / 700e9 * 1e3, rel=1e-5)
+
+
+def test_planner_lr_rows_grow_with_chunks():
+    """R16 with N chunks: a token sends one row per distinct (rank, chunk) group,
+    so the rows per pair rise with N toward 1.  The expectation (G - N)(1 - q) /
+    (k (D - 1) / D), G = N D, q = C(E - E/G, k) / C(E, k), is pinned by brute
+    force over random top-k sets; the planner's T_comm(N) under local_reduce
+    follows it (checked at N = E_loc, which a compute-dominated model picks)."""
+    E, D, k = 64, 4, 6
+    rng = np.random.default_rng(5)
+    sets = np.argsort(rng.random((40000, E)), axis=1)[:, :k]
+    home = rng.integers(0, D, size=len(sets))           # the token's own rank
+    prev = 0.0
+    for N in (1, 2, 4, 8, 16):
+        gsz = E // (N * D)
+        grp = sets // gsz                                   # group id = rank * N + chunk
+        rank = sets // (E // D)
+        remote_groups = np.array([len(set(g[r != h].tolist())) for g, r, h in zip(grp, rank, home)])
+        remote_pairs = (rank != home[:, None]).sum(axis=1)
+        f_mc = remote_groups.sum() / remote_pairs.sum()
+        assert f_mc == pytest.approx(_lr_factor(E, D, k, N), rel=0.02), (N, f_mc)
+        assert _lr_factor(E, D, k, N) > prev
+        prev = _lr_factor(E, D, k, N)
+    # planner: GEMMs dominate, no per-chunk cost -> N = E_loc; T_comm(E_loc) / T_comm(plain) = f(E_loc)
+    E, D, k, T = 32, 4, 6, 1 << 16
+    c = _flat_cost()
+    c.k_ms = 0.0
+    for kind in (0, 1):
+        c.gemm_ms[kind][0], c.gemm_ms[kind][1] = 10.0, 1000.0
+    plain = abi.plan_compute(abi.make_config(E, k, 2048, 1408, ep=D, max_tokens=T // D), T, None, c)
+    lr = abi.plan_compute(abi.make_config(E, k, 2048, 1408, ep=D, max_tokens=T // D, local_reduce=1), T, None, c)
+    assert lr.num_chunks == E // D
+    assert lr.pred_comm_ms / plain.pred_comm_ms == pytest.approx(_lr_factor(E, D, k, E // D), rel=1e-5)
+
+
+def _lr_factor(E, D, k, N):
+    G = N * D
+    q = math.prod((E - E / G - i) / (E - i) for i in range(k))
+    return (G - N) * (1 - q) / (k * (D - 1) / D)
+
+
+def test_planner_picks_the_sm_partition_from_the_cost_model():
+    """NEXT-1 (Table IV): the plan's (sm_gemm,
+    comm_ctas) is the comm budget whose modelled pipelined layer time
+    T_comp * scale + T_comm(GB/s at that budget) - G(N) is least.  SMs precious
+    (steep GEMM scaling, flat all2all rate) -> the smallest budget; all2all
+    dominant with a rate that grows with CTAs -> the largest; the copy-engine
+    plane reserves none; ep = 1 has no partition."""
+    E, D, k, H, F, T = 160, 8, 6, 5120, 1536, 65536
+    cfg = abi.make_config(E, k, H, F, ep=D, max_tokens=T // D)
+
+    def model(scales, rates, gemm):
+        c = _cost(k_ms=0.05, b_ms=0.0)
+        c.a2a_fixed_ms = 0.01
+        for kind in (0, 1):
+            c.gemm_ms[kind][0], c.gemm_ms[kind][1] = gemm * 0.01, gemm
+        c.num_sms, c.n_comm = 148, 4
+        for i, (cc, s, r) in enumerate(zip((4, 8, 12, 16), scales, rates)):
+            c.comm_ctas[i], c.gemm_scale_at[i], c.a2a_gbps_at[i] = cc, s, r
+        c.a2a_gbps = max(rates)
+        return c
+    precious = abi.plan_compute(cfg, T, None, model((1.06, 1.12, 1.19, 1.27), (700, 700, 700, 700), 1.0))
+    assert (precious.comm_ctas, precious.sm_gemm) == (4, 140)
+    comm = abi.plan_compute(cfg, T, None, model((1.03, 1.06, 1.09, 1.12), (100, 200, 400, 800), 0.05))
+    assert (comm.comm_ctas, comm.sm_gemm) == (16, 116)
+    # the choice is the argmin of the modelled time over the four budgets, checked by brute force
+    for m in (model((1.06, 1.12, 1.19, 1.27), (300, 500, 650, 720), 0.3),
+              model((1.02, 1.05, 1.30, 1.31), (200, 600, 610, 615), 0.2)):
+        p = abi.plan_compute(cfg, T, None, m)
+        best = None
+        for i in range(4):
+            mi = abi.moe_cost_model_t.from_buffer_copy(bytes(m))
+            mi.n_comm = 1
+            mi.comm_ctas[0], mi.gemm_scale_at[0], mi.a2a_gbps_at[0] = m.comm_ctas[i], m.gemm_scale_at[i], m.a2a_gbps_at[i]
+            pi = abi.plan_compute(cfg, T, None, mi)
+            t = pi.pred_comp_ms + pi.pred_comm_ms - pi.pred_gain_ms
+            if best is None or t < best[0] - 1e-6:
+                best = (t, m.comm_ctas[i])
+        assert p.comm_ctas == best[1]
+    ce = abi.plan_compute(abi.make_config(E, k, H, F, ep=D, max_tokens=T // D, a2a_p2p=2), T, None,
+                          model((1.06, 1.12, 1.19, 1.27), (100, 200, 400, 800), 0.05))
+    assert (ce.comm_ctas, ce.sm_gemm) == (0, 148)
+    one = abi.plan_compute(abi.make_config(E, k, H, F, ep=1, max_tokens=T), T, None,
+                           model((1.06, 1.12, 1.19, 1.27), (100, 200, 400, 800), 0.05))
+    assert (one.comm_ctas, one.sm_gemm, one.num_chunks) == (0, 0, 1)
+
+
+def test_hostcoll_create_rejects_the_nccl_plane():
+    """moe_layer_create_hostcoll carries counts only: a2a_p2p = 0 (rows over
+    NCCL) is refused before any device work."""
+    cfg = abi.make_config(16, 2, 64, 128, ep=2, rank=0, max_tokens=16, a2a_p2p=0)
+    fake = C.c_void_p(0x1000)
+    w = abi.moe_weights_t(fake, fake, fake, fake, None, None, None, None)
+    cb = abi.HOST_ALLGATHER_FN(lambda ctx, s, r, n: 0)
+    h = C.c_void_p()
+    st = abi.lib().moe_layer_create_hostcoll(C.byref(cfg), C.byref(w), cb, None, None, 0, C.byref(h))
+    assert st == 1 and "a2a_p2p" in abi.lib().moe_last_error().decode()

@@ -58,3 +58,37 @@ def test_our_arm_json_line_tiny():
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["value"] > 0
     assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
     assert d["gpu_launches"] > 0
+
+
+def test_bench_two_ranks_plumbing_dry_run():
+    """bench.py --gpus 2 as the driver launches it (torchrun, 127.0.0.1): the
+    rank / shard / expert-range / NCCL-id plumbing of the real run
+    (bench.dist_setup) on the gloo backend, up to the NCCL init, without a GPU.
+    Rank 0 prints one line describing both ranks."""
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                        "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "bench.py"),
+                        "--gpus", "2", "--dry-run", "--a2a", "p2p"], capture_output=True, text=True, timeout=300,
+                       cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [json.loads(line) for line in r.stdout.splitlines() if line.startswith("{")]
+    assert len(lines) == 1
+    d = lines[0]
+    assert d["dry_run"] and d["n_gpus"] == 2 and d["config"] == "dsv2"
+    ranks = sorted(d["ranks"], key=lambda x: x["rank"])
+    assert [x["rank"] for x in ranks] == [0, 1] and all(x["world"] == 2 for x in ranks)
+    assert ranks[0]["tokens"] == [0, 32768] and ranks[1]["tokens"] == [32768, 65536]   # DP shards (R12)
+    assert ranks[0]["experts"] == [0, 80] and ranks[1]["experts"] == [80, 160]         # EP ranges (P:219)
+    assert ranks[0]["uid"] == ranks[1]["uid"] and len(ranks[0]["uid"]) == 64          # one id pair, broadcast
+    assert all(x["a2a"] == 1 for x in ranks)
+
+
+def test_bench_gpus_mismatch_is_refused():
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--dry-run"],
+                       capture_output=True, text=True, timeout=120, cwd=ROOT,
+                       env=dict(os.environ, WORLD_SIZE="1", RANK="0"))
+    assert r.returncode != 0 and "WORLD_SIZE" in (r.stdout + r.stderr)

@@ -700,3 +700,22 @@ def test_pn_grid_with_token_slices_vs_hand_candidates():
         assert best == want
         n, v = oracle.pn_optimum_grid(4.0, 5.0, 0.1, 0.0, e_loc, slice_max=smax)
         assert n == want and abs(v - f(want)) < 1e-12, (e_loc, smax, n)
+
+
+def test_nan_logits_rank_below_every_number():
+    """R18: a NaN logit (NaN / Inf inputs) is never selected ahead of a number
+    and adds 0 to the softmax; a row of NaNs selects experts 0..k-1 with NaN
+    weights.  Brute force over the finite logits."""
+    rng = np.random.default_rng(2)
+    lg = rng.standard_normal((6, 12)).astype(np.float32)
+    lg[0, [1, 5]] = np.nan
+    lg[1, :] = np.nan
+    lg[2, 0] = np.nan
+    idx, w = oracle.topk_gating(lg, 3, norm_topk=0)
+    for t in (0, 2, 3):
+        fin = [e for e in range(12) if not math.isnan(float(lg[t, e]))]
+        order = sorted(fin, key=lambda e: (-float(lg[t, e]), e))[:3]
+        assert idx[t].tolist() == order
+        z = sum(math.exp(float(lg[t, e])) for e in fin)
+        assert np.allclose(w[t], [math.exp(float(lg[t, e])) / z for e in order], rtol=1e-6)
+    assert idx[1].tolist() == [0, 1, 2] and np.isnan(w[1]).all()
