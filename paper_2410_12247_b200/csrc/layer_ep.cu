@@ -436,32 +436,23 @@ moe_status_t ep_put(Ep& X, int dir, int ch, cudaStream_t ps) {
     const auto* hp = reinterpret_cast<const int64_t*>(L->p2p_host + P2P_SEGS_BYTES) + slot * (moe_layer::P2P_MAXS + 1);
     const int n = X.nseg[dir][ch];
     if (n > 0) {
-      std::vector<void*> dsts(n), srcs(n);
-      std::vector<size_t> sizes(n);
-      for (int i = 0; i < n; ++i) {
-        dsts[i] = hs[i].dst;
-        srcs[i] = const_cast<uint4*>(hs[i].src);
-        sizes[i] = (size_t)(hp[i + 1] - hp[i]) * 16;
-      }
-      cudaMemcpyAttributes attr;
-      std::memset(&attr, 0, sizeof(attr));
-      attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
-      size_t attr_idx = 0, fail_idx = 0;
-      // batched calls of at most 128 copies (B200_PROFILING.md: larger batches
-      // have crashed this driver / CUDA combination), else one copy per segment
-      constexpr int CE_BATCH_MAX = 128;
-      int done = 0;
-      while (L->ce_batch && done < n) {
-        const int nb = std::min(CE_BATCH_MAX, n - done);
-        if (cudaMemcpyBatchAsync(dsts.data() + done, srcs.data() + done, sizes.data() + done, (size_t)nb, &attr,
-                                 &attr_idx, 1, &fail_idx, ps) != cudaSuccess) {
-          (void)cudaGetLastError();
-          L->ce_batch = false;  // not supported here: per-segment copies from now on
-          break;
+      // one cudaMemcpyAsync per run of segments that are contiguous on both
+      // sides (the batched copy API is closed on this pool: it raised GPU
+      // faults); each copy is a peer copy on the copy engines
+      int i = 0;
+      while (i < n) {
+        char* dst = reinterpret_cast<char*>(hs[i].dst);
+        const char* src = reinterpret_cast<const char*>(hs[i].src);
+        size_t bytes = (size_t)(hp[i + 1] - hp[i]) * 16;
+        int j = i + 1;
+        while (j < n && reinterpret_cast<char*>(hs[j].dst) == dst + bytes &&
+               reinterpret_cast<const char*>(hs[j].src) == src + bytes) {
+          bytes += (size_t)(hp[j + 1] - hp[j]) * 16;
+          ++j;
         }
-        done += nb;
+        if (bytes) CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, ps));
+        i = j;
       }
-      for (int i = done; i < n; ++i) CUDA_TRY(cudaMemcpyAsync(dsts[i], srcs[i], sizes[i], cudaMemcpyDeviceToDevice, ps));
     }
     KERNEL_TRY(launch_p2p_signal(dfp, D, X.epoch, ps));
   } else {

@@ -95,7 +95,6 @@ struct moe_layer {
   int fuse_combine = 0;
   static constexpr int COMB_PIECES = 4;
   cudaEvent_t ev_piece[COMB_PIECES] = {};
-  bool ce_batch = true;           // copy-engine plane: cudaMemcpyBatchAsync per chunk (cleared if unsupported)
   bool overlap_shared = true;     // shared experts on s_side, concurrent with routing (EPSMOE_OVERLAP_SHARED=0: in order)
   bool split_rem = false;         // EPSMOE_SPLIT_REM=1: expert GEMMs as bulk on CTA pairs + remainder rows on
                                   // single CTAs; measured 1-3% slower than padding (DSv2, Mixtral), so off
