@@ -10,7 +10,8 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libepsmoe.so")
+# EPSMOE_LIB: another build of the same library (dev A/B of two kernel versions on one box)
+LIB_PATH = os.environ.get("EPSMOE_LIB") or os.path.join(_HERE, "libepsmoe.so")
 
 MOE_MAX_EXPERTS = 256
 MOE_MAX_TOPK = 8

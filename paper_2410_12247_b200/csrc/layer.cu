@@ -261,12 +261,16 @@ int compute_moe(moe_layer* L, const void* A, int64_t a_rows, const int32_t* row_
   return 0;
 }
 
-// Persistent GEMM grid of a forward (the SM partition, NEXT-1): all SMs
-// at ep == 1 and on the copy-engine plane; else 2 * comm_ctas SMs are left to
-// the all2all's kernels (NCCL's two communicators, or the put kernels).
-int gemm_sm_budget(const moe_layer* L) {
+// Grid of the GEMMs issued before the plan exists (router, shared experts) at
+// ep > 1 on the SM-reserving planes: the smallest grid any comm budget of the
+// installed cost model can give, so that they never hold more SMs than the
+// plan later leaves to the GEMMs (the shared experts run beside dispatch(0)).
+int pre_plan_sm_budget(const moe_layer* L) {
   if (L->cfg.ep == 1 || L->cfg.a2a_p2p == 2) return L->num_sms;
-  return L->num_sms - 2 * L->comm_ctas;
+  int cc = L->comm_ctas;
+  const int n = std::min(L->cost.n_comm, (int)MOE_COMM_POINTS);
+  for (int i = 0; i < n; ++i) cc = std::max(cc, (int)L->cost.comm_ctas[i]);
+  return std::max(2, L->num_sms - 2 * cc);
 }
 
 }  // namespace epsmoe
@@ -970,7 +974,7 @@ moe_status_t moe_layer_forward(moe_layer_t* L, const void* x, int64_t T, void* y
   // communicators' kernels or the all2all could not overlap it at all.  The
   // copy-engine plane moves rows without SMs (its flag / wait kernels are one
   // warp and co-reside), so there the GEMMs keep every SM.
-  const int default_ctas = gemm_sm_budget(L);
+  const int default_ctas = pre_plan_sm_budget(L);
   int num_ctas = (plan_in && plan.sm_gemm > 0) ? std::min(plan.sm_gemm, L->num_sms) : default_ctas;
 
   Fwd F{L, x, T, y, plan_in, st, dbg, plan};

@@ -182,7 +182,7 @@ int compute_moe(moe_layer* L, const void* A, int64_t a_rows, const int32_t* row_
                 cudaStream_t st, const int32_t* a_row_index = nullptr, const GemmRowSeg* down_rseg = nullptr,
                 int down_nrseg = 0, uint32_t* const* down_sig = nullptr, int down_nsig = 0, uint32_t down_epoch = 0);
 // Persistent GEMM grid of a forward when the plan does not fix it (the SM partition, NEXT-1).
-int gemm_sm_budget(const moe_layer* L);
+int pre_plan_sm_budget(const moe_layer* L);
 
 // One forward's context, shared by its phases (routing, EP = 1 compute + combine,
 // the EP > 1 pipeline, debug outputs).
