@@ -124,7 +124,7 @@ struct __align__(8) SmemTail {
   uint64_t gfull[Cfg<CG>::STAGES];  // GATHER, peer CTA: its A copies landed (forwarded to the leader)
   uint64_t qfull[TQ];
   uint64_t qempty[TQ];
-  int32_t tq[TQ];
+  int4 tq[TQ];  // published tiles: {t, g, mt, nt | HALF_BIT}
   uint32_t tmem_holder;
   int32_t tile_prefix[MAX_G + 1];
   int32_t gstart[MAX_G];
@@ -198,7 +198,8 @@ __device__ __forceinline__ void store_chunk(const uint32_t (&pk)[16], uint8_t* s
 
 // Linear tile index -> (group, m-tile, n-tile).  Inside a group, tiles are
 // visited in blocks of `gm` m-tiles: n-tile major across the block, m fastest
-// inside it (gm = 1: plain n-fastest order).
+// inside it (gm = 1: plain n-fastest order).  Static scheduling only; the
+// dynamic path decodes once per tile in the ticket fetcher (Tickets::fetch).
 template <int CG>
 __device__ __forceinline__ void decode_tile(const SmemTail<CG>& s, int G, int n_tiles, int gm_cfg, int t, int& g,
                                             int& mt, int& nt) {
@@ -217,61 +218,109 @@ __device__ __forceinline__ void decode_tile(const SmemTail<CG>& s, int G, int n_
   nt = within / gm;
 }
 
+// floor(a / b) for 0 <= a < 2^23, b >= 1: float reciprocal estimate (off by at
+// most one) and an exact integer correction - a few instructions instead of
+// the ~20-instruction integer division sequence.
+__device__ __forceinline__ int fdiv(int a, int b) {
+  int q = __float2int_rz(__int2float_rn(a) * __frcp_rn(__int2float_rn(b)));
+  if (q * b > a) --q;
+  else if ((q + 1) * b <= a) ++q;
+  return q;
+}
+
+constexpr int HALF_BIT = 1 << 30;  // Tile.nt tag: a group's last m-tile with <= BM rows
+
+struct Tile {
+  int t, g, mt, nt;  // t < 0: no more tiles
+  bool half;         // valid rows of the m-tile <= BM (half-tile MMA candidate)
+};
+__device__ __forceinline__ Tile unpack_tile(int4 v) { return Tile{v.x, v.y, v.z, v.w & ~HALF_BIT, (v.w & HALF_BIT) != 0}; }
+
 // Tile-ticket stream shared by every role of a CTA (pair).  The fetcher (the
-// leader's producer lane) takes tickets and publishes them; every other role
-// consumes them in the same order.  Static mode needs no communication.
+// leader's producer lane) takes tickets, decodes each ticket ONCE into
+// (group, m-tile, n-tile, half) and publishes the decoded tile; every other
+// role (MMA issuer, epilogue warps, the peer CTA's producer) consumes it in
+// the same order, so no consumer decodes on its critical path (K = 1536 Down
+// GEMMs change tile every 24 k-blocks).  Static mode needs no communication.
 template <int CG>
 struct Tickets {
   SmemTail<CG>* st;
   const KParams* p;
   int total, unit, num_units;
   uint32_t rank;
+  int G, n_tiles, gm_cfg;
   uint32_t slot = 0, phase = 0;
   int static_next;
   int prefetched = -2;  // fetcher: ticket taken one tile ahead (hides the atomic's latency)
+  int gc = 0;           // fetcher: group cursor (a fetcher's tickets only increase)
 
-  __device__ Tickets(SmemTail<CG>* s, const KParams* pp, int tot, int u, int nu, uint32_t r)
-      : st(s), p(pp), total(tot), unit(u), num_units(nu), rank(r), static_next(u) {}
+  __device__ Tickets(SmemTail<CG>* s, const KParams* pp, int tot, int u, int nu, uint32_t r, int g, int nt, int gm)
+      : st(s), p(pp), total(tot), unit(u), num_units(nu), rank(r), G(g), n_tiles(nt), gm_cfg(gm), static_next(u) {}
 
   __device__ __forceinline__ void advance() {
     if (++slot == TQ) { slot = 0; phase ^= 1; }
   }
-  // Fetcher side (one thread): returns the next tile or -1.
-  __device__ __forceinline__ int fetch() {
+  __device__ __forceinline__ Tile decode_static(int t) const {
+    Tile d{t, 0, 0, 0, false};
+    if (t >= 0) {
+      decode_tile(*st, G, n_tiles, gm_cfg, t, d.g, d.mt, d.nt);
+      d.half = st->gcount[d.g] - d.mt * Cfg<CG>::TILE_M <= BM;
+    }
+    return d;
+  }
+  // Fetcher's decode: group by the monotone cursor, then the raster with fdiv.
+  __device__ __forceinline__ Tile decode_fast(int t) {
+    while (st->tile_prefix[gc + 1] <= t) ++gc;
+    const int p0 = st->tile_prefix[gc];
+    const int local = t - p0;
+    const int m_tiles = fdiv(st->tile_prefix[gc + 1] - p0, n_tiles);
+    const int bsz = gm_cfg >= m_tiles ? m_tiles * n_tiles : gm_cfg * n_tiles;
+    const int blk = fdiv(local, bsz);
+    const int within = local - blk * bsz;
+    const int gm = min(gm_cfg, m_tiles - blk * gm_cfg);
+    const int q = fdiv(within, gm);
+    Tile d{t, gc, blk * gm_cfg + (within - q * gm), q, false};
+    d.half = st->gcount[gc] - d.mt * Cfg<CG>::TILE_M <= BM;
+    return d;
+  }
+  // Fetcher side (one thread): the next tile (t = -1 when done).
+  __device__ __forceinline__ Tile fetch() {
     if (!p->dynamic) {
       int t = static_next;
       static_next += num_units;
-      return t < total ? t : -1;
+      return decode_static(t < total ? t : -1);
     }
     int t = (prefetched == -2) ? atomicAdd(p->tile_counter, 1) : prefetched;
     if (t >= total) t = -1;
     // next ticket in flight while this tile's loads are issued (-1 stays -1)
     prefetched = (t < 0) ? -1 : atomicAdd(p->tile_counter, 1);
+    const Tile d = (t < 0) ? Tile{-1, 0, 0, 0, false} : decode_fast(t);
+    const int4 v = make_int4(d.t, d.g, d.mt, d.nt | (d.half ? HALF_BIT : 0));
     ptx::mbar_wait(ptx::smem_u32(&st->qempty[slot]), phase ^ 1);  // releases are relaxed: no acquire needed
-    st->tq[slot] = t;
+    st->tq[slot] = v;
     ptx::mbar_arrive(ptx::smem_u32(&st->qfull[slot]));
     if constexpr (CG == 2) {
-      ptx::st_cluster_u32(ptx::mapa(ptx::smem_u32(&st->tq[slot]), 1), (uint32_t)t);
+      ptx::st_cluster_v4(ptx::mapa(ptx::smem_u32(&st->tq[slot]), 1), v);
       ptx::mbar_arrive_cluster(ptx::mapa(ptx::smem_u32(&st->qfull[slot]), 1));
     }
     advance();
-    return t;
+    return d;
   }
   // Consumer side: `arrive` = this thread releases the ticket for its role.
-  __device__ __forceinline__ int consume(bool arrive) {
+  __device__ __forceinline__ Tile consume(bool arrive) {
     if (!p->dynamic) {
       int t = static_next;
       static_next += num_units;
-      return t < total ? t : -1;
+      return decode_static(t < total ? t : -1);
     }
     if (CG == 2 && rank != 0)
       ptx::mbar_wait_cluster(ptx::smem_u32(&st->qfull[slot]), phase);  // ticket written by the leader (DSMEM)
     else
       ptx::mbar_wait(ptx::smem_u32(&st->qfull[slot]), phase);
-    const int t = st->tq[slot];
+    const Tile d = unpack_tile(st->tq[slot]);
     if (arrive) release(slot);
     advance();
-    return t;
+    return d;
   }
   // Release a consumed ticket slot on the fetcher's qempty barrier.
   __device__ __forceinline__ void release(uint32_t s) {
@@ -383,7 +432,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
   ptx::tc_fence_after();
   const uint32_t tmem_base = st.tmem_holder;
   const int total = st.tile_prefix[G];
-  Tickets<CG> tk(&st, &p, total, unit, num_units, rank);
+  Tickets<CG> tk(&st, &p, total, unit, num_units, rank, G, n_tiles, p.raster_gm);
 
   if (warp == 0) {
     // ===================== TMA producer (each CTA loads its own halves) =====================
@@ -396,13 +445,23 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
     int32_t gidx[GATHER ? BM / 4 : 1];
     const size_t a_pitch = (size_t)p.K * 2;
     while (true) {
-      int t = 0;
-      if (lane == 0) t = (rank == 0) ? tk.fetch() : tk.consume(true);
-      t = __shfl_sync(0xffffffffu, t, 0);
-      if (t < 0) break;
-      int g, mt, nt;
-      decode_tile(st, G, n_tiles, p.raster_gm, t, g, mt, nt);
-      const bool half = HALF_OK && p.half_tiles && st.gcount[g] - mt * C::TILE_M <= BM;
+      int4 tv = make_int4(0, 0, 0, 0);
+      if (lane == 0) {
+        const Tile d = (rank == 0) ? tk.fetch() : tk.consume(true);
+        tv = make_int4(d.t, d.g, d.mt, d.nt | (d.half ? HALF_BIT : 0));
+      }
+      if constexpr (GATHER) {
+        tv.x = __shfl_sync(0xffffffffu, tv.x, 0);
+        tv.y = __shfl_sync(0xffffffffu, tv.y, 0);
+        tv.z = __shfl_sync(0xffffffffu, tv.z, 0);
+        tv.w = __shfl_sync(0xffffffffu, tv.w, 0);
+      } else if (lane != 0) {
+        break;  // TMA: lane 0 alone
+      }
+      const Tile d = unpack_tile(tv);
+      if (d.t < 0) break;
+      const int g = d.g, mt = d.mt, nt = d.nt;
+      const bool half = HALF_OK && p.half_tiles && d.half;
       const int a_row = st.gstart[g] + mt * C::TILE_M + (int)rank * (half ? BM / 2 : BM);
       const int b_row0 = (p.b_base + g) * p.b_group_rows + nt * n_out_tile;
       if constexpr (GATHER) {
@@ -476,14 +535,10 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
       constexpr uint32_t idesc_half = ptx::idesc_bf16_f32(C::TILE_M / 2, BN);
       uint32_t stage = 0, phase = 0, iter = 0;
       while (true) {
-        const int t = tk.consume(true);
-        if (t < 0) break;
+        const Tile d = tk.consume(true);
+        if (d.t < 0) break;
         uint32_t idesc = (EPI == EPI_F32) ? ptx::idesc_bf16_f32(C::TILE_M, p.n_mma) : idesc_full;
-        if (HALF_OK && p.half_tiles) {
-          int g, mt, nt;
-          decode_tile(st, G, n_tiles, p.raster_gm, t, g, mt, nt);
-          if (st.gcount[g] - mt * C::TILE_M <= BM) idesc = idesc_half;
-        }
+        if (HALF_OK && p.half_tiles && d.half) idesc = idesc_half;
         const uint32_t acc = iter & 1, accph = (iter >> 1) & 1;
         ptx::mbar_wait(ptx::smem_u32(&st.tempty[acc]), accph ^ 1);
         ptx::tc_fence_after();
@@ -519,7 +574,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
       // cluster-release arrive on the leader's full barrier
       if (lane == 0 && rank == 1) {
         uint32_t stage = 0, phase = 0;
-        while (tk.consume(true) >= 0) {
+        while (tk.consume(true).t >= 0) {
           for (int kb = 0; kb < num_kb; ++kb) {
             ptx::mbar_wait(ptx::smem_u32(&st.gfull[stage]), phase);
             ptx::fence_proxy_async_smem();
@@ -536,16 +591,15 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
     const uint32_t tempty_leader1 = (CG == 2) ? ptx::mapa(ptx::smem_u32(&st.tempty[1]), 0) : 0;
     uint32_t iter = 0;
     while (true) {
-      const int t = tk.consume(false);
+      const Tile d = tk.consume(false);
       __syncwarp();
       if (lane == 0 && p.dynamic) tk.release((tk.slot + TQ - 1) % TQ);  // once per warp
-      if (t < 0) break;
-      int g, mt, nt;
-      decode_tile(st, G, n_tiles, p.raster_gm, t, g, mt, nt);
+      if (d.t < 0) break;
+      const int g = d.g, mt = d.mt, nt = d.nt;
       const uint32_t acc = iter & 1, accph = (iter >> 1) & 1;
       ptx::mbar_wait(ptx::smem_u32(&st.tfull[acc]), accph);
       ptx::tc_fence_after();
-      const bool half = HALF_OK && p.half_tiles && st.gcount[g] - mt * C::TILE_M <= BM;
+      const bool half = HALF_OK && p.half_tiles && d.half;
       const int hq = half ? (q >> 1) : 0;  // half tile: which 128 (Down) / 64 (SwiGLU) column half
       const int local_row = half ? mt * C::TILE_M + (int)rank * (BM / 2) + (q & 1) * 32 + lane
                                  : mt * C::TILE_M + (int)rank * BM + q * 32 + lane;
