@@ -72,7 +72,8 @@ struct KParams {
   int dynamic;    // 1: dynamic tile tickets (tile_counter), 0: static round robin
   int row_mode;   // 0 all rows, 1 bulk (multiple of 256), 2 remainder (see GemmArgs)
   int diag;       // diagnostics only (EPSMOE_GEMM_DIAG): 1 skip output stores, 2 skip TMEM loads + stores,
-                  // 3 bulk stores into a 256-row window (L2-resident: same store traffic, no DRAM writes)
+                  // 3 bulk stores into a 256-row window (L2-resident: same store traffic, no DRAM writes),
+                  // 4 skip the MMAs (the load pipeline alone), 5 skip the operand loads (the MMA issue alone)
   int tma_store;  // bf16 outputs: full 32-row warp slices leave through TMA bulk-tensor stores (tmO)
   int half_tiles;
   int n_mma;       // MMA N: BN, or for EPI_F32 (the router, N = E) E rounded up to 16 - no 256-column padding  // CTA pairs: a group's last m-tile with <= 128 rows runs as an M = 128 2-CTA MMA (see kernel)
@@ -94,6 +95,7 @@ struct KParams {
   const float* comb_w;
   int comb_k;
   int32_t* resident;  // SM-partition probe (GemmArgs::resident) or nullptr
+  int a_wrap;         // diagnostics only (GemmArgs::a_wrap)
 };
 
 constexpr int COMB_MAX_K = 8;
@@ -462,7 +464,8 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
       if (d.t < 0) break;
       const int g = d.g, mt = d.mt, nt = d.nt;
       const bool half = HALF_OK && p.half_tiles && d.half;
-      const int a_row = st.gstart[g] + mt * C::TILE_M + (int)rank * (half ? BM / 2 : BM);
+      int a_row = st.gstart[g] + mt * C::TILE_M + (int)rank * (half ? BM / 2 : BM);
+      if (p.a_wrap) a_row %= p.a_wrap;
       const int b_row0 = (p.b_base + g) * p.b_group_rows + nt * n_out_tile;
       if constexpr (GATHER) {
         // this lane's rows of the tile: chunk (lane & 7) of rows (lane >> 3) + 4 i;
@@ -481,6 +484,11 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
           const uint32_t fb = ptx::smem_u32(&st.full[stage]);
           const uint32_t a_dst = ptx::smem_u32(sA + stage * C::A_BYTES);
           const uint32_t b_dst = ptx::smem_u32(sB + stage * C::B_BYTES);
+          if (!GATHER && p.diag == 5) {  // diagnostics: no operand loads (the MMA runs on stale smem)
+            if (rank == 0) ptx::mbar_arrive(fb);
+            if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+            continue;
+          }
           if ((CG == 1 || rank == 0) && lane == 0)
             ptx::mbar_arrive_expect_tx(fb, CG * ((GATHER ? 0 : (half ? C::A_BYTES / 2 : C::A_BYTES)) +
                                                  (EPI == EPI_F32 ? (p.n_mma / CG) * BK * 2 : C::B_BYTES)));
@@ -554,6 +562,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
           const uint64_t bdesc = ptx::sdesc_k_sw128(ptx::smem_u32(sB + stage * C::B_BYTES));
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k) {
+            if (p.diag == 4) break;  // warp-uniform; hoisted out of the unrolled MMAs
             // advance 16 bf16 = 32 B along K inside the 128 B swizzle atom
             if constexpr (CG == 1)
               ptx::mma_bf16_ss(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (kb | k) != 0);
@@ -962,6 +971,7 @@ int launch_epi(const GemmArgs& a, cudaStream_t stream) {
   p.comb_k = a.comb_k;
   p.resident = a.resident;
   p.diag = env_int("EPSMOE_GEMM_DIAG", 0);
+  p.a_wrap = a.a_wrap;
   p.n_mma = n_mma;
   p.half_tiles = (CG == 2 && !GATHER && (EPI == EPI_SWIGLU || EPI == EPI_BF16) && a.row_mode == 0) ? half_env : 0;
   CUtensorMap tO;
