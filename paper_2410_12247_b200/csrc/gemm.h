@@ -70,7 +70,6 @@ struct GemmArgs {
   // optional SM-partition probe (device int32[2]): each CTA adds itself to [0]
   // while resident and records the running maximum in [1]
   int32_t* resident;
-  int a_wrap = 0;  // diagnostics only (EPSMOE_DIAG_SEND_WRAP): A row r is read from row r % a_wrap
 };
 
 // Launch on `stream`.  Returns a cudaError_t-compatible code (0 = success).

@@ -72,10 +72,7 @@ struct KParams {
   int dynamic;    // 1: dynamic tile tickets (tile_counter), 0: static round robin
   int row_mode;   // 0 all rows, 1 bulk (multiple of 256), 2 remainder (see GemmArgs)
   int diag;       // diagnostics only (EPSMOE_GEMM_DIAG): 1 skip output stores, 2 skip TMEM loads + stores,
-                  // 3 bulk stores into a 256-row window (L2-resident: same store traffic, no DRAM writes),
-                  // 4 skip the MMAs (the load pipeline alone), 5 skip the operand loads (the MMA issue alone),
-                  // 6 / 7 skip the B / A loads (half the operand bytes; the MMA reads that operand stale),
-                  // 10 single-buffered accumulator (the MMA waits for the previous tile's drain)
+                  // 3 bulk stores into a 256-row window (L2-resident: same store traffic, no DRAM writes)
   int tma_store;  // bf16 outputs: full 32-row warp slices leave through TMA bulk-tensor stores (tmO)
   int half_tiles;
   int n_mma;       // MMA N: BN, or for EPI_F32 (the router, N = E) E rounded up to 16 - no 256-column padding  // CTA pairs: a group's last m-tile with <= 128 rows runs as an M = 128 2-CTA MMA (see kernel)
@@ -97,7 +94,6 @@ struct KParams {
   const float* comb_w;
   int comb_k;
   int32_t* resident;  // SM-partition probe (GemmArgs::resident) or nullptr
-  int a_wrap;         // diagnostics only (GemmArgs::a_wrap)
 };
 
 constexpr int COMB_MAX_K = 8;
@@ -466,8 +462,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
       if (d.t < 0) break;
       const int g = d.g, mt = d.mt, nt = d.nt;
       const bool half = HALF_OK && p.half_tiles && d.half;
-      int a_row = st.gstart[g] + mt * C::TILE_M + (int)rank * (half ? BM / 2 : BM);
-      if (p.a_wrap) a_row %= p.a_wrap;
+      const int a_row = st.gstart[g] + mt * C::TILE_M + (int)rank * (half ? BM / 2 : BM);
       const int b_row0 = (p.b_base + g) * p.b_group_rows + nt * n_out_tile;
       if constexpr (GATHER) {
         // this lane's rows of the tile: chunk (lane & 7) of rows (lane >> 3) + 4 i;
@@ -486,15 +481,9 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
           const uint32_t fb = ptx::smem_u32(&st.full[stage]);
           const uint32_t a_dst = ptx::smem_u32(sA + stage * C::A_BYTES);
           const uint32_t b_dst = ptx::smem_u32(sB + stage * C::B_BYTES);
-          if (!GATHER && p.diag == 5) {  // diagnostics: no operand loads (the MMA runs on stale smem)
-            if (rank == 0) ptx::mbar_arrive(fb);
-            if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
-            continue;
-          }
-          const bool skip_a = p.diag == 7, skip_b = p.diag == 6;  // diagnostics: one operand stale
           if ((CG == 1 || rank == 0) && lane == 0)
-            ptx::mbar_arrive_expect_tx(fb, CG * ((GATHER || skip_a ? 0 : (half ? C::A_BYTES / 2 : C::A_BYTES)) +
-                                                 (skip_b ? 0 : EPI == EPI_F32 ? (p.n_mma / CG) * BK * 2 : C::B_BYTES)));
+            ptx::mbar_arrive_expect_tx(fb, CG * ((GATHER ? 0 : (half ? C::A_BYTES / 2 : C::A_BYTES)) +
+                                                 (EPI == EPI_F32 ? (p.n_mma / CG) * BK * 2 : C::B_BYTES)));
           if constexpr (GATHER) {
             // A by 16-B cp.async straight into the 128-B swizzle (chunk c of row r at
             // c ^ (r & 7)): 4 rows x 128 B per warp instruction, no TMA descriptor per row
@@ -512,14 +501,12 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
               if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
               continue;
             }
-          } else if (skip_a) {
           } else if constexpr (CG == 1) {
             ptx::tma_load_2d(a_dst, &tmA, fb, kb * BK, a_row);
           } else {
             ptx::tma_load_2d_pair(a_dst, half ? &tmAh : &tmA, fb, kb * BK, a_row);
           }
-          if (skip_b) {
-          } else if constexpr (CG == 1) {
+          if constexpr (CG == 1) {
             if (EPI == EPI_SWIGLU) {
               ptx::tma_load_2d(b_dst, &tmB0, fb, kb * BK, b_row0);
               ptx::tma_load_2d(b_dst + C::B_BYTES / 2, &tmB1, fb, kb * BK, b_row0);
@@ -554,8 +541,6 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
         if (HALF_OK && p.half_tiles && d.half) idesc = idesc_half;
         const uint32_t acc = iter & 1, accph = (iter >> 1) & 1;
         ptx::mbar_wait(ptx::smem_u32(&st.tempty[acc]), accph ^ 1);
-        if (p.diag == 10 && iter > 0)  // diagnostics: single-buffered accumulator (wait for the previous drain)
-          ptx::mbar_wait(ptx::smem_u32(&st.tempty[(iter - 1) & 1]), ((iter - 1) >> 1) & 1);
         ptx::tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
         for (int kb = 0; kb < num_kb; ++kb) {
@@ -569,7 +554,6 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
           const uint64_t bdesc = ptx::sdesc_k_sw128(ptx::smem_u32(sB + stage * C::B_BYTES));
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k) {
-            if (p.diag == 4) break;  // warp-uniform; hoisted out of the unrolled MMAs
             // advance 16 bf16 = 32 B along K inside the 128 B swizzle atom
             if constexpr (CG == 1)
               ptx::mma_bf16_ss(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (kb | k) != 0);
@@ -978,7 +962,6 @@ int launch_epi(const GemmArgs& a, cudaStream_t stream) {
   p.comb_k = a.comb_k;
   p.resident = a.resident;
   p.diag = env_int("EPSMOE_GEMM_DIAG", 0);
-  p.a_wrap = a.a_wrap;
   p.n_mma = n_mma;
   p.half_tiles = (CG == 2 && !GATHER && (EPI == EPI_SWIGLU || EPI == EPI_BF16) && a.row_mode == 0) ? half_env : 0;
   CUtensorMap tO;

@@ -198,7 +198,6 @@ int compute_moe(moe_layer* L, const void* A, int64_t a_rows, const int32_t* row_
   g1a.out = L->h;
   g1a.ldo = c.ffn;
   g1a.out_rows = L->gemm_rows_cap;
-  if (A == L->send) { const char* w = std::getenv("EPSMOE_DIAG_SEND_WRAP"); g1a.a_wrap = w ? std::atoi(w) : 0; }  // diagnostics only
   GemmArgs g2a = layer_args(L, EPI_BF16, num_ctas);
   g2a.rows_hint = rows_per_group;
   g2a.rseg = down_rseg;  // DownGemm fused with the combine all2all (a2a_p2p)

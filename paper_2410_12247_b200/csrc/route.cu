@@ -340,7 +340,7 @@ permute_kernel(const __nv_bfloat16* __restrict__ x, int T, int H, int E, int k,
                const int32_t* __restrict__ topk_idx, const int32_t* __restrict__ range_off,
                const int32_t* __restrict__ seg_start, int R, int rt, __nv_bfloat16* __restrict__ send,
                int32_t* __restrict__ pos, int32_t* __restrict__ row_token, uint8_t* __restrict__ sendq,
-               int qpitch, int wrap) {
+               int qpitch) {
   __shared__ int32_t off_s[WARPS_R][256];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int r = blockIdx.x * WARPS_R + warp;
@@ -412,7 +412,6 @@ permute_kernel(const __nv_bfloat16* __restrict__ x, int T, int H, int E, int k,
       }
       for (int j = 0; j < k; ++j) {
         int d = __shfl_sync(0xffffffffu, dest, j);
-        if (wrap) d %= wrap;  // diagnostics only (EPSMOE_DIAG_SEND_WRAP)
         uint4* dst = reinterpret_cast<uint4*>(send + (int64_t)d * H);
 #pragma unroll
         for (int i = 0; i < MAXV; ++i) {
@@ -598,16 +597,15 @@ int launch_permute(const void* x, int T, int H, int E, int k, const int32_t* top
   auto xb = (const __nv_bfloat16*)x;
   auto sb = (__nv_bfloat16*)send;
   auto qb = (uint8_t*)sendq;
-  static const int wrap = std::getenv("EPSMOE_DIAG_SEND_WRAP") ? std::atoi(std::getenv("EPSMOE_DIAG_SEND_WRAP")) : 0;
   if (fp8 == 0)
     permute_kernel<0><<<grid, block, 0, st>>>(xb, T, H, E, k, topk_idx, range_off, seg_start, R, rt, sb, pos, row_token,
-                                              qb, qpitch, wrap);
+                                              qb, qpitch);
   else if (fp8 == 1)
     permute_kernel<1><<<grid, block, 0, st>>>(xb, T, H, E, k, topk_idx, range_off, seg_start, R, rt, sb, pos, row_token,
-                                              qb, qpitch, wrap);
+                                              qb, qpitch);
   else
     permute_kernel<2><<<grid, block, 0, st>>>(xb, T, H, E, k, topk_idx, range_off, seg_start, R, rt, sb, pos, row_token,
-                                              qb, qpitch, wrap);
+                                              qb, qpitch);
   return (int)cudaGetLastError();
 }
 
