@@ -334,7 +334,7 @@ __global__ void __launch_bounds__(256) seg_scan_kernel(const int32_t* __restrict
 // fp8: 0 = bf16 rows; 1 = bf16 rows of the FP8 round trip (ep == 1: the
 // values experts see when the payload is FP8); 2 = packed FP8 rows of `qpitch`
 // bytes (H e4m3 bytes, then H/128 int8 block exponents) into `sendq`.
-template <int fp8>
+template <int fp8, bool SPLIT>
 __global__ void __launch_bounds__(WARPS_R * 32, 4)
 permute_kernel(const __nv_bfloat16* __restrict__ x, int T, int H, int E, int k,
                const int32_t* __restrict__ topk_idx, const int32_t* __restrict__ range_off,
@@ -355,8 +355,10 @@ permute_kernel(const __nv_bfloat16* __restrict__ x, int T, int H, int E, int k,
     if (lane < k) {
       int e = topk_idx[(int64_t)t * k + lane];
       dest = off_s[warp][e];
-      pos[(int64_t)t * k + lane] = dest;
-      if (row_token) row_token[dest] = t;
+      if (!SPLIT || blockIdx.y == 0) {  // column splits (small batches): the first writes the indices
+        pos[(int64_t)t * k + lane] = dest;
+        if (row_token) row_token[dest] = t;
+      }
     }
     __syncwarp();
     if (lane < k) {
@@ -368,12 +370,16 @@ permute_kernel(const __nv_bfloat16* __restrict__ x, int T, int H, int E, int k,
     const uint4* src = reinterpret_cast<const uint4*>(x + (int64_t)t * H);
     // 16 x 16 B per lane in flight per pass (H <= 4096 per pass, <= 2 passes):
     // keeps the kernel under 128 registers so it co-resides with a GEMM CTA.
+    // Small batches split a row's 32-vector blocks over gridDim.y warps
+    // (blocks y, y + Y, ...); every value is copied / quantised exactly as unsplit.
     constexpr int MAXV = 16;
-    for (int base = 0; base < nvec; base += 32 * MAXV) {
+    const int stride = SPLIT ? 32 * (int)gridDim.y : 32;  // vectors between a warp's consecutive blocks
+    for (int base = (SPLIT ? 32 * (int)blockIdx.y : 0) + lane; base - lane < nvec; base += MAXV * stride) {
+      // this lane's vector of pass slot i: base + i * stride (>= nvec: none)
       uint4 buf[MAXV];
 #pragma unroll
       for (int i = 0; i < MAXV; ++i) {
-        int c = base + lane + 32 * i;
+        int c = base + i * stride;
         if (c < nvec) buf[i] = ld_stream(src + c, pol);
       }
       if constexpr (fp8 != 0) {
@@ -381,7 +387,7 @@ permute_kernel(const __nv_bfloat16* __restrict__ x, int T, int H, int E, int k,
         int sexp[MAXV];
 #pragma unroll
         for (int i = 0; i < MAXV; ++i) {
-          float m = (base + lane + 32 * i < nvec) ? amax8(buf[i]) : 0.f;
+          float m = (base + i * stride < nvec) ? amax8(buf[i]) : 0.f;
 #pragma unroll
           for (int off = 8; off > 0; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
           sexp[i] = fp8_block_exp(m);
@@ -389,18 +395,18 @@ permute_kernel(const __nv_bfloat16* __restrict__ x, int T, int H, int E, int k,
         if (fp8 == 1) {
 #pragma unroll
           for (int i = 0; i < MAXV; ++i)
-            if (base + lane + 32 * i < nvec) buf[i] = dequant8(quant8(buf[i], pow2f(-sexp[i])), pow2f(sexp[i]));
+            if (base + i * stride < nvec) buf[i] = dequant8(quant8(buf[i], pow2f(-sexp[i])), pow2f(sexp[i]));
         } else {
           uint2 q[MAXV];
 #pragma unroll
           for (int i = 0; i < MAXV; ++i)
-            if (base + lane + 32 * i < nvec) q[i] = quant8(buf[i], pow2f(-sexp[i]));
+            if (base + i * stride < nvec) q[i] = quant8(buf[i], pow2f(-sexp[i]));
           for (int j = 0; j < k; ++j) {
             int d = __shfl_sync(0xffffffffu, dest, j);
             uint8_t* row = sendq + (int64_t)d * qpitch;
 #pragma unroll
             for (int i = 0; i < MAXV; ++i) {
-              const int c = base + lane + 32 * i;
+              const int c = base + i * stride;
               if (c < nvec) {
                 reinterpret_cast<uint2*>(row)[c] = q[i];
                 if ((lane & 15) == 0) row[H + (c >> 4)] = (uint8_t)(int8_t)sexp[i];
@@ -415,7 +421,7 @@ permute_kernel(const __nv_bfloat16* __restrict__ x, int T, int H, int E, int k,
         uint4* dst = reinterpret_cast<uint4*>(send + (int64_t)d * H);
 #pragma unroll
         for (int i = 0; i < MAXV; ++i) {
-          int c = base + lane + 32 * i;
+          int c = base + i * stride;
           if (c < nvec) st_stream(dst + c, buf[i], pol);
         }
       }
@@ -443,6 +449,7 @@ __global__ void __launch_bounds__(256) dequant_rows_kernel(const uint8_t* __rest
 // K7 LocalReduce fused into combine (R7): one warp per token,
 // acc = fp32(s) (0 without shared experts); acc = fmaf(w_j, o[pos[t][j]], acc)
 // in slot order; y = bf16(acc).
+template <bool SPLIT>
 __global__ void __launch_bounds__(WARPS * 32)
 combine_kernel(const __nv_bfloat16* __restrict__ o, const __nv_bfloat16* __restrict__ s, int T, int H,
                int k, const int32_t* __restrict__ pos, const float* __restrict__ topk_w,
@@ -466,7 +473,10 @@ combine_kernel(const __nv_bfloat16* __restrict__ o, const __nv_bfloat16* __restr
     orow[j] = reinterpret_cast<const uint4*>(o + (int64_t)row * H);
     wj[j] = __shfl_sync(0xffffffffu, pw, j < k ? j : 0);
   }
-  for (int c = lane; c < nvec; c += 32) {
+  // small batches: gridDim.y warps share a token's columns (interleaved 32-vector
+  // blocks); each element's arithmetic is unchanged
+  const int stride = SPLIT ? 32 * (int)gridDim.y : 32;
+  for (int c = (SPLIT ? 32 * (int)blockIdx.y : 0) + lane; c < nvec; c += stride) {
     // all k rows in flight first, then the fmaf chain in slot order (R4)
     uint4 ov[MAX_K];
 #pragma unroll
@@ -587,25 +597,34 @@ int launch_range_scan(const int32_t* range_hist, int T, int E, int32_t* range_of
   return (int)cudaGetLastError();
 }
 
+// Column splits for small batches: enough warps to cover the SMs (a warp per
+// token alone leaves decode batches latency-bound).
+static int column_splits(int64_t rows, int H) {
+  const int64_t target = 148 * 16;  // warps
+  const int max_split = std::max(1, (H / 8) / 32);
+  return (int)std::max<int64_t>(1, std::min<int64_t>(max_split, (target + rows - 1) / std::max<int64_t>(rows, 1)));
+}
+
 int launch_permute(const void* x, int T, int H, int E, int k, const int32_t* topk_idx, const int32_t* range_off,
                    const int32_t* seg_start, void* send, int32_t* pos, int32_t* row_token, int fp8, void* sendq,
                    int qpitch, cudaStream_t st) {
   int R = num_ranges(T);
   const int rt = range_len(T);
   if (R == 0) return 0;
-  const dim3 grid((R + WARPS_R - 1) / WARPS_R), block(WARPS_R * 32);
+  const int splits = column_splits(R, H);
+  const dim3 grid((R + WARPS_R - 1) / WARPS_R, splits), block(WARPS_R * 32);
   auto xb = (const __nv_bfloat16*)x;
   auto sb = (__nv_bfloat16*)send;
   auto qb = (uint8_t*)sendq;
   if (fp8 == 0)
-    permute_kernel<0><<<grid, block, 0, st>>>(xb, T, H, E, k, topk_idx, range_off, seg_start, R, rt, sb, pos, row_token,
-                                              qb, qpitch);
+    (splits > 1 ? permute_kernel<0, true> : permute_kernel<0, false>)<<<grid, block, 0, st>>>(
+        xb, T, H, E, k, topk_idx, range_off, seg_start, R, rt, sb, pos, row_token, qb, qpitch);
   else if (fp8 == 1)
-    permute_kernel<1><<<grid, block, 0, st>>>(xb, T, H, E, k, topk_idx, range_off, seg_start, R, rt, sb, pos, row_token,
-                                              qb, qpitch);
+    (splits > 1 ? permute_kernel<1, true> : permute_kernel<1, false>)<<<grid, block, 0, st>>>(
+        xb, T, H, E, k, topk_idx, range_off, seg_start, R, rt, sb, pos, row_token, qb, qpitch);
   else
-    permute_kernel<2><<<grid, block, 0, st>>>(xb, T, H, E, k, topk_idx, range_off, seg_start, R, rt, sb, pos, row_token,
-                                              qb, qpitch);
+    (splits > 1 ? permute_kernel<2, true> : permute_kernel<2, false>)<<<grid, block, 0, st>>>(
+        xb, T, H, E, k, topk_idx, range_off, seg_start, R, rt, sb, pos, row_token, qb, qpitch);
   return (int)cudaGetLastError();
 }
 
@@ -619,7 +638,9 @@ int launch_dequant_rows(const void* q, int64_t rows, int H, int qpitch, void* ou
 int launch_combine(const void* o, const void* s, int T, int H, int k, const int32_t* pos, const float* topk_w,
                    void* y, cudaStream_t st) {
   if (T == 0) return 0;
-  combine_kernel<<<(T + WARPS - 1) / WARPS, WARPS * 32, 0, st>>>((const __nv_bfloat16*)o,
+  const int splits = column_splits(T, H);
+  const dim3 grid((T + WARPS - 1) / WARPS, splits);
+  (splits > 1 ? combine_kernel<true> : combine_kernel<false>)<<<grid, WARPS * 32, 0, st>>>((const __nv_bfloat16*)o,
                                                                  (const __nv_bfloat16*)s, T, H, k, pos, topk_w,
                                                                  (__nv_bfloat16*)y);
   return (int)cudaGetLastError();
