@@ -974,6 +974,14 @@ int launch_epi(const GemmArgs& a, cudaStream_t stream) {
   p.tile_counter = a.tile_counter ? a.tile_counter : ticket_counter(0);
   p.dynamic = (dynamic_sched() && p.tile_counter) ? 1 : 0;
   int grid = a.num_ctas;
+  if (!a.row_count) {
+    // one dense group (router, shared experts): no more CTAs than tiles - idle
+    // persistent CTAs would only hold SMs a concurrent kernel could use (decode)
+    const int n_out = (EPI == EPI_SWIGLU) ? 128 : BN;
+    const int64_t tiles =
+        ((int64_t)a.m_single + BM * CG - 1) / (BM * CG) * (int64_t)((a.N + n_out - 1) / n_out);
+    if (tiles * CG < grid) grid = (int)(tiles * CG);
+  }
   if (CG == 2) grid &= ~1;
   if (grid < CG) grid = CG;
   cudaLaunchConfig_t cfg = {};

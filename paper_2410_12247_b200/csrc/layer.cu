@@ -398,6 +398,7 @@ static moe_status_t create_impl(const moe_config_t* cfg, const moe_weights_t* w,
   }
   default_cost_model(L->cfg, &L->cost);
   if (const char* ov = std::getenv("EPSMOE_OVERLAP_SHARED")) L->overlap_shared = std::atoi(ov) != 0;
+  if (const char* ds = std::getenv("EPSMOE_DECODE_SIDE")) L->decode_side = std::atoi(ds) != 0;
   if (const char* fc = std::getenv("EPSMOE_FUSE_COMBINE")) L->fuse_combine = std::atoi(fc);
   if (const char* gv = std::getenv("EPSMOE_GATHER")) L->gather_a = std::atoi(gv) != 0;
   if (const char* pf = std::getenv("EPSMOE_P2P_FUSE")) L->p2p_fuse = std::atoi(pf) != 0;
@@ -683,8 +684,8 @@ moe_status_t fwd_routing(Fwd& F) {
   float* topk_w = F.topk_w;
   const bool override_routing = F.override_routing;
   // ---- Router (K1) + topKGating (K2) + histogram
-  int p0 = prof_rec(L, st);
-  if (T > 0 && !override_routing) {
+  auto router = [&]() -> int {
+    if (T == 0 || override_routing) return 0;
     GemmArgs ra = layer_args(L, EPI_F32, num_ctas);
     ra.A = x;
     ra.a_rows = T;
@@ -697,10 +698,8 @@ moe_status_t fwd_routing(Fwd& F) {
     ra.bias = L->w.router_bias;
     ra.m_single = (int)T;
     ra.tile_counter = L->tickets;
-    KERNEL_TRY(gemm_launch(ra, st));
-  }
-  int p1 = prof_rec(L, st);
-  prof_mark(L, MOE_STAGE_ROUTER, p0, p1);
+    return gemm_launch(ra, st);
+  };
 
   // Shared experts depend only on x: they run on s_side, concurrently
   // with topKGating / split (HBM-bound kernels that co-reside with the GEMM's
@@ -754,10 +753,26 @@ moe_status_t fwd_routing(Fwd& F) {
   // ep == 1: the routing kernels stream with L2 evict-first hints, so they
   // co-run with the shared GEMMs (measured ~1% faster per layer than in order).
   const bool has_shared = L->SF && T > 0 && !(L->comm_only && D > 1);
-  // (small decode batches: the routing kernels are latency-bound and a concurrent
-  // persistent GEMM only delays them, so they stay in order below 8K tokens)
-  const bool side = has_shared && (D > 1 || (L->overlap_shared && T >= 8192));
-  if (side) {
+  // Small ep == 1 batches (decode): the router and shared GEMMs each fill only a
+  // few SMs (their grids stop at the tile count) and both need only x, so the
+  // shared experts start with the router instead of after it and the whole
+  // latency-bound routing chain runs beside them.
+  const bool side_early = has_shared && D == 1 && L->overlap_shared && T < 8192 && !fuse && L->decode_side;
+  if (side_early) {
+    CUDA_TRY(cudaEventRecord(L->ev_router, st));
+    CUDA_TRY(cudaStreamWaitEvent(L->s_side, L->ev_router, 0));
+    int e = shared_experts(L->s_side);
+    if (e) { set_error(std::string("shared experts: ") + cudaGetErrorString((cudaError_t)e)); return MOE_ERR_CUDA; }
+    CUDA_TRY(cudaEventRecord(L->ev_shared, L->s_side));
+  }
+  int p0 = prof_rec(L, st);
+  if (T > 0 && !override_routing) KERNEL_TRY(router());
+  int p1 = prof_rec(L, st);
+  prof_mark(L, MOE_STAGE_ROUTER, p0, p1);
+  // (at larger batches the persistent router grid covers every SM: the shared
+  // experts follow it on s_side, concurrent with topKGating / split)
+  const bool side = has_shared && (side_early || D > 1 || (L->overlap_shared && T >= 8192));
+  if (side && !side_early) {
     CUDA_TRY(cudaEventRecord(L->ev_router, st));
     CUDA_TRY(cudaStreamWaitEvent(L->s_side, L->ev_router, 0));
     int e = shared_experts(L->s_side);

@@ -96,6 +96,7 @@ struct moe_layer {
   static constexpr int COMB_PIECES = 4;
   cudaEvent_t ev_piece[COMB_PIECES] = {};
   bool overlap_shared = true;     // shared experts on s_side, concurrent with routing (EPSMOE_OVERLAP_SHARED=0: in order)
+  bool decode_side = true;        // ep == 1, T < 8192: shared experts concurrent with the router too (EPSMOE_DECODE_SIDE)
   bool split_rem = false;         // EPSMOE_SPLIT_REM=1: expert GEMMs as bulk on CTA pairs + remainder rows on
                                   // single CTAs; measured 1-3% slower than padding (DSv2, Mixtral), so off
   int comm_ctas = 0;              // ep > 1: NCCL maxCTAs per communicator (EPSMOE_COMM_CTAS, default 8);
