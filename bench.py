@@ -477,7 +477,25 @@ def ours(args, cfg):
     burst = float(peaks.get("bf16_tflops", FALLBACK_PEAKS["bf16_tflops"]))
     nsm = torch.cuda.get_device_properties(dev).multi_processor_count
     clock_peak = 8192.0 * nsm * clk["sm_mhz"] * 1e6 / 1e12 if clk and clk.get("sm_mhz") else None
-    roofline = {"bound": "tensor", "kernel": "gemm_kernel<EPI_SWIGLU> (GateUpGemm+SiluAct)",
+    # GateUp's algorithmic HBM bytes: the activated experts' gate+up weights once, its A rows read and
+    # its h rows written once.  Decode batches stream weights (bytes / HBM peak > FLOPs / tensor peak):
+    # there the kernel's roofline is HBM, reported in GB/s against the measured copy bandwidth.
+    act_me = int((ghist[:, rank * E_loc:(rank + 1) * E_loc].sum(axis=0) > 0).sum())
+    gu_bytes = 2.0 * (2 * H * F * act_me + rows_me * H + rows_me * F)
+    hbm_pk = float(peaks.get("hbm_gbs", FALLBACK_PEAKS["hbm_gbs"]))
+    if gu_bytes / (hbm_pk * 1e9) > gu_flop / (ptf * 1e12) and gu_ms > 0:
+        roofline = {"bound": "hbm", "kernel": "gemm_kernel<EPI_SWIGLU> (GateUpGemm+SiluAct, weight-streaming)",
+                    "achieved": gu_bytes / (gu_ms / 1e3) / 1e9, "peak": hbm_pk, "unit": "GB/s",
+                    "frac": gu_bytes / (gu_ms / 1e3) / 1e9 / hbm_pk, "traffic": None,
+                    "peak_source": f"{peak_src} hbm_gbs",
+                    "achieved_tflops": achieved, "frac_tensor_sustained": achieved / ptf if achieved else None,
+                    "timing": stages_src,
+                    "algorithmic": f"2*(2*H*F*active + rows*H + rows*F) = {gu_bytes:.4g} B per step "
+                                   f"({act_me} active experts, {rows_me} rows) over "
+                                   f"{stage_cnt.get('gateup', 0) // prof_n} launch(es)"}
+    else:
+        roofline = None
+    roofline = roofline or {"bound": "tensor", "kernel": "gemm_kernel<EPI_SWIGLU> (GateUpGemm+SiluAct)",
                 "achieved": achieved, "peak": ptf, "unit": "TFLOP/s",
                 "frac": (achieved / ptf) if achieved else None, "traffic": traffic,
                 "peak_source": f"{peak_src} {pkey}",
