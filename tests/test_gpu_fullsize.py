@@ -196,3 +196,58 @@ def test_full_size_ep8_on_one_gpu(name, skew, fp8):
             L.close()
         del layers, ys
         torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("name", ["dsv2_decode", "mixtral_decode"])
+def test_decode_configs_graph_replay_vs_oracle(name):
+    """The decode-regime bench lines (256 tokens, DSv2 / Mixtral dims) in the
+    launch configuration bench.py times them: one forward captured in a CUDA
+    graph with the host-planned plan, replayed.  The replay's y equals an eager
+    forward's y bit for bit; routing stage-wise on all tokens (the oracle's
+    top-k of the GPU's fp32 logits); y on ALL 256 tokens vs oracle.moe_tokens
+    within the north-star tolerance."""
+    c = CONFIGS[name]
+    E, k, H, F, S, Fs, T, norm = c["E"], c["k"], c["H"], c["F"], c["S"], c["Fs"], c["T"], c["norm_topk"]
+    sH, sF = unif_scale(H), unif_scale(F)
+    w = dict(w_router=_gen((E, H), TID_WR, 0, MODE_UNIF, sH), w_gate=_gen((E, F, H), TID_WGATE, 0, MODE_UNIF, sH),
+             w_up=_gen((E, F, H), TID_WUP, 0, MODE_UNIF, sH), w_down=_gen((E, H, F), TID_WDOWN, 0, MODE_UNIF, sF))
+    SF = S * Fs
+    if SF:
+        w.update(ws_gate=_gen((SF, H), TID_WS_GATE, 0, MODE_UNIF, sH), ws_up=_gen((SF, H), TID_WS_UP, 0, MODE_UNIF, sH),
+                 ws_down=_gen((H, SF), TID_WS_DOWN, 0, MODE_UNIF, unif_scale(SF)))
+    x = _gen((T, H), TID_X, 0, MODE_UNIF, unif_scale(1))
+    _spot_check(x, TID_X, 0, MODE_UNIF, unif_scale(1))
+    layer = MoELayer(E, k, H, F, w, S=S, Fs=Fs, max_tokens=T, norm_topk=norm)
+    plan = layer.plan(T)
+    y = torch.empty_like(x)
+    layer.forward(x, y, plan=plan)          # warm-up, as bench.py does before capturing
+    torch.cuda.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        layer.forward(x, y, plan=plan)
+    y.zero_()
+    graph.replay()
+    graph.replay()
+    torch.cuda.synchronize()
+    y_graph = y.clone()
+    d, b = layer.debug_buffers(T)
+    y_eager = layer.forward(x, plan=plan, debug=d)
+    torch.cuda.synchronize()
+    assert torch.equal(y_graph, y_eager)
+    idx_gpu = b["topk_idx"].cpu().numpy()
+    st_idx, st_w = oracle.topk_gating(b["logits"].cpu().numpy(), k, norm)
+    assert np.array_equal(idx_gpu, st_idx)
+    assert np.allclose(b["topk_w"].cpu().numpy(), st_w, rtol=1e-5, atol=0)
+    shared = (_bits(w["ws_gate"]), _bits(w["ws_up"]), _bits(w["ws_down"])) if SF else None
+    cache = {}
+
+    def expert_weights(e):
+        if e not in cache:
+            cache.clear()
+            cache[e] = (_bits(w["w_gate"][e]), _bits(w["w_up"][e]), _bits(w["w_down"][e]))
+        return cache[e]
+    ref = oracle.moe_tokens(_bits(x), _bits(w["w_router"]), expert_weights, k, norm, shared=shared)
+    same = (ref["idx"] == idx_gpu).all(axis=1)
+    assert same.mean() >= 0.97, same.mean()
+    assert_close(y_graph.float().cpu().numpy()[same], ref["y"][same], name)
+    layer.close()
