@@ -196,6 +196,26 @@ def test_layer_parity_grid(name):
     assert L.last_launches() > 0
 
 
+@pytest.mark.parametrize("H,skew", [(1088, 0.0), (2048, 1.0), (5120, 1.0)])
+def test_router_exact_on_grid_large_h_with_bias(H, skew):
+    """Layer-level exact-logit grid check at production-size K (H = 1088: 17
+    k-blocks; 2048; 5120 = DSv2's 80 k-blocks), with and without the skew bias:
+    on the grid every fp32 partial sum is exact, so the GPU's logits equal the
+    oracle's fp32(sum) + beta bit for bit; routing, layout and y as in the grid
+    test above.  (Also the parity gate of the split-K router variant,
+    tools/r02/router_ksplit.patch, measured and dropped: DESIGN §12.)"""
+    E, k = 32, 4
+    inp = Inputs(E=E, k=k, H=H, F=128, T=600, seed=41, grid=True, skew=skew)
+    L, y, b = _run_layer(inp, k, 0)
+    ref = oracle.moe_layer(inp.x, inp.w_router, inp.w_gate, inp.w_up, inp.w_down, k=k, norm_topk=0,
+                           router_bias=inp.router_bias)
+    assert np.array_equal(b["logits"].cpu().numpy(), ref["logits"])
+    assert np.array_equal(b["topk_idx"].cpu().numpy(), ref["idx"])
+    assert np.allclose(b["topk_w"].cpu().numpy(), ref["w"], rtol=1e-5, atol=0)
+    assert np.array_equal(b["pos"].cpu().numpy(), ref["layout"]["pos"][0])
+    assert_close(to_f32(y), ref["y"], f"H={H} skew={skew}")
+
+
 @pytest.mark.parametrize("name", ["mid_shared", "e160_k6"])
 def test_layer_parity_uniform(name):
     kw, k, norm = CASES[name]
