@@ -95,7 +95,7 @@ def peak_tflops(peaks):
 class ClockSampler:
     FIELDS = "timestamp,index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active," \
              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown," \
-             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,power.draw.instant"
 
     def __init__(self, gpu_index):
         self.gpu_index = gpu_index
@@ -142,7 +142,11 @@ class ClockSampler:
         reasons = sorted({n for r in rows for n, v in zip(names, r[5:9]) if v.lower() == "active"})
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
                 "reasons": reasons, "samples": len(rows),
-                "power_w_median": statistics.median([float(r[3]) for r in rows if _isnum(r[3])]) if rows else None}
+                # power.draw is nvidia-smi's 1-second average (it spans the idle time before the
+                # region); power.draw.instant is the sample itself
+                "power_w_median": statistics.median([float(r[3]) for r in rows if _isnum(r[3])]) if rows else None,
+                "power_w_instant_median": statistics.median([float(r[9]) for r in rows if len(r) > 9 and _isnum(r[9])])
+                if any(len(r) > 9 and _isnum(r[9]) for r in rows) else None}
 
 
 def _isnum(s):
