@@ -280,31 +280,61 @@ int LocalTransport::group_start(int) {
   g_->recvs[rank_].clear();
   return 0;
 }
-int LocalTransport::send(const void* buf, size_t bytes, int peer, int, cudaStream_t) {
-  g_->sends[rank_].push_back({buf, nullptr, bytes, peer});
+int LocalTransport::send(const void* buf, size_t bytes, int peer, int channel, cudaStream_t) {
+  g_->sends[rank_].push_back({buf, nullptr, bytes, peer, channel});
   return 0;
 }
-int LocalTransport::recv(void* buf, size_t bytes, int peer, int, cudaStream_t) {
-  g_->recvs[rank_].push_back({nullptr, buf, bytes, peer});
+int LocalTransport::recv(void* buf, size_t bytes, int peer, int channel, cudaStream_t) {
+  g_->recvs[rank_].push_back({nullptr, buf, bytes, peer, channel});
   return 0;
 }
 
-int LocalTransport::group_end(int, cudaStream_t st) {
+int LocalTransport::group_end(int channel, cudaStream_t st) {
   LocalGroup& g = *g_;
   if (int e = cuda_err(cudaEventRecord(g.ev_ready[rank_], st), "cudaEventRecord")) return e;
   g.barrier();  // every rank has posted its ops and recorded its ready event
+  // What NCCL would need to complete this group instead of hanging: every op
+  // on the group's communicator, and per peer as many sends to this rank as
+  // this rank posts receives from it, matched in order with equal sizes.
+  std::string bad;
+  std::vector<size_t> sends_in(g.ep, 0), recvs_from(g.ep, 0);
+  for (int p = 0; p < g.ep; ++p)
+    for (const auto& op : g.sends[p]) {
+      if (op.channel != channel) bad = "send on another communicator in this group";
+      if (op.peer == rank_) ++sends_in[p];
+    }
+  for (const auto& rv : g.recvs[rank_]) {
+    if (rv.channel != channel) bad = "recv on another communicator in this group";
+    ++recvs_from[rv.peer];
+  }
+  for (int p = 0; p < g.ep && bad.empty(); ++p)
+    if (sends_in[p] != recvs_from[p])
+      bad = std::to_string(sends_in[p]) + " sends from rank " + std::to_string(p) + " but " +
+            std::to_string(recvs_from[p]) + " recvs";
   std::vector<size_t> next(g.ep, 0);
   for (const auto& rv : g.recvs[rank_]) {
+    if (!bad.empty()) break;
     // k-th recv from peer p matches p's k-th send to this rank (NCCL p2p order)
     const auto& ps = g.sends[rv.peer];
     size_t& i = next[rv.peer];
     while (i < ps.size() && ps[i].peer != rank_) ++i;
     if (i >= ps.size() || ps[i].bytes != rv.bytes) {
-      set_error("local transport: unmatched recv from rank " + std::to_string(rv.peer));
-      g.barrier();
-      g.barrier();
-      return MOE_ERR_MISMATCH;
+      bad = "unmatched recv from rank " + std::to_string(rv.peer);
+      break;
     }
+    ++i;
+  }
+  if (!bad.empty()) {
+    set_error("local transport (NCCL p2p contract): " + bad);
+    g.barrier();
+    g.barrier();
+    return MOE_ERR_MISMATCH;
+  }
+  std::fill(next.begin(), next.end(), 0);
+  for (const auto& rv : g.recvs[rank_]) {
+    const auto& ps = g.sends[rv.peer];
+    size_t& i = next[rv.peer];
+    while (ps[i].peer != rank_) ++i;
     if (int e = cuda_err(cudaStreamWaitEvent(st, g.ev_ready[rv.peer], 0), "cudaStreamWaitEvent")) return e;
     if (int e = cuda_err(cudaMemcpyAsync(rv.dst, ps[i].src, rv.bytes, cudaMemcpyDeviceToDevice, st),
                          "cudaMemcpyAsync"))

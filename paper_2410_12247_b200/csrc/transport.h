@@ -118,6 +118,7 @@ struct LocalGroup {
     void* dst;
     size_t bytes;
     int peer;
+    int channel;  // communicator (0 dispatch, 1 combine): NCCL matches p2p per communicator
   };
   int ep;
   std::mutex mu;
