@@ -196,28 +196,6 @@ __device__ __forceinline__ void store_chunk(const uint32_t (&pk)[16], uint8_t* s
   stage_flush(stg, out_row0, ldo, vr, lane, tmo, col, row0);
 }
 
-// Linear tile index -> (group, m-tile, n-tile).  Inside a group, tiles are
-// visited in blocks of `gm` m-tiles: n-tile major across the block, m fastest
-// inside it (gm = 1: plain n-fastest order).  Static scheduling only; the
-// dynamic path decodes once per tile in the ticket fetcher (Tickets::fetch).
-template <int CG>
-__device__ __forceinline__ void decode_tile(const SmemTail<CG>& s, int G, int n_tiles, int gm_cfg, int t, int& g,
-                                            int& mt, int& nt) {
-  int lo = 0, hi = G - 1;  // largest g with tile_prefix[g] <= t
-  while (lo < hi) {
-    int mid = (lo + hi + 1) >> 1;
-    if (s.tile_prefix[mid] <= t) lo = mid; else hi = mid - 1;
-  }
-  g = lo;
-  const int local = t - s.tile_prefix[g];
-  const int m_tiles = (s.tile_prefix[g + 1] - s.tile_prefix[g]) / n_tiles;
-  const int blk = local / (gm_cfg * n_tiles);
-  const int within = local - blk * gm_cfg * n_tiles;
-  const int gm = min(gm_cfg, m_tiles - blk * gm_cfg);
-  mt = blk * gm_cfg + within % gm;
-  nt = within / gm;
-}
-
 // floor(a / b) for 0 <= a < 2^23, b >= 1: float reciprocal estimate (off by at
 // most one) and an exact integer correction - a few instructions instead of
 // the ~20-instruction integer division sequence.
@@ -260,15 +238,11 @@ struct Tickets {
   __device__ __forceinline__ void advance() {
     if (++slot == TQ) { slot = 0; phase ^= 1; }
   }
-  __device__ __forceinline__ Tile decode_static(int t) const {
-    Tile d{t, 0, 0, 0, false};
-    if (t >= 0) {
-      decode_tile(*st, G, n_tiles, gm_cfg, t, d.g, d.mt, d.nt);
-      d.half = st->gcount[d.g] - d.mt * Cfg<CG>::TILE_M <= BM;
-    }
-    return d;
-  }
-  // Fetcher's decode: group by the monotone cursor, then the raster with fdiv.
+  // Linear tile index -> (group, m-tile, n-tile).  Inside a group, tiles are
+  // visited in blocks of `gm` m-tiles: n-tile major across the block, m fastest
+  // inside it (gm = 1: plain n-fastest order).  The group comes from a monotone
+  // cursor (the fetcher's tickets, and each role's static tiles, only increase),
+  // the raster from fdiv.
   __device__ __forceinline__ Tile decode_fast(int t) {
     while (st->tile_prefix[gc + 1] <= t) ++gc;
     const int p0 = st->tile_prefix[gc];
@@ -286,9 +260,9 @@ struct Tickets {
   // Fetcher side (one thread): the next tile (t = -1 when done).
   __device__ __forceinline__ Tile fetch() {
     if (!p->dynamic) {
-      int t = static_next;
+      const int t = static_next;
       static_next += num_units;
-      return decode_static(t < total ? t : -1);
+      return t < total ? decode_fast(t) : Tile{-1, 0, 0, 0, false};
     }
     int t = (prefetched == -2) ? atomicAdd(p->tile_counter, 1) : prefetched;
     if (t >= total) t = -1;
@@ -308,10 +282,10 @@ struct Tickets {
   }
   // Consumer side: `arrive` = this thread releases the ticket for its role.
   __device__ __forceinline__ Tile consume(bool arrive) {
-    if (!p->dynamic) {
-      int t = static_next;
+    if (!p->dynamic) {  // static: this role's tiles u, u + U, ... (increasing: the cursor decode holds)
+      const int t = static_next;
       static_next += num_units;
-      return decode_static(t < total ? t : -1);
+      return t < total ? decode_fast(t) : Tile{-1, 0, 0, 0, false};
     }
     if (CG == 2 && rank != 0)
       ptx::mbar_wait_cluster(ptx::smem_u32(&st->qfull[slot]), phase);  // ticket written by the leader (DSMEM)
@@ -859,8 +833,12 @@ int raster_gm(int epi, int N, int K, double rows_hint, int tile_m) {
   }
   return 4;
 }
-int dynamic_sched() {
+// Tile scheduling per epilogue kind: 1 = dynamic tickets, 0 = static round
+// robin.  EPSMOE_DYN_SCHED: 0 all static, 1 all dynamic, 2 dynamic except the
+// DownGemm (EPI_BF16).
+int dynamic_sched(int epi) {
   static int v = env_int("EPSMOE_DYN_SCHED", 1);
+  if (v == 2) return epi == EPI_BF16 ? 0 : 1;
   return v;
 }
 
@@ -972,7 +950,7 @@ int launch_epi(const GemmArgs& a, cudaStream_t stream) {
     p.tma_store = 1;
   // Launches that may run concurrently must use different counters (caller's).
   p.tile_counter = a.tile_counter ? a.tile_counter : ticket_counter(0);
-  p.dynamic = (dynamic_sched() && p.tile_counter) ? 1 : 0;
+  p.dynamic = (dynamic_sched(EPI) && p.tile_counter) ? 1 : 0;
   int grid = a.num_ctas;
   if (!a.row_count) {
     // one dense group (router, shared experts): no more CTAs than tiles - idle
