@@ -70,6 +70,7 @@ struct KParams {
   int K, N, G, m_single, b_group_rows, b_base;
   int raster_gm;  // tile order inside a group: blocks of raster_gm m-tiles, m fastest inside a block
   int dynamic;    // 1: dynamic tile tickets (tile_counter), 0: static round robin
+  int ticket_ahead;  // dynamic: the leader publishes the next tile before loading the current one
   int row_mode;   // 0 all rows, 1 bulk (multiple of 256), 2 remainder (see GemmArgs)
   int diag;       // diagnostics only (EPSMOE_GEMM_DIAG): 1 skip output stores, 2 skip TMEM loads + stores,
                   // 3 bulk stores into a 256-row window (L2-resident: same store traffic, no DRAM writes)
@@ -418,10 +419,22 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
     // GATHER: this lane's A row indices of the tile, A row pitch
     int32_t gidx[GATHER ? BM / 4 : 1];
     const size_t a_pitch = (size_t)p.K * 2;
+    // Dynamic tickets: the leader publishes tile i+1 before it loads tile i, so
+    // the peer's producer and the MMA issuer find the next tile already decoded
+    // at every tile boundary (EPSMOE_TICKET_AHEAD=0: publish when loading it).
+    Tile ahead{-2, 0, 0, 0, false};
     while (true) {
       int4 tv = make_int4(0, 0, 0, 0);
       if (lane == 0) {
-        const Tile d = (rank == 0) ? tk.fetch() : tk.consume(true);
+        Tile d;
+        if (rank != 0) {
+          d = tk.consume(true);
+        } else if (p.dynamic && p.ticket_ahead) {
+          d = (ahead.t == -2) ? tk.fetch() : ahead;
+          if (d.t >= 0) ahead = tk.fetch();
+        } else {
+          d = tk.fetch();
+        }
         tv = make_int4(d.t, d.g, d.mt, d.nt | (d.half ? HALF_BIT : 0));
       }
       if constexpr (GATHER) {
@@ -951,6 +964,8 @@ int launch_epi(const GemmArgs& a, cudaStream_t stream) {
   // Launches that may run concurrently must use different counters (caller's).
   p.tile_counter = a.tile_counter ? a.tile_counter : ticket_counter(0);
   p.dynamic = (dynamic_sched(EPI) && p.tile_counter) ? 1 : 0;
+  static const int ticket_ahead = env_int("EPSMOE_TICKET_AHEAD", 1);
+  p.ticket_ahead = ticket_ahead;
   int grid = a.num_ctas;
   if (!a.row_count) {
     // one dense group (router, shared experts): no more CTAs than tiles - idle
