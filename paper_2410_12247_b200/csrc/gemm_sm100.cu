@@ -52,7 +52,10 @@ constexpr int BK = 64;          // K per stage (one 128 B swizzle atom of bf16)
 constexpr int MAX_G = 256;
 constexpr int NUM_THREADS = 192;  // w0 TMA, w1 MMA + TMEM owner, w2..5 epilogue
 constexpr int TMEM_COLS = 512;    // 2 x 256-column fp32 accumulators
-constexpr int TQ = 4;             // tile-ticket queue depth
+#ifndef EPSMOE_TQ
+#define EPSMOE_TQ 4
+#endif
+constexpr int TQ = EPSMOE_TQ;     // tile-ticket queue depth
 
 template <int CG>
 struct Cfg {
