@@ -154,6 +154,39 @@ np.savez(sys.argv[1], *out)
         assert np.array_equal(a, b)
 
 
+def test_tile_scheduling_is_bit_neutral():
+    """Tile scheduling decides only WHICH CTA pair computes a tile and when, never
+    a sum order: dynamic tickets published a tile ahead (default), published when
+    loaded (EPSMOE_TICKET_AHEAD=0), static round robin for every GEMM
+    (EPSMOE_DYN_SCHED=0) and for the DownGemm only (=2) give bit-identical h-path
+    outputs: the layer's y (routed GEMMs, shared experts, router) on a DSv2-like
+    layer, in a subprocess per setting (the switches are read once per process)."""
+    import subprocess
+    import sys
+    code = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, %r)
+from gen import Inputs
+from tests.gpu_util import layer_from_inputs, dev_bf16
+inp = Inputs(E=32, k=6, H=512, F=256, S=2, Fs=128, T=3000, seed=12)
+L = layer_from_inputs(inp, 6, 0)
+y = L.forward(dev_bf16(inp.x))
+torch.cuda.synchronize()
+np.save(sys.argv[1], y.view(torch.int16).cpu().numpy())
+L.close()
+""" % os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    import tempfile
+    res = []
+    with tempfile.TemporaryDirectory() as td:
+        for i, kv in enumerate([{}, {"EPSMOE_TICKET_AHEAD": "0"}, {"EPSMOE_DYN_SCHED": "0"},
+                                {"EPSMOE_DYN_SCHED": "2"}]):
+            f = os.path.join(td, f"y{i}.npy")
+            subprocess.run([sys.executable, "-c", code, f], check=True, env=dict(os.environ, **kv), timeout=300)
+            res.append(np.load(f))
+    for r in res[1:]:
+        assert np.array_equal(res[0], r)
+
+
 # ---------------------------------------------------------------- full layer (EP = 1)
 
 CASES = {
