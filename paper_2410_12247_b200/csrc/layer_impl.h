@@ -64,6 +64,7 @@ struct moe_layer {
   void *x_dev[2] = {}, *y_dev[2] = {};  // forward_host staging, double-buffered across calls
   void* staging = nullptr;               // their one cudaMalloc (first host-buffer call), freed by destroy
   int hb = 0;                            // staging buffer of the next host call
+  bool host_inflight = false;            // an async host call is queued (cleared by moe_layer_host_sync)
   cudaEvent_t ev_xfree[2] = {}, ev_yfree[2] = {};  // staging buffer b consumed / drained
   // host
   int32_t* ghist_host = nullptr;    // pinned [ep*E]
