@@ -34,6 +34,11 @@ import numpy as np  # noqa: E402
 METRIC = "MoE-layer prefill tokens/s"
 UNIT = "tokens/s"
 FALLBACK_PEAKS = dict(hbm_gbs=6650.0, bf16_tflops=1590.0, bf16_tflops_sustained=1400.0, nvlink_gbs=770.0)
+# The paper's DeepSeek-V2 figures: context only - another machine, the whole 60-layer model, not
+# one MoE layer, so not comparable with this line's value (vs_baseline stays null).
+PAPER_CONTEXT = {"deepseek_v2_prefill_tokens_per_s": {"baseline": 100000, "with_eps_moe": 120000},
+                 "hardware": "8x H800-80GB SXM", "workload": "full DeepSeek-V2 model prefill (60 layers)",
+                 "source": "arXiv 2410.12247, PAPER.md:20, :454", "comparable": False}
 
 
 def parse():
@@ -624,7 +629,8 @@ def ours(args, cfg):
                 "roofline": roofline, "layer_roofline": layer_roofline,
                 "exposed_a2a_ms": stages.get("exposed_a2a", 0.0), "a2a_alone": a2a_alone,
                 "stages_ms": stages, "stages_source": stages_src,
-                "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk}
+                "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk,
+                "paper_context": PAPER_CONTEXT}
         print(json.dumps(line), flush=True)
     layer.close()
     if D > 1:
